@@ -1,0 +1,148 @@
+// CTA-level FP64 DMMA GEMM engine used by every trailing-update tile kernel.
+//
+//   acc(BM x BN) += opA(BM x K) * opB(BN x K)^T
+//
+// Operands are addressed through (ptr, ld, layout):
+//   layout M_MAJOR: element (r, k) at ptr[k*ld + r]   (column-major tile, rows contiguous)
+//   layout K_MAJOR: element (r, k) at ptr[r*ld + k]   (the transpose of a column-major tile)
+// so C -= A*B^T of two column-major tiles is (M_MAJOR, M_MAJOR), C -= A*B is
+// (M_MAJOR, K_MAJOR) and C -= A^T*B is (K_MAJOR, K_MAJOR).
+//
+// Global -> shared staging is a STAGES-deep cp.async (LDGSTS) ring of BK-wide
+// k-slabs; the smem rows are padded by 4 doubles so that the DMMA fragment
+// loads (4 k-rows x 8 consecutive rows per half-warp) hit 32 distinct banks.
+#pragma once
+#include "hg_common.cuh"
+
+namespace hg {
+
+enum Layout { M_MAJOR = 0, K_MAJOR = 1 };
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct GemmCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  static constexpr int FM = WM / 8, FN = WN / 8;  // 8x8 fragments per warp
+  static constexpr int PAD = 4;
+  // smem footprint of one operand slab for each layout
+  static constexpr int slab_mmaj(int rows) { return BK * (rows + PAD); }
+  static constexpr int slab_kmaj(int rows) { return rows * (BK + PAD); }
+};
+
+template <class Cfg, int LA, int LB>
+struct GemmSmem {
+  static constexpr int A_SLAB = LA == M_MAJOR ? Cfg::slab_mmaj(Cfg::BM) : Cfg::slab_kmaj(Cfg::BM);
+  static constexpr int B_SLAB = LB == M_MAJOR ? Cfg::slab_mmaj(Cfg::BN) : Cfg::slab_kmaj(Cfg::BN);
+  static constexpr int DOUBLES = Cfg::STAGES * (A_SLAB + B_SLAB);
+  static constexpr size_t BYTES = size_t(DOUBLES) * sizeof(double);
+};
+
+// Issue the cp.async copies of one (ROWS x BK) slab starting at (r0, k0).
+template <class Cfg, int L, int ROWS>
+HG_DEVICE void load_slab(double* s, const double* __restrict__ g, int ld, int r0, int k0) {
+  constexpr int BK = Cfg::BK, PAD = Cfg::PAD;
+  if constexpr (L == M_MAJOR) {
+    constexpr int CH_PER_K = ROWS / 2;  // 16-byte chunks per k-row
+    constexpr int CHUNKS = BK * CH_PER_K;
+    for (int c = threadIdx.x; c < CHUNKS; c += Cfg::THREADS) {
+      int kk = c / CH_PER_K, rr = (c % CH_PER_K) * 2;
+      cp_async16(s + kk * (ROWS + PAD) + rr, g + size_t(k0 + kk) * ld + r0 + rr);
+    }
+  } else {
+    constexpr int CH_PER_R = BK / 2;
+    constexpr int CHUNKS = ROWS * CH_PER_R;
+    for (int c = threadIdx.x; c < CHUNKS; c += Cfg::THREADS) {
+      int rr = c / CH_PER_R, kk = (c % CH_PER_R) * 2;
+      cp_async16(s + rr * (BK + PAD) + kk, g + size_t(r0 + rr) * ld + k0 + kk);
+    }
+  }
+}
+
+template <class Cfg, int L, int ROWS>
+HG_DEVICE double frag_at(const double* s, int r, int k) {
+  if constexpr (L == M_MAJOR) return s[k * (ROWS + Cfg::PAD) + r];
+  else return s[r * (Cfg::BK + Cfg::PAD) + k];
+}
+
+// Main loop over k in [k_begin, k_end) (multiples of BK). acc[FM][FN][2].
+template <class Cfg, int LA, int LB>
+HG_DEVICE void gemm_mainloop(double (&acc)[Cfg::FM][Cfg::FN][2], double* smem,
+                             const double* __restrict__ A, int lda, int m0,
+                             const double* __restrict__ B, int ldb, int n0,
+                             int k_begin, int k_end) {
+  using SM = GemmSmem<Cfg, LA, LB>;
+  constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
+  double* sA = smem;
+  double* sB = smem + STAGES * SM::A_SLAB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+  const int nk = (k_end - k_begin) / BK;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) {
+      load_slab<Cfg, LA, Cfg::BM>(sA + s * SM::A_SLAB, A, lda, m0, k_begin + s * BK);
+      load_slab<Cfg, LB, Cfg::BN>(sB + s * SM::B_SLAB, B, ldb, n0, k_begin + s * BK);
+    }
+    cp_async_commit();
+  }
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {  // prefetch slab it+STAGES-1 into the ring slot freed last iteration
+      int nxt = it + STAGES - 1;
+      if (nxt < nk) {
+        int slot = nxt % STAGES;
+        load_slab<Cfg, LA, Cfg::BM>(sA + slot * SM::A_SLAB, A, lda, m0, k_begin + nxt * BK);
+        load_slab<Cfg, LB, Cfg::BN>(sB + slot * SM::B_SLAB, B, ldb, n0, k_begin + nxt * BK);
+      }
+      cp_async_commit();
+    }
+    const double* a_s = sA + (it % STAGES) * SM::A_SLAB;
+    const double* b_s = sB + (it % STAGES) * SM::B_SLAB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) af[i] = frag_at<Cfg, LA, Cfg::BM>(a_s, wm + i * 8 + g, kk + t);
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) bf[j] = frag_at<Cfg, LB, Cfg::BN>(b_s, wn + j * 8 + g, kk + t);
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+// Visit every accumulator element with its (row, col) inside the CTA tile.
+template <class Cfg, class F>
+HG_DEVICE void for_each_acc(double (&acc)[Cfg::FM][Cfg::FN][2], F&& f) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) {
+      int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t;
+      f(r, c, acc[i][j][0]);
+      f(r, c + 1, acc[i][j][1]);
+    }
+}
+
+template <class Cfg>
+HG_DEVICE void zero_acc(double (&acc)[Cfg::FM][Cfg::FN][2]) {
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+}  // namespace hg

@@ -1,0 +1,134 @@
+// FP64 peak + DMMA tile-GEMM microbenchmark (run under gpurun).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -I paper_1402_6601_b200/csrc tools/microbench.cu -o tools/microbench
+// Prints one JSON object per measurement.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cmath>
+#include "dgemm_dmma.cuh"
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
+
+__global__ void dmma_peak(double* out, int iters) {
+  double c[16][2];
+  for (int i = 0; i < 16; ++i) c[i][0] = c[i][1] = 0.0;
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) hg::dmma_8x8x4(c[i][0], c[i][1], a, b);
+  }
+  double s = 0;
+  for (int i = 0; i < 16; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) out[0] = s;
+}
+
+__global__ void dfma_peak(double* out, int iters) {
+  double c[16];
+  for (int i = 0; i < 16; ++i) c[i] = threadIdx.x;
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) c[i] = fma(c[i], a, b);
+  }
+  double s = 0;
+  for (int i = 0; i < 16; ++i) s += c[i];
+  if (s == 12345.0) out[0] = s;
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS) gemm_nt_bench(const double* A, const double* B, double* C, int nb) {
+  extern __shared__ double smem[];
+  size_t off = size_t(blockIdx.z) * nb * nb;
+  const double* a = A + off; const double* b = B + off; double* c = C + off;
+  int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
+  double acc[Cfg::FM][Cfg::FN][2];
+  hg::zero_acc<Cfg>(acc);
+  hg::gemm_mainloop<Cfg, hg::M_MAJOR, hg::M_MAJOR>(acc, smem, a, nb, m0, b, nb, n0, 0, nb);
+  hg::for_each_acc<Cfg>(acc, [&](int r, int cc, double v) {
+    size_t idx = size_t(n0 + cc) * nb + m0 + r;
+    c[idx] -= v;
+  });
+}
+
+__global__ void gemm_nt_ref(const double* A, const double* B, double* C, int nb) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i >= nb) return;
+  double s = 0;
+  for (int k = 0; k < nb; ++k) s += A[size_t(k) * nb + i] * B[size_t(k) * nb + j];
+  C[size_t(j) * nb + i] -= s;
+}
+
+__global__ void fill(double* p, size_t n, unsigned seed) {
+  size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  if (i < n) {
+    unsigned x = (unsigned)(i * 2654435761u) ^ seed;
+    x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+    p[i] = (x & 0xffffff) / double(0x1000000) - 0.5;
+  }
+}
+
+template <class Cfg>
+void bench_cfg(const char* name, int nb, int batch) {
+  size_t n = size_t(nb) * nb * batch;
+  double *A, *B, *C, *R;
+  CK(cudaMalloc(&A, n * 8)); CK(cudaMalloc(&B, n * 8)); CK(cudaMalloc(&C, n * 8)); CK(cudaMalloc(&R, n * 8));
+  fill<<<(n + 255) / 256, 256>>>(A, n, 1); fill<<<(n + 255) / 256, 256>>>(B, n, 2);
+  fill<<<(n + 255) / 256, 256>>>(C, n, 3); CK(cudaMemcpy(R, C, n * 8, cudaMemcpyDeviceToDevice));
+  size_t smem = hg::GemmSmem<Cfg, hg::M_MAJOR, hg::M_MAJOR>::BYTES;
+  CK(cudaFuncSetAttribute(gemm_nt_bench<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(nb / Cfg::BM, nb / Cfg::BN, batch);
+  gemm_nt_bench<Cfg><<<grid, Cfg::THREADS, smem>>>(A, B, C, nb);
+  CK(cudaGetLastError());
+  // correctness on batch 0 only
+  gemm_nt_ref<<<dim3((nb + 127) / 128, nb), 128>>>(A, B, R, nb);
+  CK(cudaDeviceSynchronize());
+  std::vector<double> hc(size_t(nb) * nb), hr(size_t(nb) * nb);
+  CK(cudaMemcpy(hc.data(), C, hc.size() * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hr.data(), R, hr.size() * 8, cudaMemcpyDeviceToHost));
+  double md = 0, mx = 0;
+  for (size_t i = 0; i < hc.size(); ++i) { md = fmax(md, fabs(hc[i] - hr[i])); mx = fmax(mx, fabs(hr[i])); }
+  cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  for (int w = 0; w < 3; ++w) gemm_nt_bench<Cfg><<<grid, Cfg::THREADS, smem>>>(A, B, C, nb);
+  int reps = 10;
+  CK(cudaEventRecord(e0));
+  for (int r = 0; r < reps; ++r) gemm_nt_bench<Cfg><<<grid, Cfg::THREADS, smem>>>(A, B, C, nb);
+  CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+  float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
+  double flops = 2.0 * nb * double(nb) * nb * batch * reps;
+  printf("{\"bench\":\"gemm_nt\",\"cfg\":\"%s\",\"nb\":%d,\"batch\":%d,\"smem\":%zu,\"us_per_launch\":%.2f,\"tflops\":%.3f,\"max_abs_err\":%.3e,\"max_ref\":%.3e}\n",
+         name, nb, batch, smem, ms * 1e3 / reps, flops / (ms * 1e-3) / 1e12, md, mx);
+  CK(cudaFree(A)); CK(cudaFree(B)); CK(cudaFree(C)); CK(cudaFree(R));
+}
+
+int main() {
+  cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0));
+  printf("{\"device\":\"%s\",\"sms\":%d,\"cc\":\"%d.%d\"}\n", p.name, p.multiProcessorCount, p.major, p.minor);
+  double* out; CK(cudaMalloc(&out, 8));
+  cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  for (int blocksPerSm : {1, 2, 4}) {
+    int iters = 4096, threads = 256, blocks = p.multiProcessorCount * blocksPerSm;
+    dmma_peak<<<blocks, threads>>>(out, 16);
+    CK(cudaEventRecord(e0)); dmma_peak<<<blocks, threads>>>(out, iters); CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1)); float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
+    double flops = double(blocks) * (threads / 32) * iters * 16 * 512.0;
+    printf("{\"bench\":\"dmma_peak\",\"blocks_per_sm\":%d,\"tflops\":%.3f,\"ms\":%.3f}\n", blocksPerSm, flops / (ms * 1e-3) / 1e12, ms);
+    dfma_peak<<<blocks, threads>>>(out, 16);
+    CK(cudaEventRecord(e0)); dfma_peak<<<blocks, threads>>>(out, iters); CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1)); CK(cudaEventElapsedTime(&ms, e0, e1));
+    flops = double(blocks) * threads * iters * 16 * 2.0;
+    printf("{\"bench\":\"dfma_peak\",\"blocks_per_sm\":%d,\"tflops\":%.3f,\"ms\":%.3f}\n", blocksPerSm, flops / (ms * 1e-3) / 1e12, ms);
+  }
+  using C128 = hg::GemmCfg<128, 128, 16, 64, 32, 3>;
+  using C128w = hg::GemmCfg<128, 128, 16, 32, 64, 3>;
+  using C64 = hg::GemmCfg<64, 64, 16, 32, 32, 3>;
+  using C128x64 = hg::GemmCfg<128, 64, 16, 32, 32, 3>;
+  for (int batch : {1, 8, 32}) {
+    bench_cfg<C128>("128x128x16_w64x32_s3", 1024, batch);
+    bench_cfg<C128w>("128x128x16_w32x64_s3", 1024, batch);
+    bench_cfg<C64>("64x64x16_w32x32_s3", 1024, batch);
+    bench_cfg<C128x64>("128x64x16_w32x32_s3", 1024, batch);
+  }
+  bench_cfg<C128>("128x128x16_w64x32_s3", 512, 32);
+  bench_cfg<C64>("64x64x16_w32x32_s3", 512, 32);
+  return 0;
+}
