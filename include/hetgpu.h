@@ -1,0 +1,204 @@
+/*
+ * hetgpu.h -- C-ABI of libhetgpu.so, the B200-native execution path for the
+ * data-flow tiled FP64 factorizations of arXiv 1402.6601.
+ *
+ * The reference (`hetsim`, pure Python) has no FFI; its execution layer is
+ * the simulator `run(graph, platform, scheduler, model, ...)`
+ * (/root/reference/pkg/src/hetsim/sim.py:388-390) whose task execution call
+ * site is `Simulation._start_exec` (sim.py:353-360, `true_exec`) and whose
+ * planning decisions come from `scheduler.activate` (sim.py:201 ->
+ * sched.py:353-412).  This library replaces:
+ *
+ *   hg_plan_build  <- sim.py:97-385 event loop + sched.py:229-412 (HEFT,
+ *                     DADA) replayed bit-exactly in virtual time
+ *   hg_exec_*      <- sim.py:237-385 transfers + `_start_exec`: the planned
+ *                     DAG executed on B200s (one CUDA graph; cudaMemcpy
+ *                     peer/H2D nodes for transfer jobs, sm_100a tile kernels
+ *                     for tasks)
+ *   hg_tile_run    <- one tile kernel of kernels.py:23-38 (unit-test /
+ *                     calibration entry)
+ *
+ * Conventions: every function returns 0 on success and a negative HG_E*
+ * code otherwise; hg_last_error() returns a thread-local message.  Plain
+ * pointers and sizes only; no torch types.  Not re-entrant per handle.
+ */
+#ifndef HETGPU_H
+#define HETGPU_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HG_ABI_VERSION 1
+
+/* error codes */
+#define HG_OK 0
+#define HG_EINVAL (-1)     /* bad argument / unsupported shape        -> ValueError   */
+#define HG_ECUDA (-2)      /* CUDA runtime error                      -> SimulationError */
+#define HG_ENOTSPD (-3)    /* POTRF met a non-positive pivot          -> SimulationError */
+#define HG_EDEADLOCK (-4)  /* planner: tasks left with no events      -> DeadlockError */
+#define HG_EMODEL (-5)     /* planner: missing timing                 -> PerfModelError */
+#define HG_ESINGULAR (-6)  /* LU met an exactly zero pivot            -> SimulationError */
+
+/* kernel kinds: index in kernels.ALL_KINDS (kernels.py:39-42) */
+enum {
+  HG_KIND_POTRF = 0, HG_KIND_TRSM, HG_KIND_SYRK, HG_KIND_GEMM,
+  HG_KIND_GETRF_INC, HG_KIND_GESSM, HG_KIND_TSTRF, HG_KIND_SSSSM,
+  HG_KIND_GEQRT, HG_KIND_UNMQR, HG_KIND_TSQRT, HG_KIND_TSMQR,
+  HG_KIND_COUNT
+};
+
+/* access modes (graph.py:20-33) */
+#define HG_ACCESS_R 1
+#define HG_ACCESS_W 2
+#define HG_ACCESS_RW 3
+
+const char* hg_last_error(void);
+int hg_abi_version(void);
+/* number of CUDA devices visible (0 on a CPU-only host; never fails) */
+int hg_device_count(void);
+
+/* ------------------------------------------------------------------------
+ * Planner (sim.py:97-385 + sched.py:229-412, noise = 0)
+ * ---------------------------------------------------------------------- */
+typedef struct hg_graph_desc {
+  int32_t n_tasks;
+  int32_t n_blocks;
+  const int32_t* task_kind;   /* index into the model's kind table */
+  const double* task_flops;
+  const int64_t* acc_ptr;     /* CSR [n_tasks + 1] */
+  const int32_t* acc_block;
+  const int8_t* acc_mode;     /* HG_ACCESS_* */
+  const int64_t* succ_ptr;    /* CSR [n_tasks + 1], ascending */
+  const int32_t* succ;
+  const int64_t* block_bytes; /* [n_blocks] */
+} hg_graph_desc;
+
+typedef struct hg_platform_desc {
+  int32_t m, k, n_switches;
+  double link_bandwidth;      /* B/s, every link (build_platform) */
+  double link_latency;        /* s */
+  int32_t switch_slots;       /* Platform.switch_slots, -1 = unlimited */
+  int32_t p2p;
+} hg_platform_desc;
+
+typedef struct hg_model_desc {
+  int32_t n_kinds;
+  const double* fallback_cpu; /* [n_kinds], NaN = missing */
+  const double* fallback_gpu;
+  const int64_t* count_cpu;   /* PerfModel.samples[(kind, cls)][0], -1 if absent */
+  const int64_t* count_gpu;
+  const double* mean_cpu;     /* PerfModel.samples[(kind, cls)][1] */
+  const double* mean_gpu;
+  int64_t sample_threshold;
+} hg_model_desc;
+
+typedef struct hg_sched_desc {
+  int32_t type;               /* 0 = HEFT, 1 = DADA */
+  int32_t with_cp;
+  double alpha, epsilon, rho;
+} hg_sched_desc;
+
+typedef struct hg_plan_out {
+  /* per task [n_tasks] */
+  int32_t* worker;
+  double* start;
+  double* end;
+  int32_t* dispatch;          /* task ids in global dispatch order */
+  int64_t* wait_ptr;          /* [n_tasks + 1] */
+  int32_t* wait_job;
+  /* per transfer job [n_jobs] */
+  int32_t n_jobs;
+  int32_t* job_block;
+  int32_t* job_src;
+  int32_t* job_dst;
+  int32_t* job_version;
+  int32_t* job_src_job;
+  int32_t* job_stage_job;
+  int32_t* job_requester;
+  int64_t* job_bytes;
+  /* totals */
+  int64_t bytes_h2d, bytes_d2h, bytes_d2d;
+  double makespan;
+  double gflops;
+  double* busy;               /* [n_workers] */
+  int32_t n_workers;
+  int32_t n_activations;
+  int32_t n_fallbacks;        /* DADA batches that fell back to HEFT */
+  double plan_seconds;        /* wall time of the planner itself */
+} hg_plan_out;
+
+int hg_plan_build(const hg_graph_desc* g, const hg_platform_desc* p, const hg_model_desc* m,
+                  const hg_sched_desc* s, hg_plan_out* out);
+void hg_plan_free(hg_plan_out* out);
+/* CPython 3.12 builtin sum() over doubles (Neumaier), exposed for parity tests */
+double hg_pysum(const double* x, int64_t n);
+
+/* ------------------------------------------------------------------------
+ * Executor: one CUDA graph per plan (tile kernels + transfer copies)
+ * ---------------------------------------------------------------------- */
+typedef struct hg_exec_plan {
+  int32_t n_tasks, n_blocks, n_jobs, k;
+  int32_t nb, ib;
+  int32_t side_doubles;       /* per-tile side area (IPIV / dL / T), 0 for Cholesky */
+  const int32_t* task_kind;   /* HG_KIND_* */
+  const int32_t* task_node;   /* memory node 1..k */
+  const int64_t* acc_ptr;
+  const int32_t* acc_block;
+  const int64_t* pred_ptr;    /* CSR predecessors */
+  const int32_t* pred;
+  const int32_t* dispatch;
+  const int64_t* wait_ptr;
+  const int32_t* wait_job;
+  const int32_t* job_block;
+  const int32_t* job_src;
+  const int32_t* job_dst;
+  const int32_t* job_version;
+  const int32_t* job_src_job;
+  const int32_t* job_requester;
+  const int64_t* block_bytes; /* host image bytes per block (tile or T factor) */
+  const int32_t* final_writer;/* last writer task per block, -1 = never written */
+} hg_exec_plan;
+
+typedef struct hg_exec_opts {
+  const int32_t* devices;     /* CUDA device of GPU node g+1, [k] */
+  const double* host_in;      /* tile-major image, blocks in id order (pinned for async H2D) */
+  double* host_out;           /* final versions written back here; NULL = no write-back */
+  double* host_side_out;      /* optional: side areas of final tiles, n_blocks*side_doubles */
+  int32_t device_input;       /* 1: keep a replica of host_in in each GPU's HBM and serve
+                                 the plan's H2D jobs from it (inputs resident in HBM) */
+  int32_t reserved;
+} hg_exec_opts;
+
+typedef struct hg_exec hg_exec;
+
+typedef struct hg_exec_stats {
+  double elapsed_ms;          /* device time of the whole graph (CUDA events) */
+  int64_t bytes_h2d;          /* bytes moved by the graph's copy nodes, by direction */
+  int64_t bytes_d2d;
+  int64_t bytes_d2h;          /* incl. final write-back */
+  int64_t bytes_side;         /* side-area bytes that rode along with peer copies */
+  int32_t n_kernel_nodes;
+  int32_t n_copy_nodes;
+} hg_exec_stats;
+
+int hg_exec_create(const hg_exec_plan* plan, const hg_exec_opts* opts, hg_exec** out);
+int hg_exec_run(hg_exec* ex, hg_exec_stats* stats);
+int hg_exec_read_block(hg_exec* ex, int32_t block, int32_t node, double* host, int64_t doubles);
+int hg_exec_destroy(hg_exec* ex);
+
+/* ------------------------------------------------------------------------
+ * One tile kernel on a stream (tests / calibration).  t[] are device
+ * pointers to the task's tiles in access order (kernels.py access lists);
+ * each tile is nb*nb doubles followed by side_doubles of side area.
+ * ---------------------------------------------------------------------- */
+int hg_tile_run(int32_t kind, int32_t device, void* stream, double* const* t, int32_t n_t,
+                int32_t nb, int32_t ib, int32_t* status_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HETGPU_H */

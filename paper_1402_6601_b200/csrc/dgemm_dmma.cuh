@@ -65,12 +65,25 @@ HG_DEVICE double frag_at(const double* s, int r, int k) {
   else return s[r * (Cfg::BK + Cfg::PAD) + k];
 }
 
+// Standard operand loader: a (ROWS x k) window of a tile addressed by layout.
+template <class Cfg, int L, int ROWS>
+struct TileLoader {
+  static constexpr int layout = L;
+  static constexpr int rows = ROWS;
+  const double* p;
+  int ld;
+  int r0;
+  HG_DEVICE void load(double* s, int k0) const { load_slab<Cfg, L, ROWS>(s, p, ld, r0, k0); }
+};
+
 // Main loop over k in [k_begin, k_end) (multiples of BK). acc[FM][FN][2].
-template <class Cfg, int LA, int LB>
+// LdA / LdB are loader functors (TileLoader or a kernel-specific masked
+// loader) exposing `layout`, `rows` and `load(slab, k0)`.
+template <class Cfg, class LdA, class LdB>
 HG_DEVICE void gemm_mainloop(double (&acc)[Cfg::FM][Cfg::FN][2], double* smem,
-                             const double* __restrict__ A, int lda, int m0,
-                             const double* __restrict__ B, int ldb, int n0,
-                             int k_begin, int k_end) {
+                             const LdA& la, const LdB& lb, int k_begin, int k_end) {
+  constexpr int LA = LdA::layout, LB = LdB::layout;
+  static_assert(LdA::rows == Cfg::BM && LdB::rows == Cfg::BN, "loader rows");
   using SM = GemmSmem<Cfg, LA, LB>;
   constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
   double* sA = smem;
@@ -84,8 +97,8 @@ HG_DEVICE void gemm_mainloop(double (&acc)[Cfg::FM][Cfg::FN][2], double* smem,
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) {
-      load_slab<Cfg, LA, Cfg::BM>(sA + s * SM::A_SLAB, A, lda, m0, k_begin + s * BK);
-      load_slab<Cfg, LB, Cfg::BN>(sB + s * SM::B_SLAB, B, ldb, n0, k_begin + s * BK);
+      la.load(sA + s * SM::A_SLAB, k_begin + s * BK);
+      lb.load(sB + s * SM::B_SLAB, k_begin + s * BK);
     }
     cp_async_commit();
   }
@@ -96,8 +109,8 @@ HG_DEVICE void gemm_mainloop(double (&acc)[Cfg::FM][Cfg::FN][2], double* smem,
       int nxt = it + STAGES - 1;
       if (nxt < nk) {
         int slot = nxt % STAGES;
-        load_slab<Cfg, LA, Cfg::BM>(sA + slot * SM::A_SLAB, A, lda, m0, k_begin + nxt * BK);
-        load_slab<Cfg, LB, Cfg::BN>(sB + slot * SM::B_SLAB, B, ldb, n0, k_begin + nxt * BK);
+        la.load(sA + slot * SM::A_SLAB, k_begin + nxt * BK);
+        lb.load(sB + slot * SM::B_SLAB, k_begin + nxt * BK);
       }
       cp_async_commit();
     }

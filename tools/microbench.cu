@@ -43,7 +43,9 @@ __global__ void __launch_bounds__(Cfg::THREADS) gemm_nt_bench(const double* A, c
   int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
   double acc[Cfg::FM][Cfg::FN][2];
   hg::zero_acc<Cfg>(acc);
-  hg::gemm_mainloop<Cfg, hg::M_MAJOR, hg::M_MAJOR>(acc, smem, a, nb, m0, b, nb, n0, 0, nb);
+  hg::TileLoader<Cfg, hg::M_MAJOR, Cfg::BM> la{a, nb, m0};
+  hg::TileLoader<Cfg, hg::M_MAJOR, Cfg::BN> lb{b, nb, n0};
+  hg::gemm_mainloop<Cfg>(acc, smem, la, lb, 0, nb);
   hg::for_each_acc<Cfg>(acc, [&](int r, int cc, double v) {
     size_t idx = size_t(n0 + cc) * nb + m0 + r;
     c[idx] -= v;
