@@ -187,6 +187,10 @@ typedef struct hg_exec_stats {
 
 int hg_exec_create(const hg_exec_plan* plan, const hg_exec_opts* opts, hg_exec** out);
 int hg_exec_run(hg_exec* ex, hg_exec_stats* stats);
+/* asynchronous variant: launch on `stream` (NULL = own stream), then wait */
+int hg_exec_launch(hg_exec* ex, void* stream);
+int hg_exec_wait(hg_exec* ex);
+int hg_exec_info(hg_exec* ex, hg_exec_stats* stats);
 int hg_exec_read_block(hg_exec* ex, int32_t block, int32_t node, double* host, int64_t doubles);
 int hg_exec_destroy(hg_exec* ex);
 
@@ -197,6 +201,11 @@ int hg_exec_destroy(hg_exec* ex);
  * ---------------------------------------------------------------------- */
 int hg_tile_run(int32_t kind, int32_t device, void* stream, double* const* t, int32_t n_t,
                 int32_t nb, int32_t ib, int32_t* status_dev);
+
+/* FP64 roofline denominator: DMMA (mma.sync m8n8k4 f64) throughput of a
+ * register-only kernel filling every SM, in TFLOP/s (MEASURED_PEAKS.json has
+ * no FP64 entry).  Runs ~10 ms on `device`. */
+int hg_fp64_peak(int32_t device, double* dmma_tflops, double* dfma_tflops);
 
 #ifdef __cplusplus
 }

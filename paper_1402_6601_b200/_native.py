@@ -82,7 +82,7 @@ class ExecStats(C.Structure):
 
 EXPORTS = ("hg_last_error", "hg_abi_version", "hg_device_count", "hg_plan_build", "hg_plan_free",
            "hg_pysum", "hg_exec_create", "hg_exec_run", "hg_exec_read_block", "hg_exec_destroy",
-           "hg_tile_run")
+           "hg_tile_run", "hg_exec_launch", "hg_exec_wait", "hg_exec_info", "hg_fp64_peak")
 
 _lib = None
 
@@ -114,8 +114,19 @@ def lib():
     L.hg_exec_destroy.argtypes = [C.c_void_p]
     L.hg_tile_run.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p), C.c_int32,
                               C.c_int32, C.c_int32, C.c_void_p]
+    L.hg_exec_launch.argtypes = [C.c_void_p, C.c_void_p]
+    L.hg_exec_wait.argtypes = [C.c_void_p]
+    L.hg_exec_info.argtypes = [C.c_void_p, C.POINTER(ExecStats)]
+    L.hg_fp64_peak.argtypes = [C.c_int32, _f64p, _f64p]
     _lib = L
     return L
+
+
+def fp64_peak(device: int = 0):
+    """(DMMA, DFMA) FP64 TFLOP/s measured on ``device`` (roofline denominator)."""
+    a, b = C.c_double(), C.c_double()
+    check(lib().hg_fp64_peak(device, C.byref(a), C.byref(b)), "hg_fp64_peak")
+    return a.value, b.value
 
 
 def last_error() -> str:

@@ -152,6 +152,7 @@ struct hg_exec {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   hg_exec_stats stats{};
+  cudaStream_t last_stream = nullptr;
 };
 
 static void release(hg_exec* ex) {
@@ -428,6 +429,60 @@ extern "C" int hg_exec_run(hg_exec* ex, hg_exec_stats* stats) {
     set_error("LU: exactly zero pivot encountered");
     return HG_ESINGULAR;
   }
+  return HG_OK;
+}
+
+// Asynchronous launch on a caller stream (NULL = the executor's own stream);
+// pair with hg_exec_wait.  Lets a caller bracket K back-to-back runs with its
+// own CUDA events.
+extern "C" int hg_exec_launch(hg_exec* ex, void* stream) {
+  if (!ex) {
+    set_error("hg_exec_launch: null handle");
+    return HG_EINVAL;
+  }
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ex->stream;
+  for (int g = 0; g < ex->k; ++g) {
+    HG_CUDA(cudaSetDevice(ex->dev[g]));
+    HG_CUDA(cudaMemsetAsync(ex->status[g], 0, sizeof(int), g == 0 ? s : nullptr));
+  }
+  HG_CUDA(cudaSetDevice(ex->dev[0]));
+  HG_CUDA(cudaGraphLaunch(ex->exec, s));
+  ex->last_stream = s;
+  return HG_OK;
+}
+
+extern "C" int hg_exec_wait(hg_exec* ex) {
+  if (!ex) {
+    set_error("hg_exec_wait: null handle");
+    return HG_EINVAL;
+  }
+  HG_CUDA(cudaSetDevice(ex->dev[0]));
+  HG_CUDA(cudaStreamSynchronize(ex->last_stream ? ex->last_stream : ex->stream));
+  int bad = 0;
+  for (int g = 0; g < ex->k; ++g) {
+    int st = 0;
+    HG_CUDA(cudaSetDevice(ex->dev[g]));
+    HG_CUDA(cudaMemcpy(&st, ex->status[g], sizeof(int), cudaMemcpyDeviceToHost));
+    bad |= st;
+  }
+  HG_CUDA(cudaSetDevice(ex->dev[0]));
+  if (bad & 1) {
+    set_error("POTRF: matrix is not positive definite (non-positive pivot)");
+    return HG_ENOTSPD;
+  }
+  if (bad & 2) {
+    set_error("LU: exactly zero pivot encountered");
+    return HG_ESINGULAR;
+  }
+  return HG_OK;
+}
+
+extern "C" int hg_exec_info(hg_exec* ex, hg_exec_stats* stats) {
+  if (!ex || !stats) {
+    set_error("hg_exec_info: bad arguments");
+    return HG_EINVAL;
+  }
+  *stats = ex->stats;
   return HG_OK;
 }
 

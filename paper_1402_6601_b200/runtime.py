@@ -151,6 +151,20 @@ class Executor:
         return ExecStats(st.elapsed_ms, st.bytes_h2d, st.bytes_d2d, st.bytes_d2h, st.bytes_side,
                          st.n_kernel_nodes, st.n_copy_nodes)
 
+    def launch(self, stream: int | None = None):
+        """Enqueue one run on ``stream`` (a cudaStream_t as int; None = own stream)."""
+        _native.check(_native.lib().hg_exec_launch(self._h, C.c_void_p(stream) if stream else None),
+                      "hg_exec_launch")
+
+    def wait(self):
+        _native.check(_native.lib().hg_exec_wait(self._h), "hg_exec_wait")
+
+    def info(self) -> ExecStats:
+        st = _native.ExecStats()
+        _native.check(_native.lib().hg_exec_info(self._h, C.byref(st)), "hg_exec_info")
+        return ExecStats(st.elapsed_ms, st.bytes_h2d, st.bytes_d2d, st.bytes_d2h, st.bytes_side,
+                         st.n_kernel_nodes, st.n_copy_nodes)
+
     def read_block(self, block: int, node: int, doubles: int) -> np.ndarray:
         out = np.empty(doubles, np.float64)
         _native.check(_native.lib().hg_exec_read_block(self._h, block, node, _native.ptr(out, C.c_double),
