@@ -1,0 +1,399 @@
+"""Benchmark: tiled FP64 GFLOP/s and NVLink bytes moved, DADA vs HEFT (BASELINE.json).
+
+Default workload (N=1): BASELINE configs[1] -- tiled Cholesky N=32768, nb=1024,
+FP64, DADA(alpha=0.5)+CP vs HEFT, planned by the bit-exact native planner
+with the measured B200 cost model (timings/b200_nb1024_ib128.csv) and
+executed on the GPU as one CUDA graph of sm_100a tile kernels.
+
+A "step" is one full factorization of the synthetic SPD matrix.
+  value : GFLOP/s with the input image resident in HBM (the plan's H2D jobs
+          are served from a device replica of the host image)
+  e2e   : GFLOP/s through the public API with HOST buffers: the plan's H2D
+          jobs read pinned host memory and the factor is written back to
+          pinned host memory, both inside the timed region.
+Timing: W untimed warm-up steps, then K steps bracketed by barrier +
+cudaDeviceSynchronize, CUDA events on the launching stream, max over ranks.
+Inputs (4.4 GB of tiles) exceed L2 (126 MB), so no explicit flush.
+
+``--impl reference`` times the reference's CPU path (the oracle's tile DAG
+on the host's cores, oracle/cpu_exec.py) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tiled FP64 GFLOP/s and NVLink bytes moved, DADA vs HEFT"
+NVLINK_BW = 7.7e11   # measured peer copy B/s per direction (B200_PROFILING.md)
+NVLINK_LAT = 3e-6
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--family", default="cholesky")
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--nb", type=int, default=1024)
+    ap.add_argument("--ib", type=int, default=128)
+    ap.add_argument("--alpha", type=float, default=0.5)
+    ap.add_argument("--timings", default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-n", type=int, default=16384, help="CPU baseline sample order")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_model(H, args):
+    path = args.timings or os.path.join(ROOT, "timings", f"b200_nb{args.nb}_ib{args.ib}.csv")
+    if os.path.exists(path):
+        return H.PerfModel(H.load_timing_table(path)), os.path.relpath(path, ROOT)
+    return H.PerfModel(H.default_timing_table(args.nb, args.ib)), "hetsim default synthetic table"
+
+
+# -- clocks ----------------------------------------------------------------------
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"hg_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.dev), "-lms", "200"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -- inputs ----------------------------------------------------------------------
+
+def make_input(graph, n, nb, seed, torch):
+    """Synthetic SPD (R + R^T)/2 + n I, R ~ U(-0.5, 0.5) (torch Philox on the GPU),
+    written tile-major into pinned host memory."""
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    R = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=gen) - 0.5
+    A = (R + R.T) * 0.5
+    del R
+    A.diagonal().add_(float(n))
+    count = sum(graph.sizes) // 8
+    img = torch.empty(count, dtype=torch.float64, pin_memory=True)
+    off = 0
+    lay = graph.layout
+    for d, size in enumerate(graph.sizes):
+        c = size // 8
+        i, j = lay.tiles[d]
+        # column-major tile = row-major transpose
+        img[off:off + c].copy_(A[i * nb:(i + 1) * nb, j * nb:(j + 1) * nb].T.contiguous().view(-1))
+        off += c
+    del A
+    torch.cuda.empty_cache()
+    return img
+
+
+def factor_check(graph, img_in, img_out, nb, seed=5):
+    """Randomised residual ||A x - L (L^T x)|| / ||A x|| from the tile images (O(n^2))."""
+    lay = graph.layout
+    nt = lay.nt
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(lay.n)
+    offs = np.cumsum([0] + [s // 8 for s in graph.sizes])
+    ax = np.zeros(lay.n)
+    y = np.zeros(lay.n)
+    tiles_in, tiles_out = {}, {}
+    for d, (i, j) in lay.tiles.items():
+        tiles_in[(i, j)] = img_in[offs[d]:offs[d + 1]].reshape(nb, nb, order="F")
+        tiles_out[(i, j)] = img_out[offs[d]:offs[d + 1]].reshape(nb, nb, order="F")
+    for (i, j), a in tiles_in.items():
+        xi, xj = x[i * nb:(i + 1) * nb], x[j * nb:(j + 1) * nb]
+        if i == j:
+            low = np.tril(a)
+            sym = low + np.tril(a, -1).T
+            ax[i * nb:(i + 1) * nb] += sym @ xi
+        else:
+            ax[i * nb:(i + 1) * nb] += a @ xj
+            ax[j * nb:(j + 1) * nb] += a.T @ xi
+    for (i, j), l in tiles_out.items():
+        lt = np.tril(l) if i == j else l
+        y[j * nb:(j + 1) * nb] += lt.T @ x[i * nb:(i + 1) * nb]
+    z = np.zeros(lay.n)
+    for (i, j), l in tiles_out.items():
+        lt = np.tril(l) if i == j else l
+        z[i * nb:(i + 1) * nb] += lt @ y[j * nb:(j + 1) * nb]
+    return float(np.linalg.norm(ax - z) / np.linalg.norm(ax)), nt
+
+
+def gemm_kernel_time(torch, nb, reps=30):
+    """Average duration of the dominant kernel (GEMM tile, C -= A B^T), back-to-back
+    launches through the C-ABI on torch's current stream, CUDA events."""
+    import ctypes as C
+
+    from paper_1402_6601_b200 import _native
+
+    ts = [torch.rand(nb * nb, dtype=torch.float64, device="cuda") - 0.5 for _ in range(3)]
+    ptrs = (C.c_void_p * 3)(*[t.data_ptr() for t in ts])
+    st = torch.cuda.current_stream()
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    L = _native.lib()
+
+    def go():
+        _native.check(L.hg_tile_run(3, torch.cuda.current_device(), C.c_void_p(st.cuda_stream), ptrs, 3, nb, 0,
+                                    C.c_void_p(status.data_ptr())), "hg_tile_run")
+
+    for _ in range(3):
+        go()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        go()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e-3
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the GEMM tile kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "gemm_tile_ncu.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            return None
+    return None
+
+
+def cpu_baseline_sample(n, nb):
+    from oracle import cpu_exec
+
+    threads = cpu_exec.host_threads()
+    secs, flops, res = cpu_exec.cholesky_sample(n, nb, threads)
+    return {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"tiled Cholesky N={n} nb={nb} (oracle SciPy/OpenBLAS tile kernels, {threads} host threads, "
+                      f"1 BLAS thread each), {secs:.2f} s, residual {res:.1e}"}
+
+
+# -- arms ------------------------------------------------------------------------
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import cpu_exec
+
+    threads = cpu_exec.host_threads()
+    n = min(args.cpu_n, args.n) // 2 if args.n >= 2 * args.nb else args.n
+    n = max(n, args.nb)
+    for _ in range(args.warmup):
+        cpu_exec.cholesky_sample(n, args.nb, threads)
+    secs = []
+    flops = 0.0
+    for _ in range(args.steps):
+        s, flops, res = cpu_exec.cholesky_sample(n, args.nb, threads)
+        secs.append(s)
+    ms = float(np.mean(secs)) * 1e3
+    val = flops / (ms * 1e-3) / 1e9
+    sample = (f"tiled Cholesky N={n} nb={args.nb} per step (bounded sample of the N={args.n} workload): "
+              f"oracle SciPy/OpenBLAS tile kernels on {threads} host threads, dynamic DAG list scheduling")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"tiled {args.family} N={args.n} nb={args.nb}", "family": args.family,
+                   "n": args.n, "nb": args.nb, "sample_n": n},
+        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    import paper_1402_6601_b200 as H
+    from paper_1402_6601_b200 import _native, runtime
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    k = world
+    n, nb = args.n, args.nb
+    g = H.gen_cholesky(n // nb, nb)
+    plat = H.build_platform(k, k, k, link_bandwidth=NVLINK_BW, link_latency=NVLINK_LAT,
+                            switch_cap=math.inf, p2p=True)
+    model, model_src = load_model(H, args)
+    flops = H.flops_of("cholesky", n)
+    plans = {}
+    plan_wall = {}
+    for name, sch in (("dada", H.make_scheduler("dada", alpha=args.alpha, cp=True)), ("heft", H.make_scheduler("heft"))):
+        t0 = time.perf_counter()
+        plans[name] = H.make_plan(g, plat, sch, model)
+        plan_wall[name] = time.perf_counter() - t0
+    if k > 1:
+        raise SystemExit("multi-GPU execution: run one process per GPU is not wired in this build yet")
+
+    dmma_peak, dfma_peak = _native.fp64_peak(local)
+    img = make_input(g, n, nb, 0, torch)
+    host_in = img.numpy()
+    stream = torch.cuda.current_stream()
+
+    def timed(ex, steps, warmup):
+        for _ in range(warmup):
+            ex.launch(stream.cuda_stream)
+            ex.wait()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(steps):
+            ex.launch(stream.cuda_stream)
+        e1.record(stream)
+        ex.wait()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        return e0.elapsed_time(e1) / steps, wall / steps * 1e3
+
+    results = {}
+    clocks = None
+    for name in ("dada", "heft"):
+        plan = plans[name]
+        if name == "heft" and np.array_equal(plan.worker, plans["dada"].worker) and \
+                plan.bytes_d2d == plans["dada"].bytes_d2d and plan.bytes_h2d == plans["dada"].bytes_h2d:
+            results[name] = dict(results["dada"], same_plan_as_dada=True)
+            continue
+        ex = runtime.Executor(g, plat, plan, host_in, None, devices=[local], device_input=True)
+        info = ex.info()
+        if name == "dada":
+            with ClockSampler(local) as cs:
+                ms, wall_ms = timed(ex, args.steps, args.warmup)
+            clocks = cs.summary()
+        else:
+            ms, wall_ms = timed(ex, args.steps, args.warmup)
+        results[name] = {"ms_per_step": ms, "gflops": flops / (ms * 1e-3) / 1e9,
+                         "bytes_d2d": plan.bytes_d2d, "bytes_h2d": plan.bytes_h2d,
+                         "kernel_nodes": info.n_kernel_nodes, "copy_nodes": info.n_copy_nodes,
+                         "plan_seconds": plan_wall[name], "plan_makespan_s": plan.makespan,
+                         "dada_fallbacks": plan.n_fallbacks}
+        ex.close()
+        del ex
+        torch.cuda.empty_cache()
+
+    e2e = None
+    check = None
+    if not args.no_e2e:
+        out = torch.empty_like(img, pin_memory=True)
+        ex = runtime.Executor(g, plat, plans["dada"], host_in, out.numpy(), devices=[local], device_input=False)
+        ms_e2e, wall_e2e = timed(ex, max(1, min(args.steps, 3)), 1)
+        info = ex.info()
+        ex.close()
+        e2e = {"value": flops / (wall_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(info.bytes_h2d), "d2h_bytes_per_step": int(info.bytes_d2h),
+               "device_ms_per_step": ms_e2e, "wall_ms_per_step": wall_e2e}
+        relres, _ = factor_check(g, host_in, out.numpy(), nb)
+        check = {"randomized_relres": relres, "ok": bool(relres < 1e-12)}
+
+    t_gemm = gemm_kernel_time(torch, nb)
+    achieved = 2.0 * nb ** 3 / t_gemm / 1e12
+    roofline = {"bound": "tensor", "kernel": "k_gemm_nt (GEMM tile C -= A*B^T, DMMA)",
+                "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s", "frac": achieved / dmma_peak,
+                "traffic": ncu_traffic(),
+                "peak_source": "FP64 DMMA microbenchmark measured in this run (hg_fp64_peak; "
+                               "MEASURED_PEAKS.json has no FP64 entry)",
+                "dfma_peak": dfma_peak,
+                "step_frac": (flops / (results["dada"]["ms_per_step"] * 1e-3) / 1e12) / dmma_peak,
+                "gemm_launch_us": t_gemm * 1e6}
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        cpu = cpu_baseline_sample(args.cpu_n, nb)
+    d = results["dada"]
+    line = {
+        "metric": METRIC, "value": d["gflops"], "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": d["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"tiled Cholesky N={n} nb={nb} FP64 (BASELINE configs[1])", "family": "cholesky",
+                   "n": n, "nb": nb, "scheduler": f"DADA(alpha={args.alpha})+CP vs HEFT", "k": k,
+                   "cost_model": model_src, "l2": "inputs (tiles) > L2, no flush"},
+        "nvlink_bytes": {"dada": d["bytes_d2d"], "heft": results["heft"]["bytes_d2d"]},
+        "h2d_bytes": {"dada": d["bytes_h2d"], "heft": results["heft"]["bytes_h2d"]},
+        "heft": {"value": results["heft"]["gflops"], "ms_per_step": results["heft"]["ms_per_step"],
+                 "same_plan_as_dada": bool(results["heft"].get("same_plan_as_dada", False))},
+        "plan": {"dada_seconds": plan_wall["dada"], "heft_seconds": plan_wall["heft"],
+                 "dada_fallbacks": d["dada_fallbacks"], "planner": "native bit-exact (hg_plan_build)"},
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+        "gpu_launches": d["kernel_nodes"] * args.steps, "check": check,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
