@@ -295,13 +295,15 @@ def run_ours(args, rank, world, local):
     dmma_peak, dfma_peak = _native.fp64_peak(local)
     img = make_input(g, n, nb, 0, torch)
     host_in = img.numpy()
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real stream: events and graph launches on the same handle
 
     def timed(ex, steps, warmup):
         for _ in range(warmup):
             ex.launch(stream.cuda_stream)
             ex.wait()
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         w0 = time.perf_counter()
         e0.record(stream)

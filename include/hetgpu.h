@@ -187,7 +187,7 @@ typedef struct hg_exec_stats {
 
 int hg_exec_create(const hg_exec_plan* plan, const hg_exec_opts* opts, hg_exec** out);
 int hg_exec_run(hg_exec* ex, hg_exec_stats* stats);
-/* asynchronous variant: launch on `stream` (NULL = own stream), then wait */
+/* asynchronous variant: launch on exactly `stream` (NULL = legacy default stream), then wait */
 int hg_exec_launch(hg_exec* ex, void* stream);
 int hg_exec_wait(hg_exec* ex);
 int hg_exec_info(hg_exec* ex, hg_exec_stats* stats);

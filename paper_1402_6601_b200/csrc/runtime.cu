@@ -47,6 +47,14 @@ bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
 bool init_qr_attributes();
 bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out);
 
+int chol_scratch_ints(int kind, int nb);
+
+int task_scratch_ints(int kind, int nb, int ib) {
+  (void)ib;
+  if (kind >= K_POTRF && kind <= K_GEMM) return chol_scratch_ints(kind, nb);
+  return 0;
+}
+
 bool init_kernel_attributes() {
   return init_chol_attributes() && init_lu_attributes() && init_qr_attributes();
 }
@@ -74,6 +82,7 @@ using namespace hg;
 
 static std::once_flag g_attr_once[64];
 static bool g_attr_ok[64];
+static std::string g_attr_msg[64];
 
 static int ensure_attributes(int dev) {
   if (dev < 0 || dev >= 64) {
@@ -85,10 +94,11 @@ static int ensure_attributes(int dev) {
     cudaGetDevice(&prev);
     cudaSetDevice(dev);
     g_attr_ok[dev] = init_kernel_attributes();
+    if (!g_attr_ok[dev]) g_attr_msg[dev] = g_err;
     cudaSetDevice(prev);
   });
   if (!g_attr_ok[dev]) {
-    set_error("cudaFuncSetAttribute failed on device %d", dev);
+    set_error("kernel attribute setup failed on device %d: %s", dev, g_attr_msg[dev].c_str());
     return HG_ECUDA;
   }
   return HG_OK;
@@ -123,6 +133,23 @@ int hg_tile_run(int32_t kind, int32_t device, void* stream, double* const* t, in
   ops.nb = nb;
   ops.ib = ib;
   ops.status = status_dev;
+  // per-device scratch for hg_tile_run (flags are self-advancing; calls on one
+  // device must not overlap in time)
+  static int* scratch[64] = {nullptr};
+  static std::mutex scratch_mu;
+  const int need = task_scratch_ints(kind, nb, ib);
+  if (need > 0) {
+    std::lock_guard<std::mutex> lk(scratch_mu);
+    if (!scratch[device]) {
+      HG_CUDA(cudaMalloc(&scratch[device], size_t(1 << 16) * sizeof(int)));
+      HG_CUDA(cudaMemset(scratch[device], 0, size_t(1 << 16) * sizeof(int)));
+    }
+    if (need > (1 << 16)) {
+      set_error("hg_tile_run: scratch too small");
+      return HG_EINVAL;
+    }
+    ops.scratch = scratch[device];
+  }
   std::vector<LaunchDesc> launches;
   if (!build_task_launches(kind, ops, launches)) return HG_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -143,6 +170,7 @@ struct hg_exec {
   std::vector<double*> pool;            // per GPU node
   std::vector<double*> replica;         // per GPU node: device copy of host_in (device_input)
   std::vector<int*> status;             // per GPU node
+  std::vector<int*> scratch;            // per GPU node: per-task scratch ints
   std::vector<std::vector<int64_t>> slot;  // [node-1][block] -> offset in doubles, -1 = none
   std::vector<int64_t> host_off;        // doubles offset of each block in the host image
   std::vector<int64_t> blk_doubles;     // host-image doubles per block
@@ -153,6 +181,7 @@ struct hg_exec {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   hg_exec_stats stats{};
   cudaStream_t last_stream = nullptr;
+  bool launched = false;
 };
 
 static void release(hg_exec* ex) {
@@ -164,6 +193,7 @@ static void release(hg_exec* ex) {
     if (g < (int)ex->pool.size() && ex->pool[g]) cudaFree(ex->pool[g]);
     if (g < (int)ex->replica.size() && ex->replica[g]) cudaFree(ex->replica[g]);
     if (g < (int)ex->status.size() && ex->status[g]) cudaFree(ex->status[g]);
+    if (g < (int)ex->scratch.size() && ex->scratch[g]) cudaFree(ex->scratch[g]);
   }
   if (ex->ev0) cudaEventDestroy(ex->ev0);
   if (ex->ev1) cudaEventDestroy(ex->ev1);
@@ -182,6 +212,7 @@ static int build_graph(hg_exec* ex, const hg_exec_plan* P, const hg_exec_opts* O
   std::vector<LaunchDesc> launches;
   std::vector<cudaGraphNode_t> deps;
   int64_t side_bytes = 0;
+  std::vector<int64_t> scratch_used(ex->k, 0);
 
   auto slot_ptr = [&](int node, int block) -> double* {
     int64_t off = ex->slot[node - 1][block];
@@ -233,6 +264,11 @@ static int build_graph(hg_exec* ex, const hg_exec_plan* P, const hg_exec_opts* O
     ops.nb = ex->nb;
     ops.ib = ex->ib;
     ops.status = ex->status[node - 1];
+    const int sc = task_scratch_ints(P->task_kind[t], ex->nb, ex->ib);
+    if (sc > 0) {
+      ops.scratch = ex->scratch[node - 1] + scratch_used[node - 1];
+      scratch_used[node - 1] += sc;
+    }
     const int64_t a0 = P->acc_ptr[t], a1 = P->acc_ptr[t + 1];
     if (a1 - a0 > 4) {
       set_error("task %d has %lld accesses (max 4)", t, (long long)(a1 - a0));
@@ -314,6 +350,7 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
   ex->pool.assign(P->k, nullptr);
   ex->replica.assign(P->k, nullptr);
   ex->status.assign(P->k, nullptr);
+  ex->scratch.assign(P->k, nullptr);
   const int64_t tile_d = int64_t(P->nb) * P->nb;
   ex->host_off.resize(P->n_blocks);
   ex->blk_doubles.resize(P->n_blocks);
@@ -369,6 +406,17 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
       break;
     }
     cudaMemset(ex->status[g], 0, sizeof(int));
+    int64_t sc = 0;
+    for (int t = 0; t < P->n_tasks; ++t)
+      if (P->task_node[t] == g + 1) sc += task_scratch_ints(P->task_kind[t], P->nb, P->ib);
+    if (sc > 0) {
+      if (cudaMalloc(&ex->scratch[g], size_t(sc) * sizeof(int)) != cudaSuccess ||
+          cudaMemset(ex->scratch[g], 0, size_t(sc) * sizeof(int)) != cudaSuccess) {
+        set_error("scratch allocation failed on device %d", ex->dev[g]);
+        rc = HG_ECUDA;
+        break;
+      }
+    }
     if (O->device_input) {
       if (cudaMalloc(&ex->replica[g], size_t(host_total) * 8) != cudaSuccess ||
           cudaMemcpy(ex->replica[g], O->host_in, size_t(host_total) * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -432,15 +480,15 @@ extern "C" int hg_exec_run(hg_exec* ex, hg_exec_stats* stats) {
   return HG_OK;
 }
 
-// Asynchronous launch on a caller stream (NULL = the executor's own stream);
-// pair with hg_exec_wait.  Lets a caller bracket K back-to-back runs with its
-// own CUDA events.
+// Asynchronous launch on exactly the caller's stream (NULL = the legacy
+// default stream); pair with hg_exec_wait.  Lets a caller bracket K
+// back-to-back runs with its own CUDA events on that stream.
 extern "C" int hg_exec_launch(hg_exec* ex, void* stream) {
   if (!ex) {
     set_error("hg_exec_launch: null handle");
     return HG_EINVAL;
   }
-  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ex->stream;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int g = 0; g < ex->k; ++g) {
     HG_CUDA(cudaSetDevice(ex->dev[g]));
     HG_CUDA(cudaMemsetAsync(ex->status[g], 0, sizeof(int), g == 0 ? s : nullptr));
@@ -448,6 +496,7 @@ extern "C" int hg_exec_launch(hg_exec* ex, void* stream) {
   HG_CUDA(cudaSetDevice(ex->dev[0]));
   HG_CUDA(cudaGraphLaunch(ex->exec, s));
   ex->last_stream = s;
+  ex->launched = true;
   return HG_OK;
 }
 
@@ -457,7 +506,8 @@ extern "C" int hg_exec_wait(hg_exec* ex) {
     return HG_EINVAL;
   }
   HG_CUDA(cudaSetDevice(ex->dev[0]));
-  HG_CUDA(cudaStreamSynchronize(ex->last_stream ? ex->last_stream : ex->stream));
+  HG_CUDA(cudaStreamSynchronize(ex->launched ? ex->last_stream : ex->stream));
+  ex->launched = false;
   int bad = 0;
   for (int g = 0; g < ex->k; ++g) {
     int st = 0;

@@ -38,7 +38,12 @@ struct TaskOperands {
   int nb = 0;
   int ib = 0;
   int* status = nullptr;  // device word; kernels OR error bits into it
+  int* scratch = nullptr; // per-task device ints (task_scratch_ints), zero-initialised once;
+                          // kernels keep them self-consistent across runs
 };
+
+// Device ints of per-task scratch a kind needs (0 for most kinds).
+int task_scratch_ints(int kind, int nb, int ib);
 
 // Kind ids == index in kernels.ALL_KINDS == HG_KIND_* in include/hetgpu.h
 enum Kind {

@@ -5,18 +5,22 @@
 //
 //   GEMM  A_ij -= A_ik * A_jk^T            k_gemm_nt (full)      DMMA 64x64 CTA tiles
 //   SYRK  A_ii -= A_ik * A_ik^T  (lower)   k_gemm_nt (lower)     DMMA, upper CTAs exit
-//   TRSM  A_ik  = A_ik * L_kk^-T           k_trsm_rows           row strips, DMMA updates
-//   POTRF A_kk  = L_kk (lower)             r=64 blocked right-looking chain:
-//                                          k_potrf_diag -> k_trsm_rows -> k_gemm_nt(lower)
+//   TRSM  A_ik  = A_ik * L_kk^-T           k_trsm_wave           2-D wavefront, DMMA updates
+//   POTRF A_kk  = L_kk (lower)             k_potrf_cluster: one 16-CTA cluster kernel,
+//                                          r=64 right-looking blocked, lookahead diag
 //
 // POTRF leaves inv(L_JJ)^T of each 64x64 diagonal block in that block's
 // strict upper triangle (the upper triangle of a Cholesky tile is never read
 // by any other kind), so TRSM applies the diagonal-block inverses with DMMA
 // instead of running a scalar substitution.  The upper triangle of diagonal
 // tiles is therefore workspace, not input, after POTRF.
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include "dgemm_dmma.cuh"
 #include "tiles.h"
+
+namespace cg = cooperative_groups;
 
 namespace hg {
 
@@ -55,29 +59,24 @@ __global__ void __launch_bounds__(CfgG::THREADS) k_gemm_nt(GemmNTParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// Unblocked Cholesky of the 64x64 diagonal block at (j0, j0) + inverse.
-// Writes L (lower) and inv(L)^T into the strict upper triangle of the block.
-struct PotrfDiagParams {
-  double* A;
-  int ld, j0;
-  int* status;
-};
-
-__global__ void __launch_bounds__(256) k_potrf_diag(PotrfDiagParams p) {
-  __shared__ double s[kR][kR + 1];  // s[col][row]
-  __shared__ double inv_diag[kR];
-  double* blk = p.A + size_t(p.j0) * p.ld + p.j0;
+// Unblocked Cholesky of the 64x64 diagonal block at (j0, j0) + its inverse,
+// by one CTA of NT threads.  Writes L (lower) and inv(L)^T into the strict
+// upper triangle of the block.  s is a [kR][kR+1] smem scratch (s[col][row]).
+template <int NT>
+__device__ void diag_factor_inverse(double* A, int ld, int j0, int* status, double (*s)[kR + 1],
+                                    double* inv_diag) {
+  double* blk = A + size_t(j0) * ld + j0;
   const int tid = threadIdx.x;
-  for (int e = tid; e < kR * kR; e += blockDim.x) {
+  for (int e = tid; e < kR * kR; e += NT) {
     int c = e / kR, r = e % kR;
-    s[c][r] = blk[size_t(c) * p.ld + r];
+    s[c][r] = __ldcg(blk + size_t(c) * ld + r);
   }
   __syncthreads();
   for (int j = 0; j < kR; ++j) {
     if (tid == 0) {
       double d = s[j][j];
       if (!(d > 0.0)) {
-        if (p.status) atomicOr(p.status, 1);  // not positive definite
+        if (status) atomicOr(status, 1);  // not positive definite
         d = 1.0;
       }
       d = sqrt(d);
@@ -86,20 +85,19 @@ __global__ void __launch_bounds__(256) k_potrf_diag(PotrfDiagParams p) {
     }
     __syncthreads();
     const double rd = inv_diag[j];
-    for (int i = j + 1 + tid; i < kR; i += blockDim.x) s[j][i] *= rd;
+    for (int i = j + 1 + tid; i < kR; i += NT) s[j][i] *= rd;
     __syncthreads();
     // trailing update of columns c in (j, kR): s[c][i] -= s[j][i] * s[j][c], i >= c
     const int w = kR - j - 1;
-    for (int e = tid; e < w * w; e += blockDim.x) {
+    for (int e = tid; e < w * w; e += NT) {
       int c = j + 1 + e / w, i = j + 1 + e % w;
       if (i >= c) s[c][i] -= s[j][i] * s[j][c];
     }
     __syncthreads();
   }
-  // write L back (lower incl. diagonal)
-  for (int e = tid; e < kR * kR; e += blockDim.x) {
+  for (int e = tid; e < kR * kR; e += NT) {
     int c = e / kR, r = e % kR;
-    if (r >= c) blk[size_t(c) * p.ld + r] = s[c][r];
+    if (r >= c) blk[size_t(c) * ld + r] = s[c][r];
   }
   // inverse, one column per thread: L x = e_c (forward substitution)
   if (tid < kR) {
@@ -114,91 +112,244 @@ __global__ void __launch_bounds__(256) k_potrf_diag(PotrfDiagParams p) {
       x[i] = -acc * inv_diag[i];
     }
     // inv(i, c) for i > c goes to block position (row c, col i)
-    for (int i = c + 1; i < kR; ++i) blk[size_t(i) * p.ld + c] = x[i];
+    for (int i = c + 1; i < kR; ++i) blk[size_t(i) * ld + c] = x[i];
   }
+  __syncthreads();
+}
+
+struct PotrfDiagParams {
+  double* A;
+  int ld, j0;
+  int* status;
+};
+
+__global__ void __launch_bounds__(256) k_potrf_diag(PotrfDiagParams p) {
+  __shared__ double s[kR][kR + 1];
+  __shared__ double inv_diag[kR];
+  diag_factor_inverse<256>(p.A, p.ld, p.j0, p.status, s, inv_diag);
 }
 
 // ---------------------------------------------------------------------------
-// Row-strip triangular solve X * L^T = B for column blocks [jb0, jb1):
-//   X(:, J) = (B(:, J) - X(:, jb0..J) * L(J, jb0..J)^T) * inv(L_JJ)^T
-// Rows are independent, so each CTA owns a 32-row strip and sweeps J; the
-// update product runs on the DMMA engine, the inverse product from smem.
-struct TrsmRowsParams {
+// TRSM  X * L^T = B  (X overwrites B) as a 2-D wavefront over 64x64 blocks:
+//   X(I, J) = (B(I, J) - sum_{K<J} X(I, K) L(J, K)^T) * inv(L_JJ)^T
+// Row strips I are independent; inside a strip block J needs X(I, K < J).
+// CTA (I, J) (linear id J*nI + I, so every producer is dispatched before its
+// consumers) streams its DMMA update over whichever K blocks are already
+// final, waiting on per-block flags, then applies inv(L_JJ)^T from smem and
+// publishes X(I, J).  Flags live in per-task scratch and advance by one per
+// run (CTA (I, J) is the only writer of flag(I, J)), so no reset is needed.
+struct TrsmWaveParams {
   const double* L;  // tile holding L (and inv(L_JJ)^T in its diagonal blocks' upper triangles)
-  double* B;        // tile solved in place; rows [row0, row0 + nrows)
-  int ld, row0, jb0, jb1;
+  double* B;        // tile solved in place
+  int* flags;       // [nI][nJ] per-task scratch
+  int ld;
 };
 
-constexpr int kTrsmPipe = GemmSmem<CfgT, M_MAJOR, M_MAJOR>::DOUBLES;
-constexpr int kTrsmS = kR * (CfgT::BM + 4);  // residual, M_MAJOR [k][row]
-constexpr int kTrsmI = kR * (kR + 4);        // inv(L_JJ), [j][k]
-constexpr int kTrsmSmemDoubles = (kTrsmPipe > kTrsmS + kTrsmI) ? kTrsmPipe : (kTrsmS + kTrsmI);
+constexpr int kWaveS = kR * (kR + 4);
+constexpr int kWaveSmemDoubles =
+    (2 * kWaveS > GemmSmem<CfgG, M_MAJOR, M_MAJOR>::DOUBLES) ? 2 * kWaveS : GemmSmem<CfgG, M_MAJOR, M_MAJOR>::DOUBLES;
 
-__global__ void __launch_bounds__(CfgT::THREADS) k_trsm_rows(TrsmRowsParams p) {
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(CfgG::THREADS) k_trsm_wave(TrsmWaveParams p) {
   extern __shared__ double smem[];
-  double* sS = smem;
-  double* sI = smem + kTrsmS;
-  const int m0 = p.row0 + blockIdx.x * CfgT::BM;
-  const int ld = p.ld;
+  __shared__ int s_hi;
+  const int ld = p.ld, nI = ld / kR, nJ = ld / kR;
+  const int J = blockIdx.x / nI, I = blockIdx.x % nI;
   const int tid = threadIdx.x;
+  int* flag = p.flags + I * nJ;
+  const int gen = ld_acquire(flag + J) + 1;  // this run's generation
+  double acc[CfgG::FM][CfgG::FN][2];
+  zero_acc<CfgG>(acc);
+  TileLoader<CfgG, M_MAJOR, CfgG::BM> la{p.B, ld, I * kR};
+  TileLoader<CfgG, M_MAJOR, CfgG::BN> lb{p.L, ld, J * kR};
+  int done = 0;
+  while (done < J) {
+    if (tid == 0) {
+      while (ld_acquire(flag + done) < gen) __nanosleep(64);
+      int hi = done + 1;
+      while (hi < J && ld_acquire(flag + hi) >= gen) ++hi;
+      s_hi = hi;
+    }
+    __syncthreads();
+    const int hi = s_hi;
+    gemm_mainloop<CfgG>(acc, smem, la, lb, done * kR, hi * kR);
+    done = hi;
+  }
+  // residual -> sS[k][row]; inv(L_JJ) -> sI[j][k]
+  double* sS = smem;
+  double* sI = smem + kWaveS;
+  double* Bb = p.B + size_t(J) * kR * ld + size_t(I) * kR;
+  for_each_acc<CfgG>(acc, [&](int r, int c, double v) { sS[c * (kR + 4) + r] = __ldcg(Bb + size_t(c) * ld + r) - v; });
+  const double* Lb = p.L + size_t(J) * kR * ld + size_t(J) * kR;
+  for (int e = tid; e < kR * kR; e += CfgG::THREADS) {
+    int j = e / kR, k = e % kR;
+    double v;
+    if (k < j) v = __ldcg(Lb + size_t(j) * ld + k);
+    else if (k == j) v = 1.0 / __ldcg(Lb + size_t(j) * ld + j);
+    else v = 0.0;
+    sI[j * (kR + 4) + k] = v;
+  }
+  __syncthreads();
   const int warp = tid >> 5, lane = tid & 31;
-  const int wm = (warp % CfgT::WARPS_M) * CfgT::WM;
-  const int wn = (warp / CfgT::WARPS_M) * CfgT::WN;
+  const int wm = (warp % CfgG::WARPS_M) * CfgG::WM;
+  const int wn = (warp / CfgG::WARPS_M) * CfgG::WN;
   const int g = lane >> 2, t = lane & 3;
-  for (int J = p.jb0; J < p.jb1; ++J) {
-    const int c0 = J * kR;
-    double acc[CfgT::FM][CfgT::FN][2];
-    zero_acc<CfgT>(acc);
-    if (J > p.jb0) {
-      TileLoader<CfgT, M_MAJOR, CfgT::BM> la{p.B, ld, m0};
-      TileLoader<CfgT, M_MAJOR, CfgT::BN> lb{p.L, ld, c0};
-      gemm_mainloop<CfgT>(acc, smem, la, lb, p.jb0 * kR, c0);
-    }
-    // residual -> smem S[k][row]
-    for_each_acc<CfgT>(acc, [&](int r, int c, double v) {
-      sS[c * (CfgT::BM + 4) + r] = p.B[size_t(c0 + c) * ld + m0 + r] - v;
-    });
-    // inv(L_JJ): element (j, k) = inv(j, k), k < j stored at block (row k, col j)
-    const double* Lb = p.L + size_t(c0) * ld + c0;
-    for (int e = tid; e < kR * kR; e += CfgT::THREADS) {
-      int j = e / kR, k = e % kR;
-      double v;
-      if (k < j) v = Lb[size_t(j) * ld + k];
-      else if (k == j) v = 1.0 / Lb[size_t(j) * ld + j];
-      else v = 0.0;
-      sI[j * (kR + 4) + k] = v;
-    }
-    __syncthreads();
-    // X(:, J) = S * inv^T : acc2(r, j) = sum_k S(r, k) inv(j, k)
-    double acc2[CfgT::FM][CfgT::FN][2];
-    zero_acc<CfgT>(acc2);
+  double acc2[CfgG::FM][CfgG::FN][2];
+  zero_acc<CfgG>(acc2);
 #pragma unroll 4
-    for (int kk = 0; kk < kR; kk += 4) {
-      double af[CfgT::FM], bf[CfgT::FN];
+  for (int kk = 0; kk < kR; kk += 4) {
+    double af[CfgG::FM], bf[CfgG::FN];
 #pragma unroll
-      for (int i = 0; i < CfgT::FM; ++i) af[i] = sS[(kk + t) * (CfgT::BM + 4) + wm + i * 8 + g];
+    for (int i = 0; i < CfgG::FM; ++i) af[i] = sS[(kk + t) * (kR + 4) + wm + i * 8 + g];
 #pragma unroll
-      for (int j = 0; j < CfgT::FN; ++j) bf[j] = sI[(wn + j * 8 + g) * (kR + 4) + kk + t];
+    for (int j = 0; j < CfgG::FN; ++j) bf[j] = sI[(wn + j * 8 + g) * (kR + 4) + kk + t];
 #pragma unroll
-      for (int i = 0; i < CfgT::FM; ++i)
+    for (int i = 0; i < CfgG::FM; ++i)
 #pragma unroll
-        for (int j = 0; j < CfgT::FN; ++j) dmma_8x8x4(acc2[i][j][0], acc2[i][j][1], af[i], bf[j]);
-    }
-    for_each_acc<CfgT>(acc2, [&](int r, int c, double v) { p.B[size_t(c0 + c) * ld + m0 + r] = v; });
+      for (int j = 0; j < CfgG::FN; ++j) dmma_8x8x4(acc2[i][j][0], acc2[i][j][1], af[i], bf[j]);
+  }
+  for_each_acc<CfgG>(acc2, [&](int r, int c, double v) { Bb[size_t(c) * ld + r] = v; });
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) st_release(flag + J, gen);
+}
+
+// ---------------------------------------------------------------------------
+// POTRF of a whole nb x nb tile as ONE thread-block-cluster kernel (16 CTAs,
+// non-portable size): r=64 right-looking blocked Cholesky with cluster
+// barriers between the panel solve and the trailing update.  CTA 0 updates
+// the next diagonal block first and factors it (plus its inverse) while the
+// other 15 CTAs finish the trailing update (lookahead), so the latency-bound
+// 64x64 factorization hides behind DMMA work.
+constexpr int kPotrfCl = 16;
+
+struct PotrfParams {
+  double* A;
+  int nb;
+  int* status;
+};
+
+constexpr int kSolveS = kR * (kR + 4);
+constexpr int kPotrfSmemDoubles =
+    (2 * kSolveS > GemmSmem<CfgG, M_MAJOR, M_MAJOR>::DOUBLES) ? 2 * kSolveS : GemmSmem<CfgG, M_MAJOR, M_MAJOR>::DOUBLES;
+
+// X = A(I rows, J cols) * inv(L_JJ)^T in place (one 64x64 block, from smem).
+__device__ void potrf_solve_block(double* A, int ld, int I, int J, double* smem) {
+  double* sS = smem;            // [k][row], ld kR+4
+  double* sI = smem + kSolveS;  // [j][k],  ld kR+4
+  const int tid = threadIdx.x;
+  const double* blk = A + size_t(J) * kR * ld + size_t(I) * kR;
+  const double* Lb = A + size_t(J) * kR * ld + size_t(J) * kR;
+  for (int e = tid; e < kR * kR; e += CfgG::THREADS) {
+    int c = e / kR, r = e % kR;
+    sS[c * (kR + 4) + r] = __ldcg(blk + size_t(c) * ld + r);
+    // inverse element (j=c, k=r): k < j in the upper triangle, diag = 1/L(j,j)
+    double v;
+    if (r < c) v = __ldcg(Lb + size_t(c) * ld + r);
+    else if (r == c) v = 1.0 / __ldcg(Lb + size_t(c) * ld + c);
+    else v = 0.0;
+    sI[c * (kR + 4) + r] = v;
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = (warp % CfgG::WARPS_M) * CfgG::WM;
+  const int wn = (warp / CfgG::WARPS_M) * CfgG::WN;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[CfgG::FM][CfgG::FN][2];
+  zero_acc<CfgG>(acc);
+#pragma unroll 4
+  for (int kk = 0; kk < kR; kk += 4) {
+    double af[CfgG::FM], bf[CfgG::FN];
+#pragma unroll
+    for (int i = 0; i < CfgG::FM; ++i) af[i] = sS[(kk + t) * (kR + 4) + wm + i * 8 + g];
+#pragma unroll
+    for (int j = 0; j < CfgG::FN; ++j) bf[j] = sI[(wn + j * 8 + g) * (kR + 4) + kk + t];
+#pragma unroll
+    for (int i = 0; i < CfgG::FM; ++i)
+#pragma unroll
+      for (int j = 0; j < CfgG::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+  double* out = A + size_t(J) * kR * ld + size_t(I) * kR;
+  for_each_acc<CfgG>(acc, [&](int r, int c, double v) { out[size_t(c) * ld + r] = v; });
+  __syncthreads();
+}
+
+// A(I, K) -= X_I * X_K^T with X = column block J (lower only when I == K).
+__device__ void potrf_update_tile(double* A, int ld, int I, int K, int J, double* smem) {
+  double acc[CfgG::FM][CfgG::FN][2];
+  zero_acc<CfgG>(acc);
+  const double* X = A + size_t(J) * kR * ld;
+  TileLoader<CfgG, M_MAJOR, CfgG::BM> la{X, ld, I * kR};
+  TileLoader<CfgG, M_MAJOR, CfgG::BN> lb{X, ld, K * kR};
+  gemm_mainloop<CfgG>(acc, smem, la, lb, 0, kR);
+  double* C = A + size_t(K) * kR * ld + size_t(I) * kR;
+  const bool diag = I == K;
+  for_each_acc<CfgG>(acc, [&](int r, int c, double v) {
+    if (diag && r < c) return;
+    C[size_t(c) * ld + r] -= v;
+  });
+  __syncthreads();
+}
+
+__global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS) k_potrf_cluster(PotrfParams p) {
+  extern __shared__ double smem[];
+  __shared__ double s[kR][kR + 1];
+  __shared__ double inv_diag[kR];
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const int nb = p.nb, nJ = nb / kR;
+  if (q == 0) diag_factor_inverse<CfgG::THREADS>(p.A, nb, 0, p.status, s, inv_diag);
+  __threadfence();
+  cl.sync();
+  for (int J = 0; J < nJ; ++J) {
+    for (int I = J + 1 + q; I < nJ; I += kPotrfCl) potrf_solve_block(p.A, nb, I, J, smem);
     __threadfence();
-    __syncthreads();
+    cl.sync();
+    if (J + 1 == nJ) break;
+    // trailing tiles (I, K), J < K <= I < nJ; tile 0 is (J+1, J+1)
+    if (q == 0) {
+      potrf_update_tile(p.A, nb, J + 1, J + 1, J, smem);
+      __threadfence();
+      diag_factor_inverse<CfgG::THREADS>(p.A, nb, (J + 1) * kR, p.status, s, inv_diag);
+    } else {
+      int t = 0;
+      for (int I = J + 1; I < nJ; ++I)
+        for (int K = J + 1; K <= I; ++K, ++t) {
+          if (t == 0) continue;
+          if ((t - 1) % (kPotrfCl - 1) == q - 1) potrf_update_tile(p.A, nb, I, K, J, smem);
+        }
+    }
+    __threadfence();
+    cl.sync();
   }
 }
 
 // ---------------------------------------------------------------------------
 static unsigned gemm_smem() { return (unsigned)GemmSmem<CfgG, M_MAJOR, M_MAJOR>::BYTES; }
-static unsigned trsm_smem() { return (unsigned)(kTrsmSmemDoubles * sizeof(double)); }
+static unsigned trsm_smem() { return (unsigned)(kWaveSmemDoubles * sizeof(double)); }
+
+#define HG_ATTR(fn, attr, val)                                                                   \
+  do {                                                                                           \
+    cudaError_t e_ = cudaFuncSetAttribute(fn, attr, val);                                        \
+    if (e_ != cudaSuccess) {                                                                     \
+      set_error("cudaFuncSetAttribute(%s, %s, %d): %s", #fn, #attr, int(val), cudaGetErrorString(e_)); \
+      return false;                                                                              \
+    }                                                                                            \
+  } while (0)
 
 bool init_chol_attributes() {
-  if (cudaFuncSetAttribute(k_gemm_nt, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem()) != cudaSuccess)
-    return false;
-  if (cudaFuncSetAttribute(k_trsm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem()) != cudaSuccess)
-    return false;
+  HG_ATTR(k_gemm_nt, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem());
+  HG_ATTR(k_trsm_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
+  HG_ATTR(k_potrf_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPotrfSmemDoubles * sizeof(double)));
+  HG_ATTR(k_potrf_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return true;
 }
 
@@ -210,12 +361,8 @@ static void push_gemm(std::vector<LaunchDesc>& out, const double* A, const doubl
   out.push_back(d);
 }
 
-static void push_trsm(std::vector<LaunchDesc>& out, const double* L, double* B, int ld, int row0, int nrows,
-                      int jb0, int jb1) {
-  LaunchDesc d;
-  TrsmRowsParams p{L, B, ld, row0, jb0, jb1};
-  d.set((const void*)k_trsm_rows, dim3(nrows / CfgT::BM), dim3(CfgT::THREADS), trsm_smem(), p);
-  out.push_back(d);
+int chol_scratch_ints(int kind, int nb) {
+  return kind == K_TRSM ? (nb / kR) * (nb / kR) : 0;
 }
 
 bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out) {
@@ -227,24 +374,24 @@ bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc
   const int nJ = nb / kR;
   switch (kind) {
     case K_POTRF: {
-      double* A = o.t[0];
-      for (int J = 0; J < nJ; ++J) {
-        LaunchDesc d;
-        PotrfDiagParams pd{A, nb, J * kR, o.status};
-        d.set((const void*)k_potrf_diag, dim3(1), dim3(256), 0, pd);
-        out.push_back(d);
-        if (J + 1 < nJ) {
-          const int r1 = (J + 1) * kR, rest = nb - r1;
-          push_trsm(out, A, A, nb, r1, rest, J, J + 1);
-          const double* panel = A + size_t(J) * kR * nb + r1;
-          push_gemm(out, panel, panel, A + size_t(r1) * nb + r1, nb, rest, rest, kR, 1);
-        }
-      }
+      LaunchDesc d;
+      PotrfParams pp{o.t[0], nb, o.status};
+      d.set((const void*)k_potrf_cluster, dim3(kPotrfCl), dim3(CfgG::THREADS),
+            unsigned(kPotrfSmemDoubles * sizeof(double)), pp);
+      out.push_back(d);
       return true;
     }
-    case K_TRSM:
-      push_trsm(out, o.t[0], o.t[1], nb, 0, nb, 0, nJ);
+    case K_TRSM: {
+      if (!o.scratch) {
+        set_error("TRSM needs per-task scratch (%d ints)", nJ * nJ);
+        return false;
+      }
+      LaunchDesc d;
+      TrsmWaveParams tp{o.t[0], o.t[1], o.scratch, nb};
+      d.set((const void*)k_trsm_wave, dim3(nJ * nJ), dim3(CfgG::THREADS), trsm_smem(), tp);
+      out.push_back(d);
       return true;
+    }
     case K_SYRK:
       push_gemm(out, o.t[0], o.t[0], o.t[1], nb, nb, nb, nb, 1);
       return true;

@@ -1,9 +1,470 @@
-// LU tile kernels (placeholder until the kernels land).
+// LU with incremental pivoting tile kernels for sm_100a:
+// GETRF_INC, GESSM, TSTRF, SSSSM (reference kinds kernels.py:29-33, access
+// lists kernels.py:156-167; semantics restated in oracle/tiles_lu_qr.py).
+//
+// Two kernels build every LU kind:
+//
+//  k_lu_panel  -- one ib-wide panel factorization (GETRF: partial pivoting
+//                 over the tile rows >= j; TSTRF: pairwise pivoting between
+//                 U(j,j) and the rows of A_ik).  A thread-block CLUSTER of 8
+//                 CTAs keeps the panel resident in shared memory (CTA q owns
+//                 rows [q*nb/8, (q+1)*nb/8)); each column costs ONE cluster
+//                 barrier: every CTA publishes its local arg-max and that
+//                 row's values (double-buffered by column parity), then all
+//                 CTAs read the 8 candidates over DSMEM, agree on the pivot,
+//                 and update their own rows.  The panel ends by inverting its
+//                 unit-lower diagonal block L_uu into the tile's side area
+//                 (so every later application is a DMMA product, no scalar
+//                 substitution).
+//  k_lu_apply  -- applies panels [p0, p1) of a factor to a column strip:
+//                 row interchanges (gathered into smem, applied in order),
+//                 top <- inv(L_uu) * top and bot -= L_a * top on the DMMA
+//                 engine.  GESSM / SSSSM are one launch (all panels, all
+//                 columns); GETRF / TSTRF call it after each panel on the
+//                 trailing columns.
+//
+// Side area of a tile (after its nb*nb doubles): inv(L_uu) blocks, ib x nb
+// column-major (panel p at columns [p*ib, p*ib+sb)), then int32 ipiv[nb]
+// (GETRF: absolute row swapped with row j; TSTRF: A row swapped with U row j,
+// or -1).
+#include <cooperative_groups.h>
+
+#include "dgemm_dmma.cuh"
 #include "tiles.h"
+
+namespace cg = cooperative_groups;
+
 namespace hg {
-bool init_lu_attributes() { return true; }
-bool build_lu_launches(int kind, const TaskOperands&, std::vector<LaunchDesc>&) {
-  set_error("kind %d: LU tile kernels are not built yet", kind);
-  return false;
+
+constexpr int kLuCl = 8;          // cluster size (portable)
+constexpr int kLuThreads = 256;
+constexpr int kLuMaxSb = 128;
+
+enum { LU_GETRF = 0, LU_TSTRF = 1 };
+
+struct LuPanelParams {
+  double* A;      // panel tile (GETRF: A_kk, TSTRF: A_ik)
+  double* U;      // TSTRF: A_kk (upper part holds U); GETRF: unused
+  double* side;   // side area of A: inverse blocks (ib x nb), then ipiv
+  int nb, ib, ii, sb, mode;
+  int* status;
+};
+
+__device__ __forceinline__ bool better(double v, int r, double bv, int br) {
+  return v > bv || (v == bv && r < br);
 }
+
+__global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu_panel(LuPanelParams p) {
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const int nb = p.nb, sb = p.sb, ii = p.ii, ib = p.ib;
+  const int R = nb / kLuCl;  // rows per CTA
+  const int row0 = q * R;
+  const int LD = R + 1;
+  const int tid = threadIdx.x;
+  const bool ts = p.mode == LU_TSTRF;
+  double* s = sm;                                 // s[c*LD + r]: panel column c, local row r
+  double* cand = s + sb * LD;                     // [2][sb]  candidate (local arg-max) row
+  double* rowj = cand + 2 * kLuMaxSb;             // [2][sb]  GETRF: row j before the swap
+  double* urow = rowj + 2 * kLuMaxSb;             // [2][sb]  TSTRF: U row j (cols >= jj)
+  double* prow = urow + 2 * kLuMaxSb;             // [sb]     pivot row used for the update
+  double* slot_v = prow + kLuMaxSb;               // [2]
+  int* slot_r = reinterpret_cast<int*>(slot_v + 2);  // [2]
+  __shared__ double red_v[kLuThreads / 32];
+  __shared__ int red_r[kLuThreads / 32];
+  __shared__ int s_win_row, s_win_cta, s_swap;
+  __shared__ double s_piv;
+  int* ipiv = reinterpret_cast<int*>(p.side + size_t(ib) * nb);
+  double* inv = p.side + size_t(ii) * ib;  // this panel's ib x sb block (ld = ib)
+  double* A = p.A;
+
+  // rows this CTA stages: GETRF touches rows >= ii only
+  for (int e = tid; e < sb * R; e += kLuThreads) {
+    int c = e / R, r = e % R;
+    int gr = row0 + r;
+    s[c * LD + r] = (ts || gr >= ii) ? A[size_t(ii + c) * nb + gr] : 0.0;
+  }
+  // dL (TSTRF) is written only for swapped rows: clear this panel's block first
+  // (ordered before any owner's write by the first cluster barrier)
+  if (ts && q == 0)
+    for (int e = tid; e < ib * sb; e += kLuThreads) inv[e] = 0.0;
+  __syncthreads();
+
+  for (int jj = 0; jj < sb; ++jj) {
+    const int j = ii + jj;
+    const int par = jj & 1;
+    // ---- phase A: local arg-max, publish candidate row --------------------
+    double bv = -1.0;
+    int br = 0x7fffffff;
+    for (int r = tid; r < R; r += kLuThreads) {
+      int gr = row0 + r;
+      bool active = ts ? true : (gr >= j);
+      if (active) {
+        double v = fabs(s[jj * LD + r]);
+        if (better(v, gr, bv, br)) {
+          bv = v;
+          br = gr;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int orr = __shfl_xor_sync(0xffffffffu, br, o);
+      if (better(ov, orr, bv, br)) {
+        bv = ov;
+        br = orr;
+      }
+    }
+    if ((tid & 31) == 0) {
+      red_v[tid >> 5] = bv;
+      red_r[tid >> 5] = br;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double v = red_v[0];
+      int r = red_r[0];
+      for (int w = 1; w < kLuThreads / 32; ++w)
+        if (better(red_v[w], red_r[w], v, r)) {
+          v = red_v[w];
+          r = red_r[w];
+        }
+      slot_v[par] = v;
+      slot_r[par] = r;
+    }
+    __syncthreads();
+    {
+      const int r = slot_r[par];
+      const bool mine = r >= row0 && r < row0 + R;
+      for (int c = tid; c < sb; c += kLuThreads) {
+        cand[par * kLuMaxSb + c] = mine ? s[c * LD + (r - row0)] : 0.0;
+        if (!ts && j >= row0 && j < row0 + R) rowj[par * kLuMaxSb + c] = s[c * LD + (j - row0)];
+        if (ts) urow[par * kLuMaxSb + c] = c >= jj ? p.U[size_t(ii + c) * nb + j] : 0.0;
+      }
+    }
+    cl.sync();
+    // ---- phase B: global pivot decision (identical in every CTA) ------------
+    if (tid == 0) {
+      double v = -1.0;
+      int r = 0x7fffffff, who = 0;
+      for (int c2 = 0; c2 < kLuCl; ++c2) {
+        const double* sv = cl.map_shared_rank(slot_v, c2);
+        const int* sr = cl.map_shared_rank(slot_r, c2);
+        if (better(sv[par], sr[par], v, r)) {
+          v = sv[par];
+          r = sr[par];
+          who = c2;
+        }
+      }
+      s_win_row = r;
+      s_win_cta = who;
+      if (ts) s_swap = v > fabs(urow[par * kLuMaxSb + jj]) ? 1 : 0;
+      else s_swap = (r != j) ? 1 : 0;
+    }
+    __syncthreads();
+    const int wr = s_win_row, wc = s_win_cta;
+    const bool swap = s_swap != 0;
+    {
+      const double* wc_cand = cl.map_shared_rank(cand, wc) + par * kLuMaxSb;
+      for (int c = tid; c < sb; c += kLuThreads) {
+        double v;
+        if (ts) v = swap ? wc_cand[c] : urow[par * kLuMaxSb + c];
+        else v = wc_cand[c];
+        prow[c] = v;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_piv = prow[jj];
+      if (q == 0) ipiv[j] = ts ? (swap ? wr : -1) : wr;
+      if (s_piv == 0.0 && q == 0 && p.status) atomicOr(p.status, 2);
+    }
+    // swaps by the owners
+    if (ts) {
+      if (swap && wr >= row0 && wr < row0 + R) {
+        const int lr = wr - row0;
+        for (int c = tid; c < sb; c += kLuThreads) {
+          if (c < jj) {
+            inv[size_t(c) * ib + jj] = s[c * LD + lr];  // dL(jj, c), inverted at panel end
+            s[c * LD + lr] = 0.0;
+          } else {
+            p.U[size_t(ii + c) * nb + j] = prow[c];
+            s[c * LD + lr] = urow[par * kLuMaxSb + c];
+          }
+        }
+      }
+    } else if (swap) {
+      if (wr >= row0 && wr < row0 + R) {  // row p <- old row j
+        const int oj = (j - j % R) / R;   // owner CTA of row j
+        const double* src = cl.map_shared_rank(rowj, oj) + par * kLuMaxSb;
+        for (int c = tid; c < sb; c += kLuThreads) s[c * LD + (wr - row0)] = src[c];
+      }
+      if (j >= row0 && j < row0 + R)
+        for (int c = tid; c < sb; c += kLuThreads) s[c * LD + (j - row0)] = prow[c];
+    }
+    __syncthreads();
+    const double piv = s_piv;
+    if (piv != 0.0) {
+      const double rcp = 1.0 / piv;
+      const int w = sb - jj - 1;
+      // scale column jj of my rows, then rank-1 update of columns (jj, sb)
+      for (int r = tid; r < R; r += kLuThreads) {
+        const int gr = row0 + r;
+        if (ts || gr > j) s[jj * LD + r] *= rcp;
+      }
+      __syncthreads();
+      for (int e = tid; e < w * R; e += kLuThreads) {
+        const int c = jj + 1 + e / R, r = e % R;
+        const int gr = row0 + r;
+        if (ts || gr > j) s[c * LD + r] = fma(-s[jj * LD + r], prow[c], s[c * LD + r]);
+      }
+    }
+    __syncthreads();
+  }
+  cl.sync();
+  // ---- write the panel back ----------------------------------------------------
+  for (int e = tid; e < sb * R; e += kLuThreads) {
+    int c = e / R, r = e % R;
+    int gr = row0 + r;
+    if (ts || gr >= ii) A[size_t(ii + c) * nb + gr] = s[c * LD + r];
+  }
+  __threadfence();
+  cl.sync();
+  // ---- inv(L_uu) into the side area (columns distributed over the cluster) ----
+  // L_uu(r, c), r > c: GETRF: tile rows [ii, ii+sb) of the panel; TSTRF: dL (side)
+  double* Ls = s;  // [sb][sb+1], Ls[c*(sb+1) + r]
+  const int LL = sb + 1;
+  for (int e = tid; e < sb * sb; e += kLuThreads) {
+    int c = e / sb, r = e % sb;
+    double v = 0.0;
+    if (r > c) v = ts ? inv[size_t(c) * ib + r] : A[size_t(ii + c) * nb + ii + r];
+    Ls[c * LL + r] = v;
+  }
+  __syncthreads();
+  cl.sync();  // every CTA has its copy of dL before anyone overwrites it
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int c = q * (kLuThreads / 32) + warp; c < sb; c += kLuCl * (kLuThreads / 32)) {
+    double x[kLuMaxSb / 32];
+#pragma unroll
+    for (int m = 0; m < kLuMaxSb / 32; ++m) {
+      int i = lane + 32 * m;
+      x[m] = (i == c) ? 1.0 : 0.0;
+    }
+    for (int k = c; k < sb; ++k) {
+      double xk = __shfl_sync(0xffffffffu, x[k / 32], k % 32);
+#pragma unroll
+      for (int m = 0; m < kLuMaxSb / 32; ++m) {
+        int i = lane + 32 * m;
+        if (i > k && i < sb) x[m] = fma(-Ls[k * LL + i], xk, x[m]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kLuMaxSb / 32; ++m) {
+      int i = lane + 32 * m;
+      if (i < sb) inv[size_t(c) * ib + i] = x[m];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int SB>
+struct ApplyCfg {
+  using G = GemmCfg<SB, 64, 16, 32, 32, 3>;  // SB x 64 CTA tiles
+  static constexpr int BN = 64;
+};
+
+struct LuApplyParams {
+  const double* L;      // factor tile (GETRF: A_kk; TSTRF: A_ik)
+  const double* side;   // its side area (inverse blocks, ipiv)
+  double* top;          // tile whose rows [ii, ii+sb) are transformed
+  double* bot;          // GETRF-type: == top; TSTRF-type: the other tile
+  int nb, ib, p0, p1, col0, mode;
+};
+
+template <int SB>
+__global__ void __launch_bounds__(ApplyCfg<SB>::G::THREADS) k_lu_apply(LuApplyParams p) {
+  using G = typename ApplyCfg<SB>::G;
+  constexpr int BN = ApplyCfg<SB>::BN;
+  extern __shared__ double sm[];
+  const int nb = p.nb, ib = p.ib;
+  const int n0 = p.col0 + blockIdx.x * BN;
+  const int tid = threadIdx.x;
+  const bool ts = p.mode == LU_TSTRF;
+  const int* ipiv = reinterpret_cast<const int*>(p.side + size_t(ib) * nb);
+  // smem: swap buffer [2*SB][BN+1] + slot map [nb] ints, aliased with the GEMM ring
+  double* buf = sm;
+  constexpr int BLD = BN + 1;
+  int* slot_of = reinterpret_cast<int*>(sm + 2 * SB * BLD);
+  __shared__ int extra_row[SB];
+  __shared__ int n_extra;
+  for (int P = p.p0; P < p.p1; ++P) {
+    const int ii = P * ib;
+    // ---- 1) row interchanges of this panel, gathered into smem ----------------
+    for (int r = tid; r < nb; r += blockDim.x) slot_of[r] = -1;
+    __syncthreads();
+    if (tid == 0) {
+      int ne = 0;
+      for (int jj = 0; jj < SB; ++jj) {
+        int r = ipiv[ii + jj];
+        bool sw = ts ? (r >= 0) : (r != ii + jj);
+        if (!sw) continue;
+        int key = ts ? r : r;  // bot row (TSTRF) / tile row (GETRF)
+        bool in_top = !ts && r >= ii && r < ii + SB;
+        if (!in_top && slot_of[key] < 0) {
+          slot_of[key] = SB + ne;
+          extra_row[ne++] = key;
+        }
+      }
+      n_extra = ne;
+    }
+    __syncthreads();
+    const int ne = n_extra;
+    // gather top rows [ii, ii+SB) and the extra rows, column by column (coalesced)
+    for (int e = tid; e < BN * (SB + ne); e += blockDim.x) {
+      int c = e / (SB + ne), k = e % (SB + ne);
+      double v;
+      if (k < SB) v = p.top[size_t(n0 + c) * nb + ii + k];
+      else v = (ts ? p.bot : p.top)[size_t(n0 + c) * nb + extra_row[k - SB]];
+      buf[k * BLD + c] = v;
+    }
+    __syncthreads();
+    if (tid < BN) {
+      const int c = tid;
+      for (int jj = 0; jj < SB; ++jj) {
+        int r = ipiv[ii + jj];
+        bool sw = ts ? (r >= 0) : (r != ii + jj);
+        if (!sw) continue;
+        int k2 = (!ts && r >= ii && r < ii + SB) ? (r - ii) : slot_of[r];
+        double a = buf[jj * BLD + c];
+        buf[jj * BLD + c] = buf[k2 * BLD + c];
+        buf[k2 * BLD + c] = a;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < BN * (SB + ne); e += blockDim.x) {
+      int c = e / (SB + ne), k = e % (SB + ne);
+      double v = buf[k * BLD + c];
+      if (k < SB) p.top[size_t(n0 + c) * nb + ii + k] = v;
+      else (ts ? p.bot : p.top)[size_t(n0 + c) * nb + extra_row[k - SB]] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    // ---- 2) top <- inv(L_uu) * top (SB x BN, K = SB) -----------------------------
+    {
+      double acc[G::FM][G::FN][2];
+      zero_acc<G>(acc);
+      TileLoader<G, M_MAJOR, G::BM> la{p.side + size_t(ii) * ib, ib, 0};
+      TileLoader<G, K_MAJOR, G::BN> lb{p.top + ii, nb, n0};
+      gemm_mainloop<G>(acc, sm, la, lb, 0, SB);
+      for_each_acc<G>(acc, [&](int r, int c, double v) { p.top[size_t(n0 + c) * nb + ii + r] = v; });
+    }
+    __threadfence();
+    __syncthreads();
+    // ---- 3) bot -= L_a * top ------------------------------------------------------
+    const int m_begin = ts ? 0 : ii + SB;
+    for (int m0 = m_begin; m0 < nb; m0 += SB) {
+      double acc[G::FM][G::FN][2];
+      zero_acc<G>(acc);
+      TileLoader<G, M_MAJOR, G::BM> la{p.L + size_t(ii) * nb, nb, m0};
+      TileLoader<G, K_MAJOR, G::BN> lb{p.top + ii, nb, n0};
+      gemm_mainloop<G>(acc, sm, la, lb, 0, SB);
+      double* bot = p.bot;
+      for_each_acc<G>(acc, [&](int r, int c, double v) { bot[size_t(n0 + c) * nb + m0 + r] -= v; });
+    }
+    __threadfence();
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+static unsigned panel_smem(int nb, int sb) {
+  const int R = nb / kLuCl;
+  size_t d = size_t(sb) * (R + 1);
+  size_t inv = size_t(sb) * (sb + 1);
+  if (inv > d) d = inv;
+  d += 7 * kLuMaxSb + 4;
+  return unsigned(d * sizeof(double));
+}
+
+template <int SB>
+static unsigned apply_smem(int nb) {
+  using G = typename ApplyCfg<SB>::G;
+  size_t swap = size_t(2 * SB) * (ApplyCfg<SB>::BN + 1) * 8 + size_t(nb) * 4;
+  size_t ring = GemmSmem<G, M_MAJOR, K_MAJOR>::BYTES;
+  return unsigned(swap > ring ? swap : ring);
+}
+
+#define HG_ATTR(fn, attr, val)                                                                   \
+  do {                                                                                           \
+    cudaError_t e_ = cudaFuncSetAttribute(fn, attr, val);                                        \
+    if (e_ != cudaSuccess) {                                                                     \
+      set_error("cudaFuncSetAttribute(%s, %s, %d): %s", #fn, #attr, int(val), cudaGetErrorString(e_)); \
+      return false;                                                                              \
+    }                                                                                            \
+  } while (0)
+
+bool init_lu_attributes() {
+  HG_ATTR(k_lu_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
+  HG_ATTR(k_lu_apply<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem<128>(1024));
+  HG_ATTR(k_lu_apply<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem<64>(1024));
+  return true;
+}
+
+static void push_apply(std::vector<LaunchDesc>& out, int ib, const LuApplyParams& ap) {
+  LaunchDesc d;
+  const int ncols = ap.nb - ap.col0;
+  if (ib == 128)
+    d.set((const void*)k_lu_apply<128>, dim3(ncols / ApplyCfg<128>::BN), dim3(ApplyCfg<128>::G::THREADS),
+          apply_smem<128>(ap.nb), ap);
+  else
+    d.set((const void*)k_lu_apply<64>, dim3(ncols / ApplyCfg<64>::BN), dim3(ApplyCfg<64>::G::THREADS),
+          apply_smem<64>(ap.nb), ap);
+  out.push_back(d);
+}
+
+bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out) {
+  const int nb = o.nb, ib = o.ib;
+  if (nb % 128 != 0 || nb > 1024 || (ib != 64 && ib != 128) || nb % ib != 0) {
+    set_error("LU tile kernels need nb %% 128 == 0, nb <= 1024 and ib in {64, 128}; got nb=%d ib=%d", nb, ib);
+    return false;
+  }
+  const size_t tile = size_t(nb) * nb;
+  const int np = nb / ib;
+  auto side = [&](int i) { return o.t[i] + tile; };
+  switch (kind) {
+    case K_GETRF_INC:
+    case K_TSTRF: {
+      const bool ts = kind == K_TSTRF;
+      double* A = ts ? o.t[1] : o.t[0];
+      for (int P = 0; P < np; ++P) {
+        LuPanelParams pp{A, ts ? o.t[0] : nullptr, ts ? side(1) : side(0), nb, ib, P * ib, ib,
+                         ts ? LU_TSTRF : LU_GETRF, o.status};
+        LaunchDesc d;
+        d.set((const void*)k_lu_panel, dim3(kLuCl), dim3(kLuThreads), panel_smem(nb, ib), pp);
+        out.push_back(d);
+        if (P + 1 < np) {
+          LuApplyParams ap{A, ts ? side(1) : side(0), ts ? o.t[0] : A, A, nb, ib, P, P + 1, (P + 1) * ib,
+                           ts ? LU_TSTRF : LU_GETRF};
+          push_apply(out, ib, ap);
+        }
+      }
+      return true;
+    }
+    case K_GESSM: {
+      LuApplyParams ap{o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF};
+      push_apply(out, ib, ap);
+      return true;
+    }
+    case K_SSSSM: {
+      LuApplyParams ap{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF};
+      push_apply(out, ib, ap);
+      return true;
+    }
+    default:
+      set_error("kind %d is not an LU kind", kind);
+      return false;
+  }
+}
+
 }  // namespace hg

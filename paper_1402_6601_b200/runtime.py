@@ -151,8 +151,8 @@ class Executor:
         return ExecStats(st.elapsed_ms, st.bytes_h2d, st.bytes_d2d, st.bytes_d2h, st.bytes_side,
                          st.n_kernel_nodes, st.n_copy_nodes)
 
-    def launch(self, stream: int | None = None):
-        """Enqueue one run on ``stream`` (a cudaStream_t as int; None = own stream)."""
+    def launch(self, stream: int = 0):
+        """Enqueue one run on ``stream`` (a cudaStream_t as int; 0 = the legacy default stream)."""
         _native.check(_native.lib().hg_exec_launch(self._h, C.c_void_p(stream) if stream else None),
                       "hg_exec_launch")
 
