@@ -117,6 +117,136 @@ __device__ void diag_factor_inverse(double* A, int ld, int j0, int* status, doub
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// Fast variant for 4 warps: the 64x64 block as a 2x2 recursion on 32x32
+// leaves.  A leaf (Cholesky + inverse of a 32x32 block) runs in ONE warp with
+// the block rows in registers and shuffles as the only communication (no
+// __syncthreads inside); the off-diagonal products are spread over 128 threads.
+//   L11, I11 = leaf(A11);  L21 = A21 I11^T;  A22 -= L21 L21^T;
+//   L22, I22 = leaf(A22);  I21 = -I22 (L21 I11)
+__device__ __forceinline__ void leaf32(double* s, int lds, int r0, double* iv, int ldi, int* status) {
+  const int lane = threadIdx.x & 31;
+  double a[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) a[k] = (k <= lane) ? s[(r0 + k) * lds + r0 + lane] : 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    double ajj = __shfl_sync(0xffffffffu, a[j], j);
+    if (!(ajj > 0.0)) {
+      bad = true;
+      ajj = 1.0;
+    }
+    const double d = sqrt(ajj);
+    const double rd = 1.0 / d;
+    a[j] = (lane == j) ? d : (lane > j ? a[j] * rd : a[j]);
+#pragma unroll
+    for (int k = j + 1; k < 32; ++k) {
+      const double lk = __shfl_sync(0xffffffffu, a[j], k);
+      if (lane >= k) a[k] = fma(-a[j], lk, a[k]);
+    }
+  }
+  if (bad && lane == 0 && status) atomicOr(status, 1);
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (k <= lane) s[(r0 + k) * lds + r0 + lane] = a[k];
+  __syncwarp();
+  // inverse: lane c computes column c, x = L^{-1} e_c (broadcast smem reads of L)
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const double rli = 1.0 / s[(r0 + i) * lds + r0 + i];
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k)
+      if (k >= lane) acc = fma(s[(r0 + k) * lds + r0 + i], x[k], acc);
+    x[i] = (i == lane) ? rli : (i > lane ? -acc * rli : 0.0);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) iv[lane * ldi + i] = x[i];  // iv[c][i] = inv(i, c)
+  __syncwarp();
+}
+
+template <int NT>
+__device__ void diag_factor_inverse_fast(double* A, int ld, int j0, int* status, double (*s)[kR + 1],
+                                         double (*iv)[kR + 1], double (*tm)[33]) {
+  double* blk = A + size_t(j0) * ld + j0;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  double* S = &s[0][0];
+  double* IV = &iv[0][0];
+  constexpr int L = kR + 1;
+  for (int e = tid; e < kR * kR; e += NT) {
+    int c = e / kR, r = e % kR;
+    s[c][r] = __ldcg(blk + size_t(c) * ld + r);
+  }
+  __syncthreads();
+  if (warp == 0) leaf32(S, L, 0, IV, L, status);
+  __syncthreads();
+  // L21(i, c) = sum_{k >= c} A21(i, k) I11(k, c)^T ... = sum_k A21(i,k) inv11(c,k), k <= c
+  double out[8];
+  const int row = 32 + (tid >> 2), cb = (tid & 3) * 8;
+  if (tid < 128) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = cb + q;
+      double acc = 0.0;
+      for (int k = 0; k <= c; ++k) acc = fma(s[k][row], iv[k][c], acc);
+      out[q] = acc;
+    }
+  }
+  __syncthreads();
+  if (tid < 128) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[cb + q][row] = out[q];
+  }
+  __syncthreads();
+  // A22 -= L21 L21^T (lower)
+  if (tid < 128) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = 32 + cb + q;
+      if (c > row) continue;
+      double acc = 0.0;
+      for (int k = 0; k < 32; ++k) acc = fma(s[k][row], s[k][c], acc);
+      s[c][row] -= acc;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) leaf32(S, L, 32, IV + 32 * L + 32, L, status);
+  __syncthreads();
+  // T = L21 I11 -> tm[c][i]  (T(i, c) = sum_{k >= c} L21(i, k) I11(k, c))
+  if (tid < 128) {
+    const int i = row - 32;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = cb + q;
+      double acc = 0.0;
+      for (int k = c; k < 32; ++k) acc = fma(s[k][row], iv[c][k], acc);
+      tm[c][i] = acc;
+    }
+  }
+  __syncthreads();
+  // I21(i, c) = -sum_{k <= i} I22(i, k) T(k, c)
+  if (tid < 128) {
+    const int i = row - 32;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = cb + q;
+      double acc = 0.0;
+      for (int k = 0; k <= i; ++k) acc = fma(iv[32 + k][32 + i], tm[c][k], acc);
+      iv[c][32 + i] = -acc;
+    }
+  }
+  __syncthreads();
+  // L (lower) and inv^T (strict upper: inv(i, c), i > c, at block (row c, col i))
+  for (int e = tid; e < kR * kR; e += NT) {
+    int c = e / kR, r = e % kR;
+    if (r >= c) blk[size_t(c) * ld + r] = s[c][r];
+    else blk[size_t(c) * ld + r] = iv[r][c];
+  }
+  __syncthreads();
+}
+
 struct PotrfDiagParams {
   double* A;
   int ld, j0;
@@ -240,6 +370,7 @@ struct PotrfParams {
 constexpr int kSolveS = kR * (kR + 4);
 constexpr int kPotrfSmemDoubles =
     (2 * kSolveS > GemmSmem<CfgG, M_MAJOR, M_MAJOR>::DOUBLES) ? 2 * kSolveS : GemmSmem<CfgG, M_MAJOR, M_MAJOR>::DOUBLES;
+constexpr int kPotrfDynDoubles = kPotrfSmemDoubles + 2 * kR * (kR + 1) + 32 * 33;
 
 // X = A(I rows, J cols) * inv(L_JJ)^T in place (one 64x64 block, from smem).
 __device__ void potrf_solve_block(double* A, int ld, int I, int J, double* smem) {
@@ -301,12 +432,14 @@ __device__ void potrf_update_tile(double* A, int ld, int I, int K, int J, double
 
 __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS) k_potrf_cluster(PotrfParams p) {
   extern __shared__ double smem[];
-  __shared__ double s[kR][kR + 1];
-  __shared__ double inv_diag[kR];
+  // dynamic smem: [GEMM ring / solve buffers | s 64x65 | iv 64x65 | tm 32x33]
+  auto s = reinterpret_cast<double(*)[kR + 1]>(smem + kPotrfSmemDoubles);
+  auto iv = reinterpret_cast<double(*)[kR + 1]>(smem + kPotrfSmemDoubles + kR * (kR + 1));
+  auto tm = reinterpret_cast<double(*)[33]>(smem + kPotrfSmemDoubles + 2 * kR * (kR + 1));
   cg::cluster_group cl = cg::this_cluster();
   const int q = (int)cl.block_rank();
   const int nb = p.nb, nJ = nb / kR;
-  if (q == 0) diag_factor_inverse<CfgG::THREADS>(p.A, nb, 0, p.status, s, inv_diag);
+  if (q == 0) diag_factor_inverse_fast<CfgG::THREADS>(p.A, nb, 0, p.status, s, iv, tm);
   __threadfence();
   cl.sync();
   for (int J = 0; J < nJ; ++J) {
@@ -318,7 +451,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
     if (q == 0) {
       potrf_update_tile(p.A, nb, J + 1, J + 1, J, smem);
       __threadfence();
-      diag_factor_inverse<CfgG::THREADS>(p.A, nb, (J + 1) * kR, p.status, s, inv_diag);
+      diag_factor_inverse_fast<CfgG::THREADS>(p.A, nb, (J + 1) * kR, p.status, s, iv, tm);
     } else {
       int t = 0;
       for (int I = J + 1; I < nJ; ++I)
@@ -348,7 +481,7 @@ static unsigned trsm_smem() { return (unsigned)(kWaveSmemDoubles * sizeof(double
 bool init_chol_attributes() {
   HG_ATTR(k_gemm_nt, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem());
   HG_ATTR(k_trsm_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
-  HG_ATTR(k_potrf_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPotrfSmemDoubles * sizeof(double)));
+  HG_ATTR(k_potrf_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPotrfDynDoubles * sizeof(double)));
   HG_ATTR(k_potrf_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return true;
 }
@@ -377,7 +510,7 @@ bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc
       LaunchDesc d;
       PotrfParams pp{o.t[0], nb, o.status};
       d.set((const void*)k_potrf_cluster, dim3(kPotrfCl), dim3(CfgG::THREADS),
-            unsigned(kPotrfSmemDoubles * sizeof(double)), pp);
+            unsigned(kPotrfDynDoubles * sizeof(double)), pp);
       out.push_back(d);
       return true;
     }

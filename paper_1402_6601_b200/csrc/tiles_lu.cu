@@ -95,6 +95,8 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
     const int j = ii + jj;
     const int par = jj & 1;
     // ---- phase A: local arg-max, publish candidate row --------------------
+    if (ts)  // U row j (columns >= jj): issued first so its latency hides behind the arg-max
+      for (int c = tid; c < sb; c += kLuThreads) urow[par * kLuMaxSb + c] = c >= jj ? p.U[size_t(ii + c) * nb + j] : 0.0;
     double bv = -1.0;
     int br = 0x7fffffff;
     for (int r = tid; r < R; r += kLuThreads) {
@@ -140,27 +142,34 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
       for (int c = tid; c < sb; c += kLuThreads) {
         cand[par * kLuMaxSb + c] = mine ? s[c * LD + (r - row0)] : 0.0;
         if (!ts && j >= row0 && j < row0 + R) rowj[par * kLuMaxSb + c] = s[c * LD + (j - row0)];
-        if (ts) urow[par * kLuMaxSb + c] = c >= jj ? p.U[size_t(ii + c) * nb + j] : 0.0;
       }
     }
     cl.sync();
     // ---- phase B: global pivot decision (identical in every CTA) ------------
-    if (tid == 0) {
+    if (tid < 32) {
       double v = -1.0;
-      int r = 0x7fffffff, who = 0;
-      for (int c2 = 0; c2 < kLuCl; ++c2) {
-        const double* sv = cl.map_shared_rank(slot_v, c2);
-        const int* sr = cl.map_shared_rank(slot_r, c2);
-        if (better(sv[par], sr[par], v, r)) {
-          v = sv[par];
-          r = sr[par];
-          who = c2;
+      int r = 0x7fffffff, who = tid;
+      if (tid < kLuCl) {
+        v = cl.map_shared_rank(slot_v, tid)[par];
+        r = cl.map_shared_rank(slot_r, tid)[par];
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        int orr = __shfl_xor_sync(0xffffffffu, r, o);
+        int ow = __shfl_xor_sync(0xffffffffu, who, o);
+        if (better(ov, orr, v, r)) {
+          v = ov;
+          r = orr;
+          who = ow;
         }
       }
-      s_win_row = r;
-      s_win_cta = who;
-      if (ts) s_swap = v > fabs(urow[par * kLuMaxSb + jj]) ? 1 : 0;
-      else s_swap = (r != j) ? 1 : 0;
+      if (tid == 0) {
+        s_win_row = r;
+        s_win_cta = who;
+        if (ts) s_swap = v > fabs(urow[par * kLuMaxSb + jj]) ? 1 : 0;
+        else s_swap = (r != j) ? 1 : 0;
+      }
     }
     __syncthreads();
     const int wr = s_win_row, wc = s_win_cta;
@@ -206,18 +215,18 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
     __syncthreads();
     const double piv = s_piv;
     if (piv != 0.0) {
+      // each thread owns one row r and a 1/ngroup share of the columns; the
+      // multiplier is recomputed per group, so no barrier between scale and update
       const double rcp = 1.0 / piv;
-      const int w = sb - jj - 1;
-      // scale column jj of my rows, then rank-1 update of columns (jj, sb)
-      for (int r = tid; r < R; r += kLuThreads) {
-        const int gr = row0 + r;
-        if (ts || gr > j) s[jj * LD + r] *= rcp;
-      }
-      __syncthreads();
-      for (int e = tid; e < w * R; e += kLuThreads) {
-        const int c = jj + 1 + e / R, r = e % R;
-        const int gr = row0 + r;
-        if (ts || gr > j) s[c * LD + r] = fma(-s[jj * LD + r], prow[c], s[c * LD + r]);
+      const int ngroup = kLuThreads / R;
+      const int r = tid % R, grp = tid / R;
+      const int gr = row0 + r;
+      const bool act = grp < ngroup && (ts || gr > j);
+      const double l = act ? s[jj * LD + r] * rcp : 0.0;
+      __syncthreads();  // every group has read the unscaled value
+      if (act) {
+        for (int c = jj + 1 + grp; c < sb; c += ngroup) s[c * LD + r] = fma(-l, prow[c], s[c * LD + r]);
+        if (grp == 0) s[jj * LD + r] = l;
       }
     }
     __syncthreads();

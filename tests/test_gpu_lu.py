@@ -126,8 +126,10 @@ def test_lu_planned_factorization(k, devices):
     sd = lay.side_doubles
     gpu_tiles, gpu_side = {}, {}
     offs = np.cumsum([0] + [s // 8 for s in g.sizes])
-    for d in lay.tiles:
+    for d, (i, j) in lay.tiles.items():
         gpu_tiles[d] = out[offs[d]:offs[d + 1]].reshape(b, b, order="F").copy()
+        if i < j:
+            continue  # U tiles carry no side area
         s = side_out[d * sd:(d + 1) * sd]
         inv = s[: ib * b].reshape(ib, b, order="F")
         ipiv = s[ib * b:].view(np.int32)[:b].astype(np.int64)
