@@ -26,8 +26,8 @@ struct GemmCfg {
   static constexpr int FM = WM / 8, FN = WN / 8;  // 8x8 fragments per warp
   static constexpr int PAD = 4;
   // smem footprint of one operand slab for each layout
-  static constexpr int slab_mmaj(int rows) { return BK * (rows + PAD); }
-  static constexpr int slab_kmaj(int rows) { return rows * (BK + PAD); }
+  __host__ __device__ static constexpr int slab_mmaj(int rows) { return BK * (rows + PAD); }
+  __host__ __device__ static constexpr int slab_kmaj(int rows) { return rows * (BK + PAD); }
 };
 
 template <class Cfg, int LA, int LB>
@@ -156,6 +156,56 @@ HG_DEVICE void zero_acc(double (&acc)[Cfg::FM][Cfg::FN][2]) {
   for (int i = 0; i < Cfg::FM; ++i)
 #pragma unroll
     for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+}  // namespace hg
+
+namespace hg {
+
+// Main loop whose B operand is already resident in shared memory, stored as
+// sB[n * ldsb + k] (K-major rows of length >= k_end - k_begin, indexed from
+// k_begin).  Only A streams through the cp.async ring.
+template <class Cfg, class LdA>
+HG_DEVICE void gemm_mainloop_bsmem(double (&acc)[Cfg::FM][Cfg::FN][2], double* ring, const LdA& la,
+                                   const double* sB, int ldsb, int k_begin, int k_end) {
+  constexpr int LA = LdA::layout;
+  constexpr int A_SLAB = LA == M_MAJOR ? Cfg::slab_mmaj(Cfg::BM) : Cfg::slab_kmaj(Cfg::BM);
+  constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+  const int nk = (k_end - k_begin) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) la.load(ring + s * A_SLAB, k_begin + s * BK);
+    cp_async_commit();
+  }
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int nxt = it + STAGES - 1;
+      if (nxt < nk) la.load(ring + (nxt % STAGES) * A_SLAB, k_begin + nxt * BK);
+      cp_async_commit();
+    }
+    const double* a_s = ring + (it % STAGES) * A_SLAB;
+    const int kb = it * BK;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) af[i] = frag_at<Cfg, LA, Cfg::BM>(a_s, wm + i * 8 + g, kk + t);
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) bf[j] = sB[(wn + j * 8 + g) * ldsb + kb + kk + t];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
 }
 
 }  // namespace hg

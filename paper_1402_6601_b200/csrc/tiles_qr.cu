@@ -1,9 +1,394 @@
-// QR tile kernels (placeholder until the kernels land).
+// QR tile kernels for sm_100a: GEQRT, UNMQR, TSQRT, TSMQR (reference kinds
+// kernels.py:34-38, access lists kernels.py:192-211).  Semantics are LAPACK's
+// dgeqrt / dgemqrt / dtpqrt(l=0) / dtpmqrt(l=0) with block size ib (dlarfg
+// sign convention; T factors ib x nb in the tile's side area, panel p at
+// columns [p*ib, p*ib+sb), upper triangular, zeros below the diagonal).
+//
+//  k_qr_panel -- Householder factorization of one ib-wide panel by an
+//                8-CTA CLUSTER holding the panel rows in shared memory (CTA q
+//                owns rows [q*nb/8, (q+1)*nb/8)).  Per column: barrier 1
+//                publishes the partial squared norms (and alpha), every CTA
+//                forms the reflector identically (dlarfg); barrier 2
+//                publishes the partial products x^T [V | A] that give both
+//                the column update w and the T-factor inner products y.  The
+//                T factor is finished by CTA 0 from y and tau.
+//  k_qr_apply -- applies panels [p0, p1) to a column strip:
+//                  W = V^T C (UNMQR) or W = top + V_B^T bot (TSMQR),
+//                  W <- T^T W,  C -= V W  (resp. top -= W, bot -= V_B W),
+//                with W resident in shared memory and the masked unit-lower
+//                V blocks loaded element-wise on the diagonal slabs.
+#include <cooperative_groups.h>
+
+#include "dgemm_dmma.cuh"
 #include "tiles.h"
+
+namespace cg = cooperative_groups;
+
 namespace hg {
-bool init_qr_attributes() { return true; }
-bool build_qr_launches(int kind, const TaskOperands&, std::vector<LaunchDesc>&) {
-  set_error("kind %d: QR tile kernels are not built yet", kind);
-  return false;
+
+constexpr int kQrCl = 8;
+constexpr int kQrThreads = 256;
+constexpr int kQrMaxSb = 128;
+
+enum { QR_GEQRT = 0, QR_TSQRT = 1 };
+
+struct QrPanelParams {
+  double* A;     // GEQRT: A_kk; TSQRT: A_ik (the B part)
+  double* R;     // TSQRT: A_kk (R rows); GEQRT: unused
+  double* side;  // side area of A: T factors (ib x nb)
+  int nb, ib, ii, sb, mode;
+};
+
+__global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr_panel(QrPanelParams p) {
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const int nb = p.nb, sb = p.sb, ii = p.ii, ib = p.ib;
+  const int R = nb / kQrCl;
+  const int row0 = q * R;
+  const int LD = R + 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool ts = p.mode == QR_TSQRT;
+  double* s = sm;                          // s[c*LD + r]
+  double* pw = s + sb * LD;                // [2][sb] partial x^T [V | A]
+  double* rrow = pw + 2 * kQrMaxSb;        // [2][sb] TSQRT: R row j
+  double* wv = rrow + 2 * kQrMaxSb;        // [sb] reduced w / y
+  double* slot = wv + kQrMaxSb;            // [2][2]: partial norm^2, alpha (owner of row j)
+  __shared__ double s_red[kQrThreads / 32];
+  __shared__ double s_tau, s_beta, s_scal;
+  double* T = p.side + size_t(ii) * ib;    // this panel's ib x sb T block (ld = ib)
+  double* A = p.A;
+
+  for (int e = tid; e < sb * R; e += kQrThreads) {
+    int c = e / R, r = e % R;
+    int gr = row0 + r;
+    s[c * LD + r] = (ts || gr >= ii) ? A[size_t(ii + c) * nb + gr] : 0.0;
+  }
+  __syncthreads();
+
+  // partial ||x||^2 of column jj over my rows strictly below the diagonal row
+  auto publish_norm = [&](int jj, int par) {
+    const int j = ii + jj;
+    double acc = 0.0;
+    for (int r = tid; r < R; r += kQrThreads) {
+      int gr = row0 + r;
+      if (ts || gr > j) {
+        double v = s[jj * LD + r];
+        acc = fma(v, v, acc);
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) s_red[warp] = acc;
+    if (ts)
+      for (int c = tid; c < sb; c += kQrThreads) rrow[par * kQrMaxSb + c] = c >= jj ? p.R[size_t(ii + c) * nb + j] : 0.0;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kQrThreads / 32; ++w) t += s_red[w];
+      slot[par * 2 + 0] = t;
+      slot[par * 2 + 1] = (!ts && j >= row0 && j < row0 + R) ? s[jj * LD + (j - row0)] : 0.0;
+    }
+  };
+
+  publish_norm(0, 0);
+  for (int jj = 0; jj < sb; ++jj) {
+    const int j = ii + jj;
+    const int par = jj & 1;
+    cl.sync();  // barrier 1: norms + alpha of column jj
+    if (tid == 0) {
+      double xn2 = 0.0, alpha = 0.0;
+      const int owner = ts ? -1 : (j / R);
+      for (int c2 = 0; c2 < kQrCl; ++c2) {
+        const double* sl = cl.map_shared_rank(slot, c2) + par * 2;
+        xn2 += sl[0];
+        if (c2 == owner) alpha = sl[1];
+      }
+      if (ts) alpha = rrow[par * kQrMaxSb + jj];
+      double tau = 0.0, beta = alpha, scal = 1.0;
+      if (xn2 != 0.0) {
+        const double xnorm = sqrt(xn2);
+        beta = -copysign(hypot(alpha, xnorm), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      s_tau = tau;
+      s_beta = beta;
+      s_scal = scal;
+    }
+    __syncthreads();
+    const double tau = s_tau, beta = s_beta, scal = s_scal;
+    // scale my part of x; the owner of row j stores beta
+    for (int r = tid; r < R; r += kQrThreads) {
+      int gr = row0 + r;
+      if (ts || gr > j) s[jj * LD + r] *= scal;
+      else if (gr == j) s[jj * LD + r] = beta;
+    }
+    __syncthreads();
+    // partial products x^T [V | A] for every panel column c != jj
+    for (int c = warp; c < sb; c += kQrThreads / 32) {
+      double acc = 0.0;
+      if (c != jj) {
+        for (int r = lane; r < R; r += 32) {
+          int gr = row0 + r;
+          double v;
+          if (ts || gr > j) v = s[jj * LD + r];
+          else if (gr == j) v = 1.0;
+          else v = 0.0;
+          if (v != 0.0) {
+            // left columns hold stored reflectors (unit on their diagonal row)
+            double a = s[c * LD + r];
+            if (!ts && c < jj) a = (gr > ii + c) ? a : (gr == ii + c ? 1.0 : 0.0);
+            acc = fma(v, a, acc);
+          }
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) pw[par * kQrMaxSb + c] = acc;
+    }
+    cl.sync();  // barrier 2: partial products
+    for (int c = tid; c < sb; c += kQrThreads) {
+      double t = 0.0;
+      if (c != jj)
+        for (int c2 = 0; c2 < kQrCl; ++c2) t += cl.map_shared_rank(pw, c2)[par * kQrMaxSb + c];
+      if (ts && c > jj) t += rrow[par * kQrMaxSb + c];  // the unit of v_j sits in R row j
+      wv[c] = t;
+    }
+    __syncthreads();
+    // T column jj (y above the diagonal, tau on it) and the R row (TSQRT)
+    if (q == 0) {
+      for (int c = tid; c < ib; c += kQrThreads) T[size_t(jj) * ib + c] = c < jj ? wv[c] : (c == jj ? tau : 0.0);
+      if (ts)
+        for (int c = jj + tid; c < sb; c += kQrThreads)
+          p.R[size_t(ii + c) * nb + j] = (c == jj) ? beta : rrow[par * kQrMaxSb + c] - tau * wv[c];
+    }
+    // apply H_j to columns (jj, sb) of my rows
+    {
+      const int ngroup = kQrThreads / R;
+      const int r = tid % R, grp = tid / R;
+      const int gr = row0 + r;
+      if (grp < ngroup && tau != 0.0) {
+        double v;
+        if (ts || gr > j) v = s[jj * LD + r];
+        else if (gr == j) v = 1.0;
+        else v = 0.0;
+        if (v != 0.0) {
+          const double tv = tau * v;
+          for (int c = jj + 1 + grp; c < sb; c += ngroup) s[c * LD + r] = fma(-tv, wv[c], s[c * LD + r]);
+        }
+      }
+    }
+    __syncthreads();
+    if (jj + 1 < sb) publish_norm(jj + 1, par ^ 1);
+  }
+  __syncthreads();
+  for (int e = tid; e < sb * R; e += kQrThreads) {
+    int c = e / R, r = e % R;
+    int gr = row0 + r;
+    if (ts || gr >= ii) A[size_t(ii + c) * nb + gr] = s[c * LD + r];
+  }
+  __threadfence();
+  cl.sync();
+  if (q != 0) return;
+  // T from y and tau (dgeqrt2 / dtpqrt2 recurrence): T(0:j, j) = -tau_j T(0:j, 0:j) y(0:j, j)
+  double* Ts = s;  // [j][k] = T(k, j), ld sb+1
+  double* yv = s + sb * (sb + 1);
+  const int TL = sb + 1;
+  for (int e = tid; e < sb * sb; e += kQrThreads) {
+    int jc = e / sb, k = e % sb;
+    Ts[jc * TL + k] = __ldcg(T + size_t(jc) * ib + k);
+  }
+  __syncthreads();
+  for (int jc = 1; jc < sb; ++jc) {
+    for (int k = tid; k < jc; k += kQrThreads) yv[k] = Ts[jc * TL + k];
+    __syncthreads();
+    const double tj = Ts[jc * TL + jc];
+    for (int k = tid; k < jc; k += kQrThreads) {
+      double acc = 0.0;
+      for (int m = k; m < jc; ++m) acc = fma(Ts[m * TL + k], yv[m], acc);
+      Ts[jc * TL + k] = -tj * acc;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < sb * sb; e += kQrThreads) {
+    int jc = e / sb, k = e % sb;
+    T[size_t(jc) * ib + k] = Ts[jc * TL + k];
+  }
 }
+
+// ---------------------------------------------------------------------------
+using CfgQ = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps; requires sb == 128
+constexpr int kQrBN = 64;
+constexpr int kWld = kQrMaxSb + 4;  // W stored [n][k]
+
+// Unit-lower reflector block V of panel ii, element (tile row tr, panel col pc):
+//   tr > ii + pc: stored value, tr == ii + pc: 1, tr < ii + pc: 0.
+// L = K_MAJOR: operand rows = pc (r0 + rr), k = tr   (used for V^T)
+// L = M_MAJOR: operand rows = tr (r0 + rr), k = pc   (used for V)
+template <class Cfg, int L, int ROWS>
+struct VLoader {
+  static constexpr int layout = L;
+  static constexpr int rows = ROWS;
+  const double* v;  // tile + ii*nb: V(tr, pc) at v[pc*ld + tr]
+  int ld, r0, ii, masked;
+  HG_DEVICE double val(int tr, int pc) const {
+    if (!masked || tr > ii + pc) return v[size_t(pc) * ld + tr];
+    return tr == ii + pc ? 1.0 : 0.0;
+  }
+  HG_DEVICE void load(double* s, int k0) const {
+    constexpr int BK = Cfg::BK, PAD = Cfg::PAD;
+    bool diag;
+    if (L == K_MAJOR) diag = masked && k0 < ii + ROWS + r0 && k0 + BK > ii + r0;  // tr window vs ii+pc
+    else diag = masked && r0 < ii + k0 + BK && r0 + ROWS > ii + k0;
+    if (!diag) {
+      if (L == K_MAJOR) load_slab<Cfg, K_MAJOR, ROWS>(s, v, ld, r0, k0);  // element (pc, tr) at v[pc*ld + tr]
+      else load_slab<Cfg, M_MAJOR, ROWS>(s, v, ld, r0, k0);               // element (tr, pc) at v[pc*ld + tr]
+      return;
+    }
+    for (int e = threadIdx.x; e < ROWS * BK; e += Cfg::THREADS) {
+      int rr = e / BK, kk = e % BK;
+      if (L == K_MAJOR) s[rr * (BK + PAD) + kk] = val(k0 + kk, r0 + rr);
+      else s[kk * (ROWS + PAD) + rr] = val(r0 + rr, k0 + kk);
+    }
+  }
+};
+
+struct QrApplyParams {
+  const double* V;     // factor tile (GEQRT: A_kk; TSQRT: A_ik)
+  const double* side;  // its side area (T factors)
+  double* top;         // UNMQR: the tile C (rows [ii, nb)); TSMQR: A_kj (rows [ii, ii+sb))
+  double* bot;         // TSMQR: A_ij; UNMQR: unused
+  int nb, ib, p0, p1, col0, mode;
+};
+
+__global__ void __launch_bounds__(CfgQ::THREADS) k_qr_apply(QrApplyParams p) {
+  extern __shared__ double sm[];
+  double* ring = sm;
+  double* W = sm + GemmSmem<CfgQ, K_MAJOR, K_MAJOR>::DOUBLES;  // [n][k], ld kWld
+  const int nb = p.nb, ib = p.ib;
+  const int n0 = p.col0 + blockIdx.x * kQrBN;
+  const bool ts = p.mode == QR_TSQRT;
+  for (int P = p.p0; P < p.p1; ++P) {
+    const int ii = P * ib;
+    const double* Vp = p.V + size_t(ii) * nb;  // V(tr, pc) at Vp[pc*nb + tr]
+    // ---- W = V^T C   (UNMQR, K over tile rows [ii, nb))  |  top + V_B^T bot (TSMQR)
+    {
+      double acc[CfgQ::FM][CfgQ::FN][2];
+      zero_acc<CfgQ>(acc);
+      if (ts) {
+        VLoader<CfgQ, K_MAJOR, 128> la{Vp, nb, 0, ii, 0};
+        TileLoader<CfgQ, K_MAJOR, kQrBN> lb{p.bot, nb, n0};
+        gemm_mainloop<CfgQ>(acc, ring, la, lb, 0, nb);
+      } else {
+        VLoader<CfgQ, K_MAJOR, 128> la{Vp, nb, 0, ii, 1};
+        TileLoader<CfgQ, K_MAJOR, kQrBN> lb{p.top, nb, n0};
+        gemm_mainloop<CfgQ>(acc, ring, la, lb, ii, nb);
+      }
+      for_each_acc<CfgQ>(acc, [&](int r, int c, double v) {
+        if (ts) v += p.top[size_t(n0 + c) * nb + ii + r];
+        W[c * kWld + r] = v;
+      });
+    }
+    __syncthreads();
+    // ---- W <- T^T W  (T^T(r, k) = T(k, r) at side[(ii + r)*ib + k])
+    {
+      double acc[CfgQ::FM][CfgQ::FN][2];
+      zero_acc<CfgQ>(acc);
+      TileLoader<CfgQ, K_MAJOR, 128> la{p.side + size_t(ii) * ib, ib, 0};
+      gemm_mainloop_bsmem<CfgQ>(acc, ring, la, W, kWld, 0, 128);
+      for_each_acc<CfgQ>(acc, [&](int r, int c, double v) { W[c * kWld + r] = v; });
+    }
+    __syncthreads();
+    // ---- C -= V W  (UNMQR rows [ii, nb))  |  top -= W; bot -= V_B W (TSMQR)
+    if (ts) {
+      for (int e = threadIdx.x; e < 128 * kQrBN; e += CfgQ::THREADS) {
+        int c = e / 128, r = e % 128;
+        p.top[size_t(n0 + c) * nb + ii + r] -= W[c * kWld + r];
+      }
+    }
+    const int m_begin = ts ? 0 : ii;
+    for (int m0 = m_begin; m0 < nb; m0 += 128) {
+      double acc[CfgQ::FM][CfgQ::FN][2];
+      zero_acc<CfgQ>(acc);
+      VLoader<CfgQ, M_MAJOR, 128> la{Vp, nb, m0, ii, ts ? 0 : 1};
+      gemm_mainloop_bsmem<CfgQ>(acc, ring, la, W, kWld, 0, 128);
+      double* C = ts ? p.bot : p.top;
+      for_each_acc<CfgQ>(acc, [&](int r, int c, double v) { C[size_t(n0 + c) * nb + m0 + r] -= v; });
+    }
+    __threadfence();
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+static unsigned qr_panel_smem(int nb, int sb) {
+  const int R = nb / kQrCl;
+  size_t d = size_t(sb) * (R + 1);
+  size_t t = size_t(sb) * (sb + 1) + sb;
+  if (t > d) d = t;
+  d += 5 * kQrMaxSb + 4;
+  return unsigned(d * sizeof(double));
+}
+
+static unsigned qr_apply_smem() {
+  return unsigned((GemmSmem<CfgQ, K_MAJOR, K_MAJOR>::DOUBLES + kQrBN * kWld) * sizeof(double));
+}
+
+#define HG_QATTR(fn, attr, val)                                                                  \
+  do {                                                                                           \
+    cudaError_t e_ = cudaFuncSetAttribute(fn, attr, val);                                        \
+    if (e_ != cudaSuccess) {                                                                     \
+      set_error("cudaFuncSetAttribute(%s, %s, %d): %s", #fn, #attr, int(val), cudaGetErrorString(e_)); \
+      return false;                                                                              \
+    }                                                                                            \
+  } while (0)
+
+bool init_qr_attributes() {
+  HG_QATTR(k_qr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_panel_smem(1024, 128));
+  HG_QATTR(k_qr_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem());
+  return true;
+}
+
+bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out) {
+  const int nb = o.nb, ib = o.ib;
+  if (nb % 128 != 0 || nb > 1024 || ib != 128) {
+    set_error("QR tile kernels need nb %% 128 == 0, nb <= 1024 and ib == 128; got nb=%d ib=%d", nb, ib);
+    return false;
+  }
+  const size_t tile = size_t(nb) * nb;
+  const int np = nb / ib;
+  auto side = [&](int i) { return o.t[i] + tile; };
+  auto push_apply = [&](const QrApplyParams& ap) {
+    LaunchDesc d;
+    d.set((const void*)k_qr_apply, dim3((nb - ap.col0) / kQrBN), dim3(CfgQ::THREADS), qr_apply_smem(), ap);
+    out.push_back(d);
+  };
+  switch (kind) {
+    case K_GEQRT:
+    case K_TSQRT: {
+      const bool ts = kind == K_TSQRT;
+      double* A = ts ? o.t[1] : o.t[0];
+      for (int P = 0; P < np; ++P) {
+        QrPanelParams pp{A, ts ? o.t[0] : nullptr, ts ? side(1) : side(0), nb, ib, P * ib, ib,
+                         ts ? QR_TSQRT : QR_GEQRT};
+        LaunchDesc d;
+        d.set((const void*)k_qr_panel, dim3(kQrCl), dim3(kQrThreads), qr_panel_smem(nb, ib), pp);
+        out.push_back(d);
+        if (P + 1 < np)
+          push_apply(QrApplyParams{A, ts ? side(1) : side(0), ts ? o.t[0] : A, ts ? A : nullptr, nb, ib, P, P + 1,
+                                   (P + 1) * ib, ts ? QR_TSQRT : QR_GEQRT});
+      }
+      return true;
+    }
+    case K_UNMQR:
+      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], nullptr, nb, ib, 0, np, 0, QR_GEQRT});
+      return true;
+    case K_TSMQR:
+      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, QR_TSQRT});
+      return true;
+    default:
+      set_error("kind %d is not a QR kind", kind);
+      return false;
+  }
+}
+
 }  // namespace hg
