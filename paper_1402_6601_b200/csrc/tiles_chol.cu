@@ -5,15 +5,15 @@
 //
 //   GEMM  A_ij -= A_ik * A_jk^T            k_gemm_nt (full)      DMMA 64x64 CTA tiles
 //   SYRK  A_ii -= A_ik * A_ik^T  (lower)   k_gemm_nt (lower)     DMMA, upper CTAs exit
-//   TRSM  A_ik  = A_ik * L_kk^-T           k_trsm_wave           2-D wavefront, DMMA updates
+//   TRSM  A_ik  = A_ik * L_kk^-T           k_trsm_inv            DMMA product with M = L_kk^-1
 //   POTRF A_kk  = L_kk (lower)             k_potrf_cluster: one 16-CTA cluster kernel,
-//                                          r=64 right-looking blocked, lookahead diag
+//                                          r=64 right-looking blocked, lookahead diag,
+//                                          also accumulates M = L_kk^-1 (upper triangle)
 //
-// POTRF leaves inv(L_JJ)^T of each 64x64 diagonal block in that block's
-// strict upper triangle (the upper triangle of a Cholesky tile is never read
-// by any other kind), so TRSM applies the diagonal-block inverses with DMMA
-// instead of running a scalar substitution.  The upper triangle of diagonal
-// tiles is therefore workspace, not input, after POTRF.
+// POTRF leaves M^T = L_kk^-T in the strict upper triangle of the diagonal tile
+// (the upper triangle of a Cholesky tile is never read by any other kind), so
+// TRSM is a DMMA product instead of a substitution.  The upper triangle of
+// diagonal tiles is therefore workspace, not input, after POTRF.
 #include <cooperative_groups.h>
 
 #include <cmath>
@@ -260,105 +260,16 @@ __global__ void __launch_bounds__(256) k_potrf_diag(PotrfDiagParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// TRSM  X * L^T = B  (X overwrites B) as a 2-D wavefront over 64x64 blocks:
-//   X(I, J) = (B(I, J) - sum_{K<J} X(I, K) L(J, K)^T) * inv(L_JJ)^T
-// Row strips I are independent; inside a strip block J needs X(I, K < J).
-// CTA (I, J) (linear id J*nI + I, so every producer is dispatched before its
-// consumers) streams its DMMA update over whichever K blocks are already
-// final, waiting on per-block flags, then applies inv(L_JJ)^T from smem and
-// publishes X(I, J).  Flags live in per-task scratch and advance by one per
-// run (CTA (I, J) is the only writer of flag(I, J)), so no reset is needed.
-struct TrsmWaveParams {
-  const double* L;  // tile holding L (and inv(L_JJ)^T in its diagonal blocks' upper triangles)
-  double* B;        // tile solved in place
-  int* flags;       // [nI][nJ] per-task scratch
-  int ld;
-};
-
-constexpr int kWaveS = kR * (kR + 4);
-constexpr int kWaveSmemDoubles =
-    (2 * kWaveS > GemmSmem<CfgG, M_MAJOR, M_MAJOR>::DOUBLES) ? 2 * kWaveS : GemmSmem<CfgG, M_MAJOR, M_MAJOR>::DOUBLES;
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__global__ void __launch_bounds__(CfgG::THREADS) k_trsm_wave(TrsmWaveParams p) {
-  extern __shared__ double smem[];
-  __shared__ int s_hi;
-  const int ld = p.ld, nI = ld / kR, nJ = ld / kR;
-  const int J = blockIdx.x / nI, I = blockIdx.x % nI;
-  const int tid = threadIdx.x;
-  int* flag = p.flags + I * nJ;
-  const int gen = ld_acquire(flag + J) + 1;  // this run's generation
-  double acc[CfgG::FM][CfgG::FN][2];
-  zero_acc<CfgG>(acc);
-  TileLoader<CfgG, M_MAJOR, CfgG::BM> la{p.B, ld, I * kR};
-  TileLoader<CfgG, M_MAJOR, CfgG::BN> lb{p.L, ld, J * kR};
-  int done = 0;
-  while (done < J) {
-    if (tid == 0) {
-      while (ld_acquire(flag + done) < gen) __nanosleep(64);
-      int hi = done + 1;
-      while (hi < J && ld_acquire(flag + hi) >= gen) ++hi;
-      s_hi = hi;
-    }
-    __syncthreads();
-    const int hi = s_hi;
-    gemm_mainloop<CfgG>(acc, smem, la, lb, done * kR, hi * kR);
-    done = hi;
-  }
-  // residual -> sS[k][row]; inv(L_JJ) -> sI[j][k]
-  double* sS = smem;
-  double* sI = smem + kWaveS;
-  double* Bb = p.B + size_t(J) * kR * ld + size_t(I) * kR;
-  for_each_acc<CfgG>(acc, [&](int r, int c, double v) { sS[c * (kR + 4) + r] = __ldcg(Bb + size_t(c) * ld + r) - v; });
-  const double* Lb = p.L + size_t(J) * kR * ld + size_t(J) * kR;
-  for (int e = tid; e < kR * kR; e += CfgG::THREADS) {
-    int j = e / kR, k = e % kR;
-    double v;
-    if (k < j) v = __ldcg(Lb + size_t(j) * ld + k);
-    else if (k == j) v = 1.0 / __ldcg(Lb + size_t(j) * ld + j);
-    else v = 0.0;
-    sI[j * (kR + 4) + k] = v;
-  }
-  __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
-  const int wm = (warp % CfgG::WARPS_M) * CfgG::WM;
-  const int wn = (warp / CfgG::WARPS_M) * CfgG::WN;
-  const int g = lane >> 2, t = lane & 3;
-  double acc2[CfgG::FM][CfgG::FN][2];
-  zero_acc<CfgG>(acc2);
-#pragma unroll 4
-  for (int kk = 0; kk < kR; kk += 4) {
-    double af[CfgG::FM], bf[CfgG::FN];
-#pragma unroll
-    for (int i = 0; i < CfgG::FM; ++i) af[i] = sS[(kk + t) * (kR + 4) + wm + i * 8 + g];
-#pragma unroll
-    for (int j = 0; j < CfgG::FN; ++j) bf[j] = sI[(wn + j * 8 + g) * (kR + 4) + kk + t];
-#pragma unroll
-    for (int i = 0; i < CfgG::FM; ++i)
-#pragma unroll
-      for (int j = 0; j < CfgG::FN; ++j) dmma_8x8x4(acc2[i][j][0], acc2[i][j][1], af[i], bf[j]);
-  }
-  for_each_acc<CfgG>(acc2, [&](int r, int c, double v) { Bb[size_t(c) * ld + r] = v; });
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) st_release(flag + J, gen);
-}
-
-// ---------------------------------------------------------------------------
 // POTRF of a whole nb x nb tile as ONE thread-block-cluster kernel (16 CTAs,
-// non-portable size): r=64 right-looking blocked Cholesky with cluster
-// barriers between the panel solve and the trailing update.  CTA 0 updates
-// the next diagonal block first and factors it (plus its inverse) while the
-// other 15 CTAs finish the trailing update (lookahead), so the latency-bound
-// 64x64 factorization hides behind DMMA work.
+// non-portable size), r = 64 right-looking blocked Cholesky that ALSO
+// accumulates M = L^{-1} (stored transposed in the tile's strict upper
+// triangle, diagonal implicit 1/L(j,j)) so that every TRSM of this column is
+// a plain DMMA product X = B M^T.  Per step J (cluster barriers between):
+//   P: L(I,J) = A(I,J) inv(L_JJ)^T (I > J)   and   M(J,K) <- inv(L_JJ) M(J,K) (K < J)
+//   U: A(I,K) -= L(I,J) L(K,J)^T (J < K <= I) and   M(I,K) -= L(I,J) M(J,K) (I > J, K <= J)
+// CTA 0 updates the next diagonal block first and factors it (lookahead) while
+// the other CTAs finish U.  M starts as the identity, so M(I,J) for K == J is
+// initialised (=) instead of accumulated.
 constexpr int kPotrfCl = 16;
 
 struct PotrfParams {
@@ -372,17 +283,15 @@ constexpr int kPotrfSmemDoubles =
     (2 * kSolveS > GemmSmem<CfgG, M_MAJOR, M_MAJOR>::DOUBLES) ? 2 * kSolveS : GemmSmem<CfgG, M_MAJOR, M_MAJOR>::DOUBLES;
 constexpr int kPotrfDynDoubles = kPotrfSmemDoubles + 2 * kR * (kR + 1) + 32 * 33;
 
-// X = A(I rows, J cols) * inv(L_JJ)^T in place (one 64x64 block, from smem).
-__device__ void potrf_solve_block(double* A, int ld, int I, int J, double* smem) {
+// blk (64x64, ld) <- blk * inv(L_JJ)^T in place; inv(L_JJ)(j, k), k < j, sits at
+// diagonal-block position (row k, col j), its diagonal is 1/L(j, j).
+__device__ void apply_inv_right(double* blk, int ld, const double* Lb, double* smem) {
   double* sS = smem;            // [k][row], ld kR+4
   double* sI = smem + kSolveS;  // [j][k],  ld kR+4
   const int tid = threadIdx.x;
-  const double* blk = A + size_t(J) * kR * ld + size_t(I) * kR;
-  const double* Lb = A + size_t(J) * kR * ld + size_t(J) * kR;
   for (int e = tid; e < kR * kR; e += CfgG::THREADS) {
     int c = e / kR, r = e % kR;
     sS[c * (kR + 4) + r] = __ldcg(blk + size_t(c) * ld + r);
-    // inverse element (j=c, k=r): k < j in the upper triangle, diag = 1/L(j,j)
     double v;
     if (r < c) v = __ldcg(Lb + size_t(c) * ld + r);
     else if (r == c) v = 1.0 / __ldcg(Lb + size_t(c) * ld + c);
@@ -408,24 +317,42 @@ __device__ void potrf_solve_block(double* A, int ld, int I, int J, double* smem)
 #pragma unroll
       for (int j = 0; j < CfgG::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
   }
-  double* out = A + size_t(J) * kR * ld + size_t(I) * kR;
-  for_each_acc<CfgG>(acc, [&](int r, int c, double v) { out[size_t(c) * ld + r] = v; });
+  for_each_acc<CfgG>(acc, [&](int r, int c, double v) { blk[size_t(c) * ld + r] = v; });
   __syncthreads();
 }
 
-// A(I, K) -= X_I * X_K^T with X = column block J (lower only when I == K).
-__device__ void potrf_update_tile(double* A, int ld, int I, int K, int J, double* smem) {
+// inv(L_JJ)^T as an M_MAJOR operand: element (r, k) = inv(k, r): k > r stored at
+// (row r, col k), k == r -> 1/L(r, r), k < r -> 0
+template <class Cfg, int ROWS>
+struct InvTLoader {
+  static constexpr int layout = M_MAJOR;
+  static constexpr int rows = ROWS;
+  const double* blk;  // diagonal block base, ld
+  int ld;
+  HG_DEVICE void load(double* s, int k0) const {
+    for (int e = threadIdx.x; e < ROWS * Cfg::BK; e += Cfg::THREADS) {
+      int kk = e / ROWS, rr = e % ROWS;
+      int k = k0 + kk;
+      double v;
+      if (k > rr) v = __ldcg(blk + size_t(k) * ld + rr);
+      else if (k == rr) v = 1.0 / __ldcg(blk + size_t(rr) * ld + rr);
+      else v = 0.0;
+      s[kk * (ROWS + Cfg::PAD) + rr] = v;
+    }
+  }
+};
+
+// C(64x64 at Cp, ld) (-)= A_op * B_op^T, optional lower mask / initialisation
+template <class LdA, class LdB>
+__device__ void block_update(double* Cp, int ld, const LdA& la, const LdB& lb, bool lower, bool init,
+                             double* smem) {
   double acc[CfgG::FM][CfgG::FN][2];
   zero_acc<CfgG>(acc);
-  const double* X = A + size_t(J) * kR * ld;
-  TileLoader<CfgG, M_MAJOR, CfgG::BM> la{X, ld, I * kR};
-  TileLoader<CfgG, M_MAJOR, CfgG::BN> lb{X, ld, K * kR};
   gemm_mainloop<CfgG>(acc, smem, la, lb, 0, kR);
-  double* C = A + size_t(K) * kR * ld + size_t(I) * kR;
-  const bool diag = I == K;
   for_each_acc<CfgG>(acc, [&](int r, int c, double v) {
-    if (diag && r < c) return;
-    C[size_t(c) * ld + r] -= v;
+    if (lower && r < c) return;
+    double* q = Cp + size_t(c) * ld + r;
+    *q = init ? -v : *q - v;
   });
   __syncthreads();
 }
@@ -438,26 +365,51 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
   auto tm = reinterpret_cast<double(*)[33]>(smem + kPotrfSmemDoubles + 2 * kR * (kR + 1));
   cg::cluster_group cl = cg::this_cluster();
   const int q = (int)cl.block_rank();
-  const int nb = p.nb, nJ = nb / kR;
-  if (q == 0) diag_factor_inverse_fast<CfgG::THREADS>(p.A, nb, 0, p.status, s, iv, tm);
+  const int nb = p.nb, nJ = nb / kR, ld = nb;
+  double* A = p.A;
+  auto blk = [&](int I, int K) { return A + size_t(K) * kR * ld + size_t(I) * kR; };  // block (I, K)
+  if (q == 0) diag_factor_inverse_fast<CfgG::THREADS>(A, nb, 0, p.status, s, iv, tm);
   __threadfence();
   cl.sync();
   for (int J = 0; J < nJ; ++J) {
-    for (int I = J + 1 + q; I < nJ; I += kPotrfCl) potrf_solve_block(p.A, nb, I, J, smem);
+    // ---- P: panel solve (I > J) and M row scaling (K < J): nJ-1 tasks -------------
+    for (int t = q; t < nJ - 1; t += kPotrfCl) {
+      if (t < nJ - 1 - J) apply_inv_right(blk(J + 1 + t, J), ld, blk(J, J), smem);
+      else apply_inv_right(blk(t - (nJ - 1 - J), J), ld, blk(J, J), smem);  // upper block (K, J) = M(J,K)^T
+    }
     __threadfence();
     cl.sync();
     if (J + 1 == nJ) break;
-    // trailing tiles (I, K), J < K <= I < nJ; tile 0 is (J+1, J+1)
+    // ---- U: trailing lower tiles + M accumulation tiles ----------------------------
     if (q == 0) {
-      potrf_update_tile(p.A, nb, J + 1, J + 1, J, smem);
+      TileLoader<CfgG, M_MAJOR, kR> la{blk(0, J), ld, (J + 1) * kR};
+      block_update(blk(J + 1, J + 1), ld, la, la, true, false, smem);
       __threadfence();
-      diag_factor_inverse_fast<CfgG::THREADS>(p.A, nb, (J + 1) * kR, p.status, s, iv, tm);
+      diag_factor_inverse_fast<CfgG::THREADS>(A, nb, (J + 1) * kR, p.status, s, iv, tm);
     } else {
       int t = 0;
+      const int others = kPotrfCl - 1;
+      // (iii) A(I,K) -= L(I,J) L(K,J)^T, J < K <= I, skipping (J+1, J+1)
       for (int I = J + 1; I < nJ; ++I)
-        for (int K = J + 1; K <= I; ++K, ++t) {
-          if (t == 0) continue;
-          if ((t - 1) % (kPotrfCl - 1) == q - 1) potrf_update_tile(p.A, nb, I, K, J, smem);
+        for (int K = J + 1; K <= I; ++K) {
+          if (I == J + 1 && K == J + 1) continue;
+          if (t++ % others != q - 1) continue;
+          TileLoader<CfgG, M_MAJOR, kR> la{blk(0, J), ld, I * kR};
+          TileLoader<CfgG, M_MAJOR, kR> lb{blk(0, J), ld, K * kR};
+          block_update(blk(I, K), ld, la, lb, I == K, false, smem);
+        }
+      // (iv) M(I,K)^T (upper block (K, I)) -= M(J,K)^T L(I,J)^T, I > J, K <= J
+      for (int I = J + 1; I < nJ; ++I)
+        for (int K = 0; K <= J; ++K) {
+          if (t++ % others != q - 1) continue;
+          TileLoader<CfgG, M_MAJOR, kR> lb{blk(0, J), ld, I * kR};
+          if (K == J) {
+            InvTLoader<CfgG, kR> la{blk(J, J), ld};
+            block_update(blk(K, I), ld, la, lb, false, true, smem);
+          } else {
+            TileLoader<CfgG, M_MAJOR, kR> la{blk(0, J), ld, K * kR};  // upper block (K, J) rows
+            block_update(blk(K, I), ld, la, lb, false, false, smem);
+          }
         }
     }
     __threadfence();
@@ -466,8 +418,83 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
 }
 
 // ---------------------------------------------------------------------------
+// TRSM  B <- B L^{-T} = B M^T with M = L^{-1} from POTRF (upper triangle of the
+// diagonal tile, transposed; diagonal 1/L(j,j)).  A plain DMMA product per
+// 64x64 block X(I, J) = sum_{K <= J} B(I, K) M(J, K)^T.  In place: X(I, J)
+// may only be written once every CTA of row strip I has finished reading B,
+// so each CTA computes two blocks (J, nJ-1-J: equal work), then meets the
+// other CTAs of its strip on a self-advancing counter, then writes.
+struct TrsmInvParams {
+  const double* L;  // diagonal tile after POTRF (M^T in its upper triangle)
+  double* B;
+  int* count;       // [nI] per-task scratch
+  int ld;
+};
+
+template <class Cfg, int ROWS>
+struct MRowLoader {  // rows j in [j0, j0+ROWS): element (j, k) = M(j, k)
+  static constexpr int layout = K_MAJOR;
+  static constexpr int rows = ROWS;
+  const double* L;
+  int ld, j0;
+  HG_DEVICE void load(double* s, int k0) const {
+    if (k0 + Cfg::BK <= j0) {  // strictly left of the diagonal block: plain upper-triangle rows
+      load_slab<Cfg, K_MAJOR, ROWS>(s, L, ld, j0, k0);
+      return;
+    }
+    for (int e = threadIdx.x; e < ROWS * Cfg::BK; e += Cfg::THREADS) {
+      int rr = e / Cfg::BK, kk = e % Cfg::BK;
+      int j = j0 + rr, k = k0 + kk;
+      double v;
+      if (k < j) v = __ldcg(L + size_t(j) * ld + k);
+      else if (k == j) v = 1.0 / __ldcg(L + size_t(j) * ld + j);
+      else v = 0.0;
+      s[rr * (Cfg::BK + Cfg::PAD) + kk] = v;
+    }
+  }
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(CfgG::THREADS) k_trsm_inv(TrsmInvParams p) {
+  extern __shared__ double smem[];
+  const int ld = p.ld, nI = ld / kR, nJ = ld / kR, P = nJ / 2;
+  const int I = blockIdx.x % nI, pair = blockIdx.x / nI;
+  const int Js[2] = {pair, nJ - 1 - pair};
+  double acc0[CfgG::FM][CfgG::FN][2], acc1[CfgG::FM][CfgG::FN][2];
+  zero_acc<CfgG>(acc0);
+  zero_acc<CfgG>(acc1);
+  TileLoader<CfgG, M_MAJOR, kR> la{p.B, ld, I * kR};
+  {
+    MRowLoader<CfgG, kR> lb{p.L, ld, Js[0] * kR};
+    gemm_mainloop<CfgG>(acc0, smem, la, lb, 0, (Js[0] + 1) * kR);
+  }
+  {
+    MRowLoader<CfgG, kR> lb{p.L, ld, Js[1] * kR};
+    gemm_mainloop<CfgG>(acc1, smem, la, lb, 0, (Js[1] + 1) * kR);
+  }
+  // all reads of B by this CTA are complete (mainloop ends with wait_group 0 + barrier)
+  __shared__ int s_go;
+  if (threadIdx.x == 0) {
+    int* cnt = p.count + I;
+    const int old = atomicAdd(cnt, 1);
+    const int target = (old / P + 1) * P;
+    while (ld_acquire(cnt) < target) __nanosleep(32);
+    s_go = 1;
+  }
+  __syncthreads();
+  double* B = p.B;
+  for_each_acc<CfgG>(acc0, [&](int r, int c, double v) { B[size_t(Js[0] * kR + c) * ld + I * kR + r] = v; });
+  for_each_acc<CfgG>(acc1, [&](int r, int c, double v) { B[size_t(Js[1] * kR + c) * ld + I * kR + r] = v; });
+}
+
+// ---------------------------------------------------------------------------
 static unsigned gemm_smem() { return (unsigned)GemmSmem<CfgG, M_MAJOR, M_MAJOR>::BYTES; }
-static unsigned trsm_smem() { return (unsigned)(kWaveSmemDoubles * sizeof(double)); }
+static unsigned trsm_smem() { return (unsigned)GemmSmem<CfgG, M_MAJOR, K_MAJOR>::BYTES; }
 
 #define HG_ATTR(fn, attr, val)                                                                   \
   do {                                                                                           \
@@ -480,7 +507,7 @@ static unsigned trsm_smem() { return (unsigned)(kWaveSmemDoubles * sizeof(double
 
 bool init_chol_attributes() {
   HG_ATTR(k_gemm_nt, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem());
-  HG_ATTR(k_trsm_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
+  HG_ATTR(k_trsm_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
   HG_ATTR(k_potrf_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPotrfDynDoubles * sizeof(double)));
   HG_ATTR(k_potrf_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return true;
@@ -495,7 +522,7 @@ static void push_gemm(std::vector<LaunchDesc>& out, const double* A, const doubl
 }
 
 int chol_scratch_ints(int kind, int nb) {
-  return kind == K_TRSM ? (nb / kR) * (nb / kR) : 0;
+  return kind == K_TRSM ? (nb / kR) : 0;
 }
 
 bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out) {
@@ -516,12 +543,16 @@ bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc
     }
     case K_TRSM: {
       if (!o.scratch) {
-        set_error("TRSM needs per-task scratch (%d ints)", nJ * nJ);
+        set_error("TRSM needs per-task scratch (%d ints)", nJ);
+        return false;
+      }
+      if (nJ % 2) {
+        set_error("TRSM needs an even number of 64-blocks per tile (nb=%d)", nb);
         return false;
       }
       LaunchDesc d;
-      TrsmWaveParams tp{o.t[0], o.t[1], o.scratch, nb};
-      d.set((const void*)k_trsm_wave, dim3(nJ * nJ), dim3(CfgG::THREADS), trsm_smem(), tp);
+      TrsmInvParams tp{o.t[0], o.t[1], o.scratch, nb};
+      d.set((const void*)k_trsm_inv, dim3(nJ * (nJ / 2)), dim3(CfgG::THREADS), trsm_smem(), tp);
       out.push_back(d);
       return true;
     }
