@@ -170,7 +170,10 @@ typedef struct hg_exec_opts {
   double* host_side_out;      /* optional: side areas of final tiles, n_blocks*side_doubles */
   int32_t device_input;       /* 1: keep a replica of host_in in each GPU's HBM and serve
                                  the plan's H2D jobs from it (inputs resident in HBM) */
-  int32_t reserved;
+  int32_t rank_node;          /* 0: this process drives every GPU node (one CUDA graph over all
+                                 devices).  r+1: one process per GPU -- this process executes
+                                 node r+1 only; exchange pools with hg_exec_ipc_handle /
+                                 hg_exec_ipc_open, then hg_exec_build */
 } hg_exec_opts;
 
 typedef struct hg_exec hg_exec;
@@ -186,6 +189,18 @@ typedef struct hg_exec_stats {
 } hg_exec_stats;
 
 int hg_exec_create(const hg_exec_plan* plan, const hg_exec_opts* opts, hg_exec** out);
+/* one-process-per-GPU mode: export this rank's pool (64-byte cudaIpcMemHandle),
+ * map a peer node's pool, then build the rank-local graph.  Cross-rank
+ * dependencies are device flags (release/acquire, system scope) carrying the
+ * run's epoch. */
+int hg_exec_ipc_handle(hg_exec* ex, void* handle64);
+int hg_exec_ipc_open(hg_exec* ex, int32_t node, const void* handle64);
+int hg_exec_build(hg_exec* ex);
+/* CPU-only dry run of the per-rank partition: counts4 = {local tasks, local
+ * copy jobs, remote flags waited on, flags signalled}; optional id lists
+ * (capacity n_tasks + n_jobs; flag id = task id, or n_tasks + job id) */
+int hg_exec_partition(const hg_exec_plan* plan, int32_t rank_node, int32_t* counts4, int32_t* waits,
+                      int32_t* signals);
 int hg_exec_run(hg_exec* ex, hg_exec_stats* stats);
 /* asynchronous variant: launch on exactly `stream` (NULL = legacy default stream), then wait */
 int hg_exec_launch(hg_exec* ex, void* stream);

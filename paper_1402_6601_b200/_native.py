@@ -71,7 +71,7 @@ class ExecPlan(C.Structure):
 
 class ExecOpts(C.Structure):
     _fields_ = [("devices", _i32p), ("host_in", _f64p), ("host_out", _f64p), ("host_side_out", _f64p),
-                ("device_input", C.c_int32), ("reserved", C.c_int32)]
+                ("device_input", C.c_int32), ("rank_node", C.c_int32)]
 
 
 class ExecStats(C.Structure):
@@ -82,7 +82,8 @@ class ExecStats(C.Structure):
 
 EXPORTS = ("hg_last_error", "hg_abi_version", "hg_device_count", "hg_plan_build", "hg_plan_free",
            "hg_pysum", "hg_exec_create", "hg_exec_run", "hg_exec_read_block", "hg_exec_destroy",
-           "hg_tile_run", "hg_exec_launch", "hg_exec_wait", "hg_exec_info", "hg_fp64_peak")
+           "hg_tile_run", "hg_exec_launch", "hg_exec_wait", "hg_exec_info", "hg_fp64_peak",
+           "hg_exec_ipc_handle", "hg_exec_ipc_open", "hg_exec_build", "hg_exec_partition")
 
 _lib = None
 
@@ -118,6 +119,10 @@ def lib():
     L.hg_exec_wait.argtypes = [C.c_void_p]
     L.hg_exec_info.argtypes = [C.c_void_p, C.POINTER(ExecStats)]
     L.hg_fp64_peak.argtypes = [C.c_int32, _f64p, _f64p]
+    L.hg_exec_ipc_handle.argtypes = [C.c_void_p, C.c_void_p]
+    L.hg_exec_ipc_open.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+    L.hg_exec_build.argtypes = [C.c_void_p]
+    L.hg_exec_partition.argtypes = [C.POINTER(ExecPlan), C.c_int32, _i32p, _i32p, _i32p]
     _lib = L
     return L
 

@@ -163,18 +163,77 @@ int hg_tile_run(int32_t kind, int32_t device, void* stream, double* const* t, in
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
+// Executor.  Two modes share one graph builder:
+//  * single process (opts.rank_node == 0): every GPU node is local; one CUDA
+//    graph spans all devices and cross-device ordering is plain graph edges;
+//  * one process per GPU (opts.rank_node == r+1): the process builds only its
+//    node's tasks and inbound copy jobs.  Peer slot pools are mapped with CUDA
+//    IPC (hg_exec_ipc_handle / hg_exec_ipc_open), and every dependency that
+//    crosses processes becomes a device flag in the producer's pool header:
+//    the producer's graph ends the task/job with a release store of the run's
+//    epoch, the consumer's graph waits for it with an acquire spin before the
+//    copy / kernel that needs it.
+// Pool layout per node: [flag header: int task_flag[n_tasks], job_flag[n_jobs],
+// epoch; 256-byte aligned] [slots of every block the plan ever places there].
+
+namespace hg {
+
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct FlagParams {
+  int* flag;
+  const int* epoch;
+};
+
+__global__ void k_wait_flag(FlagParams p) {
+  if (threadIdx.x == 0) {
+    const int e = *reinterpret_cast<volatile const int*>(p.epoch);
+    while (ld_acquire_sys(p.flag) < e) __nanosleep(256);
+  }
+}
+
+__global__ void k_signal_flag(FlagParams p) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(p.flag, *reinterpret_cast<volatile const int*>(p.epoch));
+  }
+}
+
+__global__ void k_set_epoch(int* epoch, int v) {
+  if (threadIdx.x == 0) *epoch = v;
+}
+
+}  // namespace hg
+
 struct hg_exec {
-  int k = 0, nb = 0, ib = 0, side = 0;
-  int n_blocks = 0;
+  // plan (owned copy)
+  int k = 0, nb = 0, ib = 0, side = 0, n_blocks = 0, n_tasks = 0, n_jobs = 0;
+  std::vector<int32_t> task_kind, task_node, acc_block, pred, dispatch, wait_job;
+  std::vector<int64_t> acc_ptr, pred_ptr, wait_ptr, block_bytes;
+  std::vector<int32_t> job_block, job_src, job_dst, job_version, job_src_job, job_requester, final_writer;
+  // options
+  int rank_node = 0;
+  const double* host_in = nullptr;
+  double* host_out = nullptr;
+  double* host_side_out = nullptr;
+  int device_input = 0;
+  // memory
   std::vector<int> dev;                 // node g+1 -> device
-  std::vector<double*> pool;            // per GPU node
-  std::vector<double*> replica;         // per GPU node: device copy of host_in (device_input)
-  std::vector<int*> status;             // per GPU node
-  std::vector<int*> scratch;            // per GPU node: per-task scratch ints
-  std::vector<std::vector<int64_t>> slot;  // [node-1][block] -> offset in doubles, -1 = none
-  std::vector<int64_t> host_off;        // doubles offset of each block in the host image
-  std::vector<int64_t> blk_doubles;     // host-image doubles per block
-  std::vector<int64_t> slot_doubles;    // device slot doubles per block
+  std::vector<double*> base;            // per node: pool base (local allocation or IPC mapping)
+  std::vector<char> ipc;                // per node: base came from cudaIpcOpenMemHandle
+  std::vector<double*> replica;         // per local node: device copy of host_in
+  std::vector<int*> status, scratch;    // per local node
+  std::vector<std::vector<int64_t>> slot;  // [node-1][block] -> doubles offset, -1 = none
+  std::vector<int64_t> pool_doubles;    // per node
+  int64_t header_doubles = 0;
+  std::vector<int64_t> host_off, blk_doubles, slot_doubles;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaStream_t stream = nullptr;
@@ -182,6 +241,18 @@ struct hg_exec {
   hg_exec_stats stats{};
   cudaStream_t last_stream = nullptr;
   bool launched = false;
+  int epoch = 0;
+  bool built = false;
+
+  bool is_local(int node) const { return node >= 1 && node <= k && (rank_node == 0 || node == rank_node); }
+  int* flags(int node) const { return reinterpret_cast<int*>(base[node - 1]); }
+  int* task_flag(int node, int t) const { return flags(node) + t; }
+  int* job_flag(int node, int j) const { return flags(node) + n_tasks + j; }
+  int* epoch_ptr(int node) const { return flags(node) + n_tasks + n_jobs; }
+  double* slot_ptr(int node, int b) const {
+    int64_t off = slot[node - 1][b];
+    return off < 0 ? nullptr : base[node - 1] + off;
+  }
 };
 
 static void release(hg_exec* ex) {
@@ -189,11 +260,15 @@ static void release(hg_exec* ex) {
   if (ex->exec) cudaGraphExecDestroy(ex->exec);
   if (ex->graph) cudaGraphDestroy(ex->graph);
   for (int g = 0; g < ex->k; ++g) {
+    if (g >= (int)ex->base.size()) break;
     cudaSetDevice(ex->dev[g]);
-    if (g < (int)ex->pool.size() && ex->pool[g]) cudaFree(ex->pool[g]);
-    if (g < (int)ex->replica.size() && ex->replica[g]) cudaFree(ex->replica[g]);
-    if (g < (int)ex->status.size() && ex->status[g]) cudaFree(ex->status[g]);
-    if (g < (int)ex->scratch.size() && ex->scratch[g]) cudaFree(ex->scratch[g]);
+    if (ex->base[g]) {
+      if (ex->ipc[g]) cudaIpcCloseMemHandle(ex->base[g]);
+      else cudaFree(ex->base[g]);
+    }
+    if (ex->replica[g]) cudaFree(ex->replica[g]);
+    if (ex->status[g]) cudaFree(ex->status[g]);
+    if (ex->scratch[g]) cudaFree(ex->scratch[g]);
   }
   if (ex->ev0) cudaEventDestroy(ex->ev0);
   if (ex->ev1) cudaEventDestroy(ex->ev1);
@@ -201,52 +276,179 @@ static void release(hg_exec* ex) {
   delete ex;
 }
 
-static int build_graph(hg_exec* ex, const hg_exec_plan* P, const hg_exec_opts* O) {
-  const int n = P->n_tasks;
+// Deterministic per-node layout (every process computes every node's).
+static void plan_layout(hg_exec* ex) {
+  const int64_t tile_d = int64_t(ex->nb) * ex->nb;
+  ex->host_off.resize(ex->n_blocks);
+  ex->blk_doubles.resize(ex->n_blocks);
+  ex->slot_doubles.resize(ex->n_blocks);
+  int64_t host_total = 0;
+  for (int b = 0; b < ex->n_blocks; ++b) {
+    ex->blk_doubles[b] = ex->block_bytes[b] / 8;
+    ex->slot_doubles[b] = ex->blk_doubles[b] + (ex->blk_doubles[b] == tile_d ? ex->side : 0);
+    ex->host_off[b] = host_total;
+    host_total += ex->blk_doubles[b];
+  }
+  const int64_t flag_ints = int64_t(ex->n_tasks) + ex->n_jobs + 1;
+  ex->header_doubles = ((flag_ints * 4 + 255) / 256) * 32;
+  ex->slot.assign(ex->k, std::vector<int64_t>(ex->n_blocks, -1));
+  ex->pool_doubles.assign(ex->k, ex->header_doubles);
+  auto need = [&](int node, int b) {
+    if (node < 1 || node > ex->k) return;
+    int64_t& s = ex->slot[node - 1][b];
+    if (s < 0) {
+      s = ex->pool_doubles[node - 1];
+      ex->pool_doubles[node - 1] += (ex->slot_doubles[b] + 31) / 32 * 32;  // 256-byte aligned slots
+    }
+  };
+  for (int t = 0; t < ex->n_tasks; ++t)
+    for (int64_t a = ex->acc_ptr[t]; a < ex->acc_ptr[t + 1]; ++a) need(ex->task_node[t], ex->acc_block[a]);
+  for (int j = 0; j < ex->n_jobs; ++j) need(ex->job_dst[j], ex->job_block[j]);
+}
+
+// Which producers must signal (consumer on another, non-local node) and which
+// consumers must wait (producer on another, non-local node).
+struct Partition {
+  std::vector<char> sig_task, sig_job, waited;  // waited: [n_tasks + n_jobs] flags this rank spins on
+  int n_local_tasks = 0, n_local_jobs = 0, n_waits = 0, n_signals = 0;
+};
+
+static Partition partition(const hg_exec* ex) {
+  Partition P;
+  P.sig_task.assign(ex->n_tasks, 0);
+  P.sig_job.assign(ex->n_jobs, 0);
+  auto cross = [&](int prod_node, int cons_node) {
+    return prod_node != cons_node && !(ex->is_local(prod_node) && ex->is_local(cons_node));
+  };
+  std::vector<char> wt(ex->n_tasks + ex->n_jobs, 0);  // remote flags this rank waits on
+  for (int t = 0; t < ex->n_tasks; ++t) {
+    const int cn = ex->task_node[t];
+    if (ex->is_local(cn)) P.n_local_tasks++;
+    for (int64_t q = ex->pred_ptr[t]; q < ex->pred_ptr[t + 1]; ++q) {
+      const int u = ex->pred[q];
+      if (cross(ex->task_node[u], cn)) {
+        P.sig_task[u] = 1;
+        if (ex->is_local(cn)) wt[u] = 1;
+      }
+    }
+  }
+  for (int j = 0; j < ex->n_jobs; ++j) {
+    const int cn = ex->job_dst[j];
+    if (ex->is_local(cn)) P.n_local_jobs++;
+    if (ex->job_src_job[j] >= 0) {
+      const int sj = ex->job_src_job[j];
+      if (cross(ex->job_dst[sj], cn)) {
+        P.sig_job[sj] = 1;
+        if (ex->is_local(cn)) wt[ex->n_tasks + sj] = 1;
+      }
+    } else if (ex->job_version[j] >= 0) {
+      const int v = ex->job_version[j];
+      if (cross(ex->task_node[v], cn)) {
+        P.sig_task[v] = 1;
+        if (ex->is_local(cn)) wt[v] = 1;
+      }
+    }
+  }
+  for (char w : wt) P.n_waits += w;
+  P.waited = wt;
+  for (int t = 0; t < ex->n_tasks; ++t) P.n_signals += P.sig_task[t] && ex->is_local(ex->task_node[t]);
+  for (int j = 0; j < ex->n_jobs; ++j) P.n_signals += P.sig_job[j] && ex->is_local(ex->job_dst[j]);
+  return P;
+}
+
+static int add_flag_kernel(cudaGraph_t g, cudaGraphNode_t* out, const cudaGraphNode_t* deps, size_t nd,
+                           const void* fn, hg::FlagParams fp) {
+  cudaKernelNodeParams kp{};
+  void* args[1] = {&fp};
+  kp.func = const_cast<void*>(fn);
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(32);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  HG_CUDA(cudaGraphAddKernelNode(out, g, deps, nd, &kp));
+  return HG_OK;
+}
+
+static int build_graph(hg_exec* ex) {
+  const int n = ex->n_tasks;
+  const Partition part = partition(ex);
   HG_CUDA(cudaGraphCreate(&ex->graph, 0));
-  std::vector<cudaGraphNode_t> task_last(n, nullptr), task_first(n, nullptr);
-  std::vector<cudaGraphNode_t> job_node(P->n_jobs, nullptr);
-  // jobs grouped by requester, in job order
+  std::vector<cudaGraphNode_t> task_last(n, nullptr);
+  std::vector<cudaGraphNode_t> job_node(ex->n_jobs, nullptr);
+  std::vector<cudaGraphNode_t> wait_node(size_t(n) + ex->n_jobs, nullptr);
   std::vector<std::vector<int>> jobs_of(n);
-  for (int j = 0; j < P->n_jobs; ++j) jobs_of[P->job_requester[j]].push_back(j);
+  for (int j = 0; j < ex->n_jobs; ++j) jobs_of[ex->job_requester[j]].push_back(j);
   std::vector<LaunchDesc> launches;
   std::vector<cudaGraphNode_t> deps;
   int64_t side_bytes = 0;
   std::vector<int64_t> scratch_used(ex->k, 0);
+  hg_exec_stats& st = ex->stats;
 
-  auto slot_ptr = [&](int node, int block) -> double* {
-    int64_t off = ex->slot[node - 1][block];
-    return off < 0 ? nullptr : ex->pool[node - 1] + off;
+  // dependency on the producer of a task output / job delivery for a consumer on cons_node
+  auto dep_task = [&](int u, int cons_node) -> int {
+    const int pn = ex->task_node[u];
+    if (ex->is_local(pn) && (ex->is_local(cons_node))) {
+      deps.push_back(task_last[u]);
+      return HG_OK;
+    }
+    cudaGraphNode_t& w = wait_node[u];
+    if (!w) {
+      HG_CUDA(cudaSetDevice(ex->dev[cons_node - 1]));
+      int rc = add_flag_kernel(ex->graph, &w, nullptr, 0, (const void*)hg::k_wait_flag,
+                               hg::FlagParams{ex->task_flag(pn, u), ex->epoch_ptr(cons_node)});
+      if (rc) return rc;
+    }
+    deps.push_back(w);
+    return HG_OK;
+  };
+  auto dep_job = [&](int sj, int cons_node) -> int {
+    const int pn = ex->job_dst[sj];
+    if (ex->is_local(pn) && ex->is_local(cons_node)) {
+      deps.push_back(job_node[sj]);
+      return HG_OK;
+    }
+    cudaGraphNode_t& w = wait_node[size_t(n) + sj];
+    if (!w) {
+      HG_CUDA(cudaSetDevice(ex->dev[cons_node - 1]));
+      int rc = add_flag_kernel(ex->graph, &w, nullptr, 0, (const void*)hg::k_wait_flag,
+                               hg::FlagParams{ex->job_flag(pn, sj), ex->epoch_ptr(cons_node)});
+      if (rc) return rc;
+    }
+    deps.push_back(w);
+    return HG_OK;
   };
 
   for (int di = 0; di < n; ++di) {
-    const int t = P->dispatch[di];
-    // 1) the copy jobs this dispatch created
+    const int t = ex->dispatch[di];
+    // 1) inbound copy jobs created by this dispatch
     for (int j : jobs_of[t]) {
-      const int b = P->job_block[j], src = P->job_src[j], dst = P->job_dst[j];
+      const int dst = ex->job_dst[j];
+      if (!ex->is_local(dst)) continue;
+      const int b = ex->job_block[j], src = ex->job_src[j];
       deps.clear();
-      if (P->job_src_job[j] >= 0) deps.push_back(job_node[P->job_src_job[j]]);
-      else if (P->job_version[j] >= 0) deps.push_back(task_last[P->job_version[j]]);
-      double* dptr = slot_ptr(dst, b);
+      int rc = HG_OK;
+      if (ex->job_src_job[j] >= 0) rc = dep_job(ex->job_src_job[j], dst);
+      else if (ex->job_version[j] >= 0) rc = dep_task(ex->job_version[j], dst);
+      if (rc) return rc;
+      double* dptr = ex->slot_ptr(dst, b);
       const void* sptr;
       size_t bytes;
       if (src == 0) {
-        bytes = size_t(ex->blk_doubles[b]) * 8;
-        if (P->job_version[j] >= 0 || P->job_src_job[j] >= 0) {
+        if (ex->job_version[j] >= 0 || ex->job_src_job[j] >= 0) {
           set_error("job %d: host-staged versions (p2p=False) are not executable", j);
           return HG_EINVAL;
         }
-        sptr = O->device_input ? (const void*)(ex->replica[dst - 1] + ex->host_off[b])
-                               : (const void*)(O->host_in + ex->host_off[b]);
-        if (O->device_input) ex->stats.bytes_d2d += 0;  // served from HBM, still an H2D job of the plan
-        ex->stats.bytes_h2d += bytes;
+        bytes = size_t(ex->blk_doubles[b]) * 8;
+        sptr = ex->device_input ? (const void*)(ex->replica[dst - 1] + ex->host_off[b])
+                                : (const void*)(ex->host_in + ex->host_off[b]);
+        st.bytes_h2d += bytes;
       } else if (dst == 0) {
         set_error("job %d: device->host jobs are not executable on a GPU-only platform", j);
         return HG_EINVAL;
       } else {
         bytes = size_t(ex->slot_doubles[b]) * 8;
-        sptr = slot_ptr(src, b);
-        ex->stats.bytes_d2d += size_t(ex->blk_doubles[b]) * 8;
+        sptr = ex->slot_ptr(src, b);
+        st.bytes_d2d += size_t(ex->blk_doubles[b]) * 8;
         side_bytes += bytes - size_t(ex->blk_doubles[b]) * 8;
       }
       if (!dptr || !sptr) {
@@ -254,32 +456,42 @@ static int build_graph(hg_exec* ex, const hg_exec_plan* P, const hg_exec_opts* O
         return HG_EINVAL;
       }
       HG_CUDA(cudaSetDevice(ex->dev[dst - 1]));
-      HG_CUDA(cudaGraphAddMemcpyNode1D(&job_node[j], ex->graph, deps.data(), deps.size(), dptr, sptr,
-                                       bytes, cudaMemcpyDefault));
-      ex->stats.n_copy_nodes++;
+      HG_CUDA(cudaGraphAddMemcpyNode1D(&job_node[j], ex->graph, deps.data(), deps.size(), dptr, sptr, bytes,
+                                       cudaMemcpyDefault));
+      st.n_copy_nodes++;
+      if (part.sig_job[j]) {
+        cudaGraphNode_t sn;
+        int rc2 = add_flag_kernel(ex->graph, &sn, &job_node[j], 1, (const void*)hg::k_signal_flag,
+                                  hg::FlagParams{ex->job_flag(dst, j), ex->epoch_ptr(dst)});
+        if (rc2) return rc2;
+      }
     }
     // 2) the task's kernel chain
-    const int node = P->task_node[t];
+    const int node = ex->task_node[t];
+    if (!ex->is_local(node)) continue;
     TaskOperands ops;
     ops.nb = ex->nb;
     ops.ib = ex->ib;
     ops.status = ex->status[node - 1];
-    const int sc = task_scratch_ints(P->task_kind[t], ex->nb, ex->ib);
+    const int sc = task_scratch_ints(ex->task_kind[t], ex->nb, ex->ib);
     if (sc > 0) {
       ops.scratch = ex->scratch[node - 1] + scratch_used[node - 1];
       scratch_used[node - 1] += sc;
     }
-    const int64_t a0 = P->acc_ptr[t], a1 = P->acc_ptr[t + 1];
+    const int64_t a0 = ex->acc_ptr[t], a1 = ex->acc_ptr[t + 1];
     if (a1 - a0 > 4) {
       set_error("task %d has %lld accesses (max 4)", t, (long long)(a1 - a0));
       return HG_EINVAL;
     }
-    for (int64_t a = a0; a < a1; ++a) ops.t[ops.n_t++] = slot_ptr(node, P->acc_block[a]);
+    for (int64_t a = a0; a < a1; ++a) ops.t[ops.n_t++] = ex->slot_ptr(node, ex->acc_block[a]);
     launches.clear();
-    if (!build_task_launches(P->task_kind[t], ops, launches)) return HG_EINVAL;
+    if (!build_task_launches(ex->task_kind[t], ops, launches)) return HG_EINVAL;
     deps.clear();
-    for (int64_t w = P->wait_ptr[t]; w < P->wait_ptr[t + 1]; ++w) deps.push_back(job_node[P->wait_job[w]]);
-    for (int64_t q = P->pred_ptr[t]; q < P->pred_ptr[t + 1]; ++q) deps.push_back(task_last[P->pred[q]]);
+    for (int64_t w = ex->wait_ptr[t]; w < ex->wait_ptr[t + 1]; ++w) deps.push_back(job_node[ex->wait_job[w]]);
+    for (int64_t q = ex->pred_ptr[t]; q < ex->pred_ptr[t + 1]; ++q) {
+      int rc = dep_task(ex->pred[q], node);
+      if (rc) return rc;
+    }
     HG_CUDA(cudaSetDevice(ex->dev[node - 1]));
     cudaGraphNode_t prev = nullptr;
     for (size_t li = 0; li < launches.size(); ++li) {
@@ -290,45 +502,54 @@ static int build_graph(hg_exec* ex, const hg_exec_plan* P, const hg_exec_opts* O
       kp.blockDim = launches[li].block;
       kp.sharedMemBytes = launches[li].smem;
       kp.kernelParams = args;
-      kp.extra = nullptr;
       cudaGraphNode_t nd;
-      if (li == 0) {
-        HG_CUDA(cudaGraphAddKernelNode(&nd, ex->graph, deps.data(), deps.size(), &kp));
-        task_first[t] = nd;
-      } else {
-        HG_CUDA(cudaGraphAddKernelNode(&nd, ex->graph, &prev, 1, &kp));
-      }
+      if (li == 0) HG_CUDA(cudaGraphAddKernelNode(&nd, ex->graph, deps.data(), deps.size(), &kp));
+      else HG_CUDA(cudaGraphAddKernelNode(&nd, ex->graph, &prev, 1, &kp));
       prev = nd;
-      ex->stats.n_kernel_nodes++;
+      st.n_kernel_nodes++;
     }
     task_last[t] = prev;
+    if (part.sig_task[t]) {
+      cudaGraphNode_t sn;
+      int rc = add_flag_kernel(ex->graph, &sn, &task_last[t], 1, (const void*)hg::k_signal_flag,
+                               hg::FlagParams{ex->task_flag(node, t), ex->epoch_ptr(node)});
+      if (rc) return rc;
+    }
   }
-  // 3) write-back of final versions
-  if (O->host_out) {
+  // 3) write-back of final versions produced on local nodes
+  if (ex->host_out) {
     for (int b = 0; b < ex->n_blocks; ++b) {
-      const int w = P->final_writer[b];
+      const int w = ex->final_writer[b];
       if (w < 0) continue;
-      const int node = P->task_node[w];
+      const int node = ex->task_node[w];
+      if (!ex->is_local(node)) continue;
       size_t bytes = size_t(ex->blk_doubles[b]) * 8;
       cudaGraphNode_t nd;
       HG_CUDA(cudaSetDevice(ex->dev[node - 1]));
-      HG_CUDA(cudaGraphAddMemcpyNode1D(&nd, ex->graph, &task_last[w], 1, O->host_out + ex->host_off[b],
-                                       slot_ptr(node, b), bytes, cudaMemcpyDefault));
-      ex->stats.bytes_d2h += bytes;
-      ex->stats.n_copy_nodes++;
-      if (O->host_side_out && ex->side > 0 && ex->slot_doubles[b] > ex->blk_doubles[b]) {
+      HG_CUDA(cudaGraphAddMemcpyNode1D(&nd, ex->graph, &task_last[w], 1, ex->host_out + ex->host_off[b],
+                                       ex->slot_ptr(node, b), bytes, cudaMemcpyDefault));
+      st.bytes_d2h += bytes;
+      st.n_copy_nodes++;
+      if (ex->host_side_out && ex->side > 0 && ex->slot_doubles[b] > ex->blk_doubles[b]) {
         HG_CUDA(cudaGraphAddMemcpyNode1D(&nd, ex->graph, &task_last[w], 1,
-                                         O->host_side_out + int64_t(b) * ex->side,
-                                         slot_ptr(node, b) + ex->blk_doubles[b], size_t(ex->side) * 8,
+                                         ex->host_side_out + int64_t(b) * ex->side,
+                                         ex->slot_ptr(node, b) + ex->blk_doubles[b], size_t(ex->side) * 8,
                                          cudaMemcpyDefault));
-        ex->stats.n_copy_nodes++;
+        st.n_copy_nodes++;
       }
     }
   }
-  ex->stats.bytes_side = side_bytes;
-  HG_CUDA(cudaSetDevice(ex->dev[0]));
+  st.bytes_side = side_bytes;
+  int first = ex->rank_node ? ex->rank_node : 1;
+  HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
   HG_CUDA(cudaGraphInstantiate(&ex->exec, ex->graph, 0));
+  ex->built = true;
   return HG_OK;
+}
+
+template <class T>
+static std::vector<T> vcopy(const T* p, int64_t n) {
+  return n > 0 && p ? std::vector<T>(p, p + n) : std::vector<T>();
 }
 
 extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_exec** out) {
@@ -340,51 +561,61 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
     set_error("hg_exec_create: host_in is required (initial residency is the host, sim.py:47-48)");
     return HG_EINVAL;
   }
+  if (O->rank_node < 0 || O->rank_node > P->k) {
+    set_error("hg_exec_create: rank_node %d out of range", O->rank_node);
+    return HG_EINVAL;
+  }
   hg_exec* ex = new hg_exec();
   ex->k = P->k;
   ex->nb = P->nb;
   ex->ib = P->ib;
   ex->side = P->side_doubles;
   ex->n_blocks = P->n_blocks;
+  ex->n_tasks = P->n_tasks;
+  ex->n_jobs = P->n_jobs;
+  const int n = P->n_tasks, nj = P->n_jobs;
+  ex->task_kind = vcopy(P->task_kind, n);
+  ex->task_node = vcopy(P->task_node, n);
+  ex->acc_ptr = vcopy(P->acc_ptr, n + 1);
+  ex->acc_block = vcopy(P->acc_block, P->acc_ptr[n]);
+  ex->pred_ptr = vcopy(P->pred_ptr, n + 1);
+  ex->pred = vcopy(P->pred, P->pred_ptr[n]);
+  ex->dispatch = vcopy(P->dispatch, n);
+  ex->wait_ptr = vcopy(P->wait_ptr, n + 1);
+  ex->wait_job = vcopy(P->wait_job, P->wait_ptr[n]);
+  ex->job_block = vcopy(P->job_block, nj);
+  ex->job_src = vcopy(P->job_src, nj);
+  ex->job_dst = vcopy(P->job_dst, nj);
+  ex->job_version = vcopy(P->job_version, nj);
+  ex->job_src_job = vcopy(P->job_src_job, nj);
+  ex->job_requester = vcopy(P->job_requester, nj);
+  ex->block_bytes = vcopy(P->block_bytes, P->n_blocks);
+  ex->final_writer = vcopy(P->final_writer, P->n_blocks);
+  ex->rank_node = O->rank_node;
+  ex->host_in = O->host_in;
+  ex->host_out = O->host_out;
+  ex->host_side_out = O->host_side_out;
+  ex->device_input = O->device_input;
   ex->dev.assign(O->devices, O->devices + P->k);
-  ex->pool.assign(P->k, nullptr);
+  ex->base.assign(P->k, nullptr);
+  ex->ipc.assign(P->k, 0);
   ex->replica.assign(P->k, nullptr);
   ex->status.assign(P->k, nullptr);
   ex->scratch.assign(P->k, nullptr);
-  const int64_t tile_d = int64_t(P->nb) * P->nb;
-  ex->host_off.resize(P->n_blocks);
-  ex->blk_doubles.resize(P->n_blocks);
-  ex->slot_doubles.resize(P->n_blocks);
+  plan_layout(ex);
   int64_t host_total = 0;
-  for (int b = 0; b < P->n_blocks; ++b) {
-    ex->blk_doubles[b] = P->block_bytes[b] / 8;
-    ex->slot_doubles[b] = ex->blk_doubles[b] + (ex->blk_doubles[b] == tile_d ? P->side_doubles : 0);
-    ex->host_off[b] = host_total;
-    host_total += ex->blk_doubles[b];
-  }
-  // slots: (block, node) pairs the plan ever touches
-  ex->slot.assign(P->k, std::vector<int64_t>(P->n_blocks, -1));
-  std::vector<int64_t> used(P->k, 0);
-  auto need = [&](int node, int b) {
-    if (node < 1 || node > P->k) return;
-    int64_t& s = ex->slot[node - 1][b];
-    if (s < 0) {
-      s = used[node - 1];
-      used[node - 1] += (ex->slot_doubles[b] + 31) / 32 * 32;  // 256-byte aligned slots
-    }
-  };
-  for (int t = 0; t < P->n_tasks; ++t)
-    for (int64_t a = P->acc_ptr[t]; a < P->acc_ptr[t + 1]; ++a) need(P->task_node[t], P->acc_block[a]);
-  for (int j = 0; j < P->n_jobs; ++j) need(P->job_dst[j], P->job_block[j]);
+  for (int b = 0; b < ex->n_blocks; ++b) host_total += ex->blk_doubles[b];
   int rc = HG_OK;
   for (int g = 0; g < P->k && rc == HG_OK; ++g) {
+    const int node = g + 1;
+    if (!ex->is_local(node)) continue;
     if (cudaSetDevice(ex->dev[g]) != cudaSuccess) {
       set_error("cudaSetDevice(%d) failed", ex->dev[g]);
       rc = HG_ECUDA;
       break;
     }
     if ((rc = ensure_attributes(ex->dev[g]))) break;
-    for (int h = 0; h < P->k; ++h) {
+    for (int h = 0; h < P->k && ex->rank_node == 0; ++h) {
       if (h == g || ex->dev[h] == ex->dev[g]) continue;
       int can = 0;
       cudaDeviceCanAccessPeer(&can, ex->dev[g], ex->dev[h]);
@@ -398,24 +629,23 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
       }
     }
     if (rc) break;
-    if (cudaMalloc(&ex->pool[g], size_t(std::max<int64_t>(used[g], 32)) * 8) != cudaSuccess ||
+    if (cudaMalloc(&ex->base[g], size_t(ex->pool_doubles[g]) * 8) != cudaSuccess ||
         cudaMalloc(&ex->status[g], sizeof(int)) != cudaSuccess) {
       set_error("cudaMalloc of the tile pool failed on device %d (%lld bytes)", ex->dev[g],
-                (long long)used[g] * 8);
+                (long long)ex->pool_doubles[g] * 8);
       rc = HG_ECUDA;
       break;
     }
+    cudaMemset(ex->base[g], 0, size_t(ex->header_doubles) * 8);  // flags + epoch
     cudaMemset(ex->status[g], 0, sizeof(int));
     int64_t sc = 0;
     for (int t = 0; t < P->n_tasks; ++t)
-      if (P->task_node[t] == g + 1) sc += task_scratch_ints(P->task_kind[t], P->nb, P->ib);
-    if (sc > 0) {
-      if (cudaMalloc(&ex->scratch[g], size_t(sc) * sizeof(int)) != cudaSuccess ||
-          cudaMemset(ex->scratch[g], 0, size_t(sc) * sizeof(int)) != cudaSuccess) {
-        set_error("scratch allocation failed on device %d", ex->dev[g]);
-        rc = HG_ECUDA;
-        break;
-      }
+      if (ex->task_node[t] == node) sc += task_scratch_ints(ex->task_kind[t], P->nb, P->ib);
+    if (sc > 0 && (cudaMalloc(&ex->scratch[g], size_t(sc) * sizeof(int)) != cudaSuccess ||
+                   cudaMemset(ex->scratch[g], 0, size_t(sc) * sizeof(int)) != cudaSuccess)) {
+      set_error("scratch allocation failed on device %d", ex->dev[g]);
+      rc = HG_ECUDA;
+      break;
     }
     if (O->device_input) {
       if (cudaMalloc(&ex->replica[g], size_t(host_total) * 8) != cudaSuccess ||
@@ -427,14 +657,15 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
     }
   }
   if (rc == HG_OK) {
-    cudaSetDevice(ex->dev[0]);
+    const int first = ex->rank_node ? ex->rank_node : 1;
+    cudaSetDevice(ex->dev[first - 1]);
     if (cudaStreamCreateWithFlags(&ex->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&ex->ev0) != cudaSuccess || cudaEventCreate(&ex->ev1) != cudaSuccess) {
       set_error("stream/event creation failed");
       rc = HG_ECUDA;
     }
   }
-  if (rc == HG_OK) rc = build_graph(ex, P, O);
+  if (rc == HG_OK && ex->rank_node == 0) rc = build_graph(ex);
   if (rc != HG_OK) {
     release(ex);
     return rc;
@@ -443,32 +674,94 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
   return HG_OK;
 }
 
-extern "C" int hg_exec_run(hg_exec* ex, hg_exec_stats* stats) {
-  if (!ex) {
-    set_error("hg_exec_run: null handle");
+extern "C" int hg_exec_ipc_handle(hg_exec* ex, void* handle64) {
+  if (!ex || !handle64 || ex->rank_node == 0) {
+    set_error("hg_exec_ipc_handle: needs a per-rank executor");
     return HG_EINVAL;
   }
-  for (int g = 0; g < ex->k; ++g) {
-    HG_CUDA(cudaSetDevice(ex->dev[g]));
-    HG_CUDA(cudaMemset(ex->status[g], 0, sizeof(int)));
+  cudaIpcMemHandle_t h;
+  HG_CUDA(cudaSetDevice(ex->dev[ex->rank_node - 1]));
+  HG_CUDA(cudaIpcGetMemHandle(&h, ex->base[ex->rank_node - 1]));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  memcpy(handle64, &h, 64);
+  return HG_OK;
+}
+
+extern "C" int hg_exec_ipc_open(hg_exec* ex, int32_t node, const void* handle64) {
+  if (!ex || !handle64 || ex->rank_node == 0 || node < 1 || node > ex->k || node == ex->rank_node) {
+    set_error("hg_exec_ipc_open: bad arguments");
+    return HG_EINVAL;
   }
-  HG_CUDA(cudaSetDevice(ex->dev[0]));
-  HG_CUDA(cudaEventRecord(ex->ev0, ex->stream));
-  HG_CUDA(cudaGraphLaunch(ex->exec, ex->stream));
-  HG_CUDA(cudaEventRecord(ex->ev1, ex->stream));
-  HG_CUDA(cudaEventSynchronize(ex->ev1));
-  float ms = 0.f;
-  HG_CUDA(cudaEventElapsedTime(&ms, ex->ev0, ex->ev1));
-  int bad = 0;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  void* p = nullptr;
+  HG_CUDA(cudaSetDevice(ex->dev[ex->rank_node - 1]));
+  HG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  ex->base[node - 1] = static_cast<double*>(p);
+  ex->ipc[node - 1] = 1;
+  return HG_OK;
+}
+
+extern "C" int hg_exec_build(hg_exec* ex) {
+  if (!ex || ex->built) {
+    set_error("hg_exec_build: bad handle or already built");
+    return HG_EINVAL;
+  }
+  for (int g = 0; g < ex->k; ++g)
+    if (!ex->base[g]) {
+      set_error("hg_exec_build: pool of node %d is not mapped (hg_exec_ipc_open)", g + 1);
+      return HG_EINVAL;
+    }
+  return build_graph(ex);
+}
+
+extern "C" int hg_exec_partition(const hg_exec_plan* P, int32_t rank_node, int32_t* counts4, int32_t* waits,
+                                 int32_t* signals) {
+  if (!P || !counts4) {
+    set_error("hg_exec_partition: bad arguments");
+    return HG_EINVAL;
+  }
+  hg_exec ex;
+  ex.k = P->k;
+  ex.n_tasks = P->n_tasks;
+  ex.n_jobs = P->n_jobs;
+  ex.rank_node = rank_node;
+  const int n = P->n_tasks, nj = P->n_jobs;
+  ex.task_node = vcopy(P->task_node, n);
+  ex.pred_ptr = vcopy(P->pred_ptr, n + 1);
+  ex.pred = vcopy(P->pred, P->pred_ptr[n]);
+  ex.job_dst = vcopy(P->job_dst, nj);
+  ex.job_version = vcopy(P->job_version, nj);
+  ex.job_src_job = vcopy(P->job_src_job, nj);
+  Partition part = partition(&ex);
+  counts4[0] = part.n_local_tasks;
+  counts4[1] = part.n_local_jobs;
+  counts4[2] = part.n_waits;
+  counts4[3] = part.n_signals;
+  // flag ids: task t -> t, job j -> n_tasks + j
+  int nw = 0, ns = 0;
+  for (int f = 0; f < n + nj; ++f) {
+    if (waits && part.waited[f]) waits[nw++] = f;
+    const bool sig = f < n ? (part.sig_task[f] && ex.is_local(ex.task_node[f]))
+                           : (part.sig_job[f - n] && ex.is_local(ex.job_dst[f - n]));
+    if (signals && sig) signals[ns++] = f;
+  }
+  return HG_OK;
+}
+
+static int all_status(hg_exec* ex, int* bad) {
+  *bad = 0;
   for (int g = 0; g < ex->k; ++g) {
+    if (!ex->is_local(g + 1)) continue;
     int st = 0;
     HG_CUDA(cudaSetDevice(ex->dev[g]));
     HG_CUDA(cudaMemcpy(&st, ex->status[g], sizeof(int), cudaMemcpyDeviceToHost));
-    bad |= st;
+    *bad |= st;
   }
-  HG_CUDA(cudaSetDevice(ex->dev[0]));
-  ex->stats.elapsed_ms = ms;
-  if (stats) *stats = ex->stats;
+  return HG_OK;
+}
+
+static int status_error(int bad) {
   if (bad & 1) {
     set_error("POTRF: matrix is not positive definite (non-positive pivot)");
     return HG_ENOTSPD;
@@ -484,16 +777,26 @@ extern "C" int hg_exec_run(hg_exec* ex, hg_exec_stats* stats) {
 // default stream); pair with hg_exec_wait.  Lets a caller bracket K
 // back-to-back runs with its own CUDA events on that stream.
 extern "C" int hg_exec_launch(hg_exec* ex, void* stream) {
-  if (!ex) {
-    set_error("hg_exec_launch: null handle");
+  if (!ex || !ex->built) {
+    set_error("hg_exec_launch: null handle or graph not built");
     return HG_EINVAL;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ex->epoch++;
   for (int g = 0; g < ex->k; ++g) {
+    if (!ex->is_local(g + 1)) continue;
     HG_CUDA(cudaSetDevice(ex->dev[g]));
-    HG_CUDA(cudaMemsetAsync(ex->status[g], 0, sizeof(int), g == 0 ? s : nullptr));
+    const bool first = (ex->rank_node ? ex->rank_node : 1) == g + 1;
+    cudaStream_t sg = first ? s : nullptr;
+    HG_CUDA(cudaMemsetAsync(ex->status[g], 0, sizeof(int), sg));
+    if (ex->rank_node) {  // flags are only used across processes
+      hg::k_set_epoch<<<1, 32, 0, sg>>>(ex->epoch_ptr(g + 1), ex->epoch);
+      HG_CUDA(cudaGetLastError());
+    }
+    if (!first) HG_CUDA(cudaDeviceSynchronize());  // other devices' resets precede the graph
   }
-  HG_CUDA(cudaSetDevice(ex->dev[0]));
+  const int first = ex->rank_node ? ex->rank_node : 1;
+  HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
   HG_CUDA(cudaGraphLaunch(ex->exec, s));
   ex->last_stream = s;
   ex->launched = true;
@@ -505,26 +808,35 @@ extern "C" int hg_exec_wait(hg_exec* ex) {
     set_error("hg_exec_wait: null handle");
     return HG_EINVAL;
   }
-  HG_CUDA(cudaSetDevice(ex->dev[0]));
+  const int first = ex->rank_node ? ex->rank_node : 1;
+  HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
   HG_CUDA(cudaStreamSynchronize(ex->launched ? ex->last_stream : ex->stream));
   ex->launched = false;
   int bad = 0;
-  for (int g = 0; g < ex->k; ++g) {
-    int st = 0;
-    HG_CUDA(cudaSetDevice(ex->dev[g]));
-    HG_CUDA(cudaMemcpy(&st, ex->status[g], sizeof(int), cudaMemcpyDeviceToHost));
-    bad |= st;
+  int rc = all_status(ex, &bad);
+  if (rc) return rc;
+  HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
+  return status_error(bad);
+}
+
+extern "C" int hg_exec_run(hg_exec* ex, hg_exec_stats* stats) {
+  if (!ex || !ex->built) {
+    set_error("hg_exec_run: null handle or graph not built");
+    return HG_EINVAL;
   }
-  HG_CUDA(cudaSetDevice(ex->dev[0]));
-  if (bad & 1) {
-    set_error("POTRF: matrix is not positive definite (non-positive pivot)");
-    return HG_ENOTSPD;
-  }
-  if (bad & 2) {
-    set_error("LU: exactly zero pivot encountered");
-    return HG_ESINGULAR;
-  }
-  return HG_OK;
+  const int first = ex->rank_node ? ex->rank_node : 1;
+  HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
+  HG_CUDA(cudaEventRecord(ex->ev0, ex->stream));
+  int rc = hg_exec_launch(ex, ex->stream);
+  if (rc) return rc;
+  HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
+  HG_CUDA(cudaEventRecord(ex->ev1, ex->stream));
+  rc = hg_exec_wait(ex);
+  float ms = 0.f;
+  HG_CUDA(cudaEventElapsedTime(&ms, ex->ev0, ex->ev1));
+  ex->stats.elapsed_ms = ms;
+  if (stats) *stats = ex->stats;
+  return rc;
 }
 
 extern "C" int hg_exec_info(hg_exec* ex, hg_exec_stats* stats) {
@@ -537,7 +849,7 @@ extern "C" int hg_exec_info(hg_exec* ex, hg_exec_stats* stats) {
 }
 
 extern "C" int hg_exec_read_block(hg_exec* ex, int32_t block, int32_t node, double* host, int64_t doubles) {
-  if (!ex || block < 0 || block >= ex->n_blocks || node < 1 || node > ex->k) {
+  if (!ex || block < 0 || block >= ex->n_blocks || node < 1 || node > ex->k || !ex->base[node - 1]) {
     set_error("hg_exec_read_block: bad arguments");
     return HG_EINVAL;
   }
@@ -547,8 +859,9 @@ extern "C" int hg_exec_read_block(hg_exec* ex, int32_t block, int32_t node, doub
     return HG_EINVAL;
   }
   if (doubles > ex->slot_doubles[block]) doubles = ex->slot_doubles[block];
-  HG_CUDA(cudaSetDevice(ex->dev[node - 1]));
-  HG_CUDA(cudaMemcpy(host, ex->pool[node - 1] + off, size_t(doubles) * 8, cudaMemcpyDeviceToHost));
+  const int first = ex->rank_node ? ex->rank_node : node;
+  HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
+  HG_CUDA(cudaMemcpy(host, ex->base[node - 1] + off, size_t(doubles) * 8, cudaMemcpyDefault));
   return HG_OK;
 }
 

@@ -427,7 +427,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
 struct TrsmInvParams {
   const double* L;  // diagonal tile after POTRF (M^T in its upper triangle)
   double* B;
-  int* count;       // [nI] per-task scratch
+  int* count;       // [2*nI] per-task scratch (arrivals, departures per strip)
   int ld;
 };
 
@@ -477,19 +477,25 @@ __global__ void __launch_bounds__(CfgG::THREADS) k_trsm_inv(TrsmInvParams p) {
     MRowLoader<CfgG, kR> lb{p.L, ld, Js[1] * kR};
     gemm_mainloop<CfgG>(acc1, smem, la, lb, 0, (Js[1] + 1) * kR);
   }
-  // all reads of B by this CTA are complete (mainloop ends with wait_group 0 + barrier)
-  __shared__ int s_go;
+  // all reads of B by this CTA are complete (mainloop ends with wait_group 0 + barrier).
+  // Strip barrier on two counters (arrivals, departures): the last CTA to depart
+  // resets both, so the scratch is clean for the next run whatever its shape.
   if (threadIdx.x == 0) {
-    int* cnt = p.count + I;
-    const int old = atomicAdd(cnt, 1);
-    const int target = (old / P + 1) * P;
-    while (ld_acquire(cnt) < target) __nanosleep(32);
-    s_go = 1;
+    int* arr = p.count + 2 * I;
+    atomicAdd(arr, 1);
+    while (ld_acquire(arr) < P) __nanosleep(32);
   }
   __syncthreads();
   double* B = p.B;
   for_each_acc<CfgG>(acc0, [&](int r, int c, double v) { B[size_t(Js[0] * kR + c) * ld + I * kR + r] = v; });
   for_each_acc<CfgG>(acc1, [&](int r, int c, double v) { B[size_t(Js[1] * kR + c) * ld + I * kR + r] = v; });
+  if (threadIdx.x == 0) {
+    int* arr = p.count + 2 * I;
+    if (atomicAdd(arr + 1, 1) == P - 1) {  // every CTA of the strip has passed its wait
+      atomicExch(arr, 0);
+      atomicExch(arr + 1, 0);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -522,7 +528,7 @@ static void push_gemm(std::vector<LaunchDesc>& out, const double* A, const doubl
 }
 
 int chol_scratch_ints(int kind, int nb) {
-  return kind == K_TRSM ? (nb / kR) : 0;
+  return kind == K_TRSM ? 2 * (nb / kR) : 0;
 }
 
 bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out) {
@@ -543,7 +549,7 @@ bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc
     }
     case K_TRSM: {
       if (!o.scratch) {
-        set_error("TRSM needs per-task scratch (%d ints)", nJ);
+        set_error("TRSM needs per-task scratch (%d ints)", 2 * nJ);
         return false;
       }
       if (nJ % 2) {

@@ -96,7 +96,8 @@ class Executor:
     """A plan compiled into a CUDA graph bound to host buffers; ``run()`` repeats it."""
 
     def __init__(self, graph, platform, plan, host_in: np.ndarray, host_out: np.ndarray | None = None,
-                 devices=None, device_input: bool = False, host_side_out: np.ndarray | None = None):
+                 devices=None, device_input: bool = False, host_side_out: np.ndarray | None = None,
+                 rank_node: int = 0):
         L = _native.lib()
         lay = graph.layout
         if lay is None:
@@ -139,11 +140,12 @@ class Executor:
             _native.ptr(self.host_in, C.c_double),
             _native.ptr(host_out, C.c_double) if host_out is not None else None,
             _native.ptr(host_side_out, C.c_double) if host_side_out is not None else None,
-            int(bool(device_input)), 0)
+            int(bool(device_input)), int(rank_node))
         h = C.c_void_p()
         _native.check(L.hg_exec_create(C.byref(ep), C.byref(opts), C.byref(h)), "hg_exec_create")
         self._h = h
         self._ep = ep
+        self.rank_node = rank_node
 
     def run(self) -> ExecStats:
         st = _native.ExecStats()
@@ -181,6 +183,103 @@ class Executor:
             self.close()
         except Exception:
             pass
+
+
+class DistributedExecutor(Executor):
+    """One process per GPU (torchrun): this rank executes GPU node ``rank + 1``.
+
+    Every rank computes the same (deterministic) plan; the ranks check that by
+    exchanging a digest, exchange their slot pools as CUDA IPC handles
+    (``torch.distributed.all_gather_object`` -- plumbing only, no collective
+    on the data path), and build rank-local CUDA graphs whose cross-rank
+    dependencies are device flags in the producer's pool.  Tile moves between
+    ranks are peer copies (NVLink) pulled by the consumer.
+    """
+
+    def __init__(self, graph, platform, plan, host_in, host_out=None, rank=None, world=None, device=None,
+                 device_input=False, host_side_out=None, group=None):
+        import torch.distributed as dist
+
+        rank = dist.get_rank(group) if rank is None else rank
+        world = dist.get_world_size(group) if world is None else world
+        if world != platform.k:
+            raise PlatformError(f"{world} ranks for a {platform.k}-GPU platform: one process per GPU node")
+        check_same_plan(plan, world, group)
+        dev = int(device if device is not None else rank % max(1, _native.lib().hg_device_count()))
+        super().__init__(graph, platform, plan, host_in, host_out, devices=[dev] * platform.k,
+                         device_input=device_input, host_side_out=host_side_out, rank_node=rank + 1)
+        L = _native.lib()
+        mine = (C.c_char * 64)()
+        _native.check(L.hg_exec_ipc_handle(self._h, mine), "hg_exec_ipc_handle")
+        handles = exchange_handles(bytes(mine), world, group)
+        for r, hb in enumerate(handles):
+            if r != rank:
+                buf = (C.c_char * 64).from_buffer_copy(hb)
+                _native.check(L.hg_exec_ipc_open(self._h, r + 1, buf), "hg_exec_ipc_open")
+        _native.check(L.hg_exec_build(self._h), "hg_exec_build")
+        dist.barrier(group=group)
+
+
+def check_same_plan(plan, world, group=None):
+    """All ranks must execute the identical plan (each computes it locally)."""
+    import torch.distributed as dist
+
+    digests = [None] * world
+    dist.all_gather_object(digests, plan_digest(plan), group=group)
+    if any(d != digests[0] for d in digests):
+        raise RuntimeError("ranks computed different plans (inputs differ across ranks)")
+    return digests[0]
+
+
+def exchange_handles(mine: bytes, world, group=None):
+    """All-gather the 64-byte CUDA IPC handles of every rank's slot pool."""
+    import torch.distributed as dist
+
+    if len(mine) != 64:
+        raise ValueError("CUDA IPC handles are 64 bytes")
+    handles = [None] * world
+    dist.all_gather_object(handles, mine, group=group)
+    return handles
+
+
+def plan_digest(plan) -> str:
+    """Content hash of everything the executor consumes from a plan."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for key in ("worker", "dispatch", "job_block", "job_src", "job_dst", "job_version", "job_src_job",
+                "job_requester", "wait_ptr", "wait_job"):
+        h.update(np.ascontiguousarray(getattr(plan, key)).tobytes())
+    return h.hexdigest()
+
+
+def partition_counts(graph, platform, plan, rank_node: int, with_flags: bool = False):
+    """CPU dry run of a rank's share: (local tasks, local copy jobs, remote waits, signals)
+    [, waited flag ids, signalled flag ids]."""
+    fl = graph.flat()
+    n = len(graph)
+    holder = type("H", (), {})()
+    kind_map = np.asarray([ALL_KINDS.index(kd) if kd in ALL_KINDS else 0 for kd in fl["kinds"]], np.int32)
+    holder.task_kind = kind_map[fl["kind_id"]].astype(np.int32)
+    holder.task_node = _gpu_nodes(plan, platform)
+    preds = [graph.predecessors(t) for t in range(n)]
+    holder.pred_ptr = np.zeros(n + 1, np.int64)
+    holder.pred_ptr[1:] = np.cumsum([len(p) for p in preds])
+    holder.pred = np.asarray([q for p in preds for q in p], np.int32)
+    holder.final_writer = np.full(len(graph.data), -1, np.int32)
+    lay = graph.layout
+    ep = ExecPlan_from(plan, n, len(graph.data), platform.k, lay, holder, fl)
+    out = np.zeros(4, np.int32)
+    cap = n + plan.n_jobs
+    waits = np.full(max(cap, 1), -1, np.int32)
+    sigs = np.full(max(cap, 1), -1, np.int32)
+    _native.check(_native.lib().hg_exec_partition(C.byref(ep), int(rank_node), _native.ptr(out, C.c_int32),
+                                                  _native.ptr(waits, C.c_int32), _native.ptr(sigs, C.c_int32)),
+                  "hg_exec_partition")
+    counts = tuple(int(x) for x in out)
+    if with_flags:
+        return counts + (waits[:counts[2]].copy(), sigs[:counts[3]].copy())
+    return counts
 
 
 def ExecPlan_from(plan, n, n_blocks, k, lay, ex, fl):
