@@ -116,17 +116,26 @@ HG_DEVICE void gemm_mainloop(double (&acc)[Cfg::FM][Cfg::FN][2], double* smem,
     }
     const double* a_s = sA + (it % STAGES) * SM::A_SLAB;
     const double* b_s = sB + (it % STAGES) * SM::B_SLAB;
+    // fragments double-buffered in registers: k-step kk+4 is loaded while the
+    // 16 DMMAs of k-step kk issue
+    double af[2][Cfg::FM], bf[2][Cfg::FN];
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i) af[0][i] = frag_at<Cfg, LA, Cfg::BM>(a_s, wm + i * 8 + g, t);
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) bf[0][j] = frag_at<Cfg, LB, Cfg::BN>(b_s, wn + j * 8 + g, t);
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[Cfg::FM], bf[Cfg::FN];
+      const int cur = (kk >> 2) & 1, nxt = cur ^ 1;
+      if (kk + 4 < BK) {
 #pragma unroll
-      for (int i = 0; i < Cfg::FM; ++i) af[i] = frag_at<Cfg, LA, Cfg::BM>(a_s, wm + i * 8 + g, kk + t);
+        for (int i = 0; i < Cfg::FM; ++i) af[nxt][i] = frag_at<Cfg, LA, Cfg::BM>(a_s, wm + i * 8 + g, kk + 4 + t);
 #pragma unroll
-      for (int j = 0; j < Cfg::FN; ++j) bf[j] = frag_at<Cfg, LB, Cfg::BN>(b_s, wn + j * 8 + g, kk + t);
+        for (int j = 0; j < Cfg::FN; ++j) bf[nxt][j] = frag_at<Cfg, LB, Cfg::BN>(b_s, wn + j * 8 + g, kk + 4 + t);
+      }
 #pragma unroll
       for (int i = 0; i < Cfg::FM; ++i)
 #pragma unroll
-        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
     }
   }
   cp_async_wait<0>();

@@ -120,17 +120,21 @@ int main() {
     flops = double(blocks) * threads * iters * 16 * 2.0;
     printf("{\"bench\":\"dfma_peak\",\"blocks_per_sm\":%d,\"tflops\":%.3f,\"ms\":%.3f}\n", blocksPerSm, flops / (ms * 1e-3) / 1e12, ms);
   }
-  using C128 = hg::GemmCfg<128, 128, 16, 64, 32, 3>;
-  using C128w = hg::GemmCfg<128, 128, 16, 32, 64, 3>;
   using C64 = hg::GemmCfg<64, 64, 16, 32, 32, 3>;
+  using C64b32 = hg::GemmCfg<64, 64, 32, 32, 32, 3>;
+  using C64s4 = hg::GemmCfg<64, 64, 16, 32, 32, 4>;
+  using C64w2 = hg::GemmCfg<64, 64, 16, 32, 64, 3>;
   using C128x64 = hg::GemmCfg<128, 64, 16, 32, 32, 3>;
+  using C128w16 = hg::GemmCfg<128, 128, 16, 32, 32, 3>;
+  using C128x64w64 = hg::GemmCfg<128, 64, 16, 64, 32, 3>;
   for (int batch : {1, 8, 32}) {
-    bench_cfg<C128>("128x128x16_w64x32_s3", 1024, batch);
-    bench_cfg<C128w>("128x128x16_w32x64_s3", 1024, batch);
     bench_cfg<C64>("64x64x16_w32x32_s3", 1024, batch);
+    bench_cfg<C64b32>("64x64x32_w32x32_s3", 1024, batch);
+    bench_cfg<C64s4>("64x64x16_w32x32_s4", 1024, batch);
+    bench_cfg<C64w2>("64x64x16_w32x64_s3", 1024, batch);
     bench_cfg<C128x64>("128x64x16_w32x32_s3", 1024, batch);
+    bench_cfg<C128w16>("128x128x16_w32x32_s3", 1024, batch);
+    bench_cfg<C128x64w64>("128x64x16_w64x32_s3", 1024, batch);
   }
-  bench_cfg<C128>("128x128x16_w64x32_s3", 512, 32);
-  bench_cfg<C64>("64x64x16_w32x32_s3", 512, 32);
   return 0;
 }
