@@ -189,29 +189,70 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
   __threadfence();
   cl.sync();
   if (q != 0) return;
-  // T from y and tau (dgeqrt2 / dtpqrt2 recurrence): T(0:j, j) = -tau_j T(0:j, 0:j) y(0:j, j)
-  double* Ts = s;  // [j][k] = T(k, j), ld sb+1
-  double* yv = s + sb * (sb + 1);
-  const int TL = sb + 1;
+  // T from y and tau by the compact-WY identity T^{-1} = diag(1/tau) + striu(V^T V)
+  // (y(k, j) = V_k^T v_j is exactly striu(V^T V)), inverted by 16x16 blocks in
+  // order of block distance.  Packed smem: U (strict upper, row-major), T
+  // stored transposed in the strict lower part, tau on the side.
+  const int LS = sb + 1;
+  double* S = s;                 // S[r*LS + c]
+  double* tv = s + sb * LS;      // tau[sb]
+  double* Wb = tv + sb;          // work blocks: up to 7 x 256
   for (int e = tid; e < sb * sb; e += kQrThreads) {
-    int jc = e / sb, k = e % sb;
-    Ts[jc * TL + k] = __ldcg(T + size_t(jc) * ib + k);
+    int jc = e / sb, k = e % sb;  // T area column jc, row k
+    double v = __ldcg(T + size_t(jc) * ib + k);
+    if (k < jc) S[k * LS + jc] = v;        // U(k, jc) = y
+    else if (k == jc) tv[k] = v;           // tau
   }
   __syncthreads();
-  for (int jc = 1; jc < sb; ++jc) {
-    for (int k = tid; k < jc; k += kQrThreads) yv[k] = Ts[jc * TL + k];
-    __syncthreads();
-    const double tj = Ts[jc * TL + jc];
-    for (int k = tid; k < jc; k += kQrThreads) {
+  auto Uat = [&](int r, int c) { return S[r * LS + c]; };                        // r < c
+  auto Tat = [&](int r, int c) { return r == c ? tv[r] : S[c * LS + r]; };       // r <= c
+  const int nbk = sb / 16;
+  // level 0: diagonal blocks, one warp each, lane i = column i (back substitution)
+  if (warp < nbk && lane < 16) {
+    const int a0 = warp * 16, i = lane;
+    double tcol[16];
+#pragma unroll
+    for (int r = 15; r >= 0; --r) {
+      double v = 0.0;
+      if (r == i) v = tv[a0 + i];
+      else if (r < i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int m = r + 1; m < 16; ++m)
+          if (m <= i) acc = fma(Uat(a0 + r, a0 + m), tcol[m], acc);
+        v = -tv[a0 + r] * acc;
+      }
+      tcol[r] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (r < i) S[(a0 + i) * LS + a0 + r] = tcol[r];
+  }
+  __syncthreads();
+  for (int d = 1; d < nbk; ++d) {
+    const int nblk = nbk - d;
+    // W_ab = sum_{c=a+1}^{b} U_ac T_cb
+    for (int e = tid; e < nblk * 256; e += kQrThreads) {
+      const int a = e / 256, b = a + d, i = (e % 256) / 16, j = e % 16;
+      const int r0 = a * 16 + i, c0 = b * 16 + j;
       double acc = 0.0;
-      for (int m = k; m < jc; ++m) acc = fma(Ts[m * TL + k], yv[m], acc);
-      Ts[jc * TL + k] = -tj * acc;
+      for (int m = (a + 1) * 16; m <= c0; ++m) acc = fma(Uat(r0, m), Tat(m, c0), acc);
+      Wb[e] = acc;
+    }
+    __syncthreads();
+    // T_ab = -T_aa W_ab
+    for (int e = tid; e < nblk * 256; e += kQrThreads) {
+      const int a = e / 256, b = a + d, i = (e % 256) / 16, j = e % 16;
+      const int r0 = a * 16 + i, c0 = b * 16 + j;
+      double acc = 0.0;
+      for (int m = i; m < 16; ++m) acc = fma(Tat(r0, a * 16 + m), Wb[a * 256 + m * 16 + j], acc);
+      S[c0 * LS + r0] = -acc;
     }
     __syncthreads();
   }
   for (int e = tid; e < sb * sb; e += kQrThreads) {
     int jc = e / sb, k = e % sb;
-    T[size_t(jc) * ib + k] = Ts[jc * TL + k];
+    T[size_t(jc) * ib + k] = k <= jc ? Tat(k, jc) : 0.0;
   }
 }
 
@@ -323,7 +364,7 @@ __global__ void __launch_bounds__(CfgQ::THREADS) k_qr_apply(QrApplyParams p) {
 static unsigned qr_panel_smem(int nb, int sb) {
   const int R = nb / kQrCl;
   size_t d = size_t(sb) * (R + 1);
-  size_t t = size_t(sb) * (sb + 1) + sb;
+  size_t t = size_t(sb) * (sb + 1) + sb + 7 * 256;
   if (t > d) d = t;
   d += 5 * kQrMaxSb + 4;
   return unsigned(d * sizeof(double));
