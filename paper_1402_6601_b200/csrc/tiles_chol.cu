@@ -167,6 +167,36 @@ __device__ __forceinline__ void leaf32(double* s, int lds, int r0, double* iv, i
   __syncwarp();
 }
 
+// 32x32x32 product on DMMA by 4 warps (warp w owns the 16x16 quadrant
+// (w&1, w>>1)); a(i, k), b(c, k) fetch operands, out(i, c, v) consumes results.
+template <class FA, class FB, class FO>
+__device__ __forceinline__ void mma32(FA a, FB b, FO out) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp >= 4) return;
+  const int g = lane >> 2, t = lane & 3;
+  const int i0 = (warp & 1) * 16, c0 = (warp >> 1) * 16;
+  double acc[2][2][2] = {};
+#pragma unroll
+  for (int k0 = 0; k0 < 32; k0 += 4) {
+    double af[2], bf[2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) af[m] = a(i0 + m * 8 + g, k0 + t);
+#pragma unroll
+    for (int n = 0; n < 2; ++n) bf[n] = b(c0 + n * 8 + g, k0 + t);
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < 2; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+  }
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      out(i0 + m * 8 + g, c0 + n * 8 + 2 * t, acc[m][n][0]);
+      out(i0 + m * 8 + g, c0 + n * 8 + 2 * t + 1, acc[m][n][1]);
+    }
+}
+
 template <int NT>
 __device__ void diag_factor_inverse_fast(double* A, int ld, int j0, int* status, double (*s)[kR + 1],
                                          double (*iv)[kR + 1], double (*tm)[33]) {
@@ -182,61 +212,27 @@ __device__ void diag_factor_inverse_fast(double* A, int ld, int j0, int* status,
   __syncthreads();
   if (warp == 0) leaf32(S, L, 0, IV, L, status);
   __syncthreads();
-  // L21(i, c) = sum_{k >= c} A21(i, k) I11(k, c)^T ... = sum_k A21(i,k) inv11(c,k), k <= c
-  double out[8];
-  const int row = 32 + (tid >> 2), cb = (tid & 3) * 8;
-  if (tid < 128) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = cb + q;
-      double acc = 0.0;
-      for (int k = 0; k <= c; ++k) acc = fma(s[k][row], iv[k][c], acc);
-      out[q] = acc;
-    }
-  }
+  // L21 = A21 I11^T : out(i, c) = sum_k A21(i, k) I11(c, k), I11(c, k) = iv[k][c]
+  mma32([&](int i, int k) { return s[k][32 + i]; }, [&](int c, int k) { return iv[k][c]; },
+        [&](int i, int c, double v) { tm[c][i] = v; });
   __syncthreads();
-  if (tid < 128) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) s[cb + q][row] = out[q];
-  }
+  for (int e = tid; e < 32 * 32; e += NT) s[e / 32][32 + e % 32] = tm[e / 32][e % 32];
   __syncthreads();
   // A22 -= L21 L21^T (lower)
-  if (tid < 128) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = 32 + cb + q;
-      if (c > row) continue;
-      double acc = 0.0;
-      for (int k = 0; k < 32; ++k) acc = fma(s[k][row], s[k][c], acc);
-      s[c][row] -= acc;
-    }
-  }
+  mma32([&](int i, int k) { return s[k][32 + i]; }, [&](int c, int k) { return s[k][32 + c]; },
+        [&](int i, int c, double v) {
+          if (i >= c) s[32 + c][32 + i] -= v;
+        });
   __syncthreads();
   if (warp == 0) leaf32(S, L, 32, IV + 32 * L + 32, L, status);
   __syncthreads();
-  // T = L21 I11 -> tm[c][i]  (T(i, c) = sum_{k >= c} L21(i, k) I11(k, c))
-  if (tid < 128) {
-    const int i = row - 32;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = cb + q;
-      double acc = 0.0;
-      for (int k = c; k < 32; ++k) acc = fma(s[k][row], iv[c][k], acc);
-      tm[c][i] = acc;
-    }
-  }
+  // T = L21 I11 : T(i, c) = sum_k L21(i, k) I11(k, c), I11(k, c) = iv[c][k]
+  mma32([&](int i, int k) { return s[k][32 + i]; }, [&](int c, int k) { return iv[c][k]; },
+        [&](int i, int c, double v) { tm[c][i] = v; });
   __syncthreads();
-  // I21(i, c) = -sum_{k <= i} I22(i, k) T(k, c)
-  if (tid < 128) {
-    const int i = row - 32;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = cb + q;
-      double acc = 0.0;
-      for (int k = 0; k <= i; ++k) acc = fma(iv[32 + k][32 + i], tm[c][k], acc);
-      iv[c][32 + i] = -acc;
-    }
-  }
+  // I21 = -I22 T : I21(i, c) = -sum_k I22(i, k) T(k, c), I22(i, k) = iv[32 + k][32 + i]
+  mma32([&](int i, int k) { return iv[32 + k][32 + i]; }, [&](int c, int k) { return tm[c][k]; },
+        [&](int i, int c, double v) { iv[c][32 + i] = -v; });
   __syncthreads();
   // L (lower) and inv^T (strict upper: inv(i, c), i > c, at block (row c, col i))
   for (int e = tid; e < kR * kR; e += NT) {
@@ -463,7 +459,9 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __global__ void __launch_bounds__(CfgG::THREADS) k_trsm_inv(TrsmInvParams p) {
   extern __shared__ double smem[];
   const int ld = p.ld, nI = ld / kR, nJ = ld / kR, P = nJ / 2;
-  const int I = blockIdx.x % nI, pair = blockIdx.x / nI;
+  // strip-major ids: the P CTAs that meet on a strip counter are dispatched
+  // consecutively, so at most one strip per kernel is ever partially resident
+  const int I = blockIdx.x / P, pair = blockIdx.x % P;
   const int Js[2] = {pair, nJ - 1 - pair};
   double acc0[CfgG::FM][CfgG::FN][2], acc1[CfgG::FM][CfgG::FN][2];
   zero_acc<CfgG>(acc0);

@@ -54,6 +54,8 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
   double* rrow = pw + 2 * kQrMaxSb;        // [2][sb] TSQRT: R row j
   double* wv = rrow + 2 * kQrMaxSb;        // [sb] reduced w / y
   double* slot = wv + kQrMaxSb;            // [2][2]: partial norm^2, alpha (owner of row j)
+  double* vv = slot + 4;                   // [R]  reflector entries of my rows for column jj
+  double* ph = vv + kQrMaxSb;              // [2][sb] half-row partial sums
   __shared__ double s_red[kQrThreads / 32];
   __shared__ double s_tau, s_beta, s_scal;
   double* T = p.side + size_t(ii) * ib;    // this panel's ib x sb T block (ld = ib)
@@ -95,61 +97,76 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     const int j = ii + jj;
     const int par = jj & 1;
     cl.sync();  // barrier 1: norms + alpha of column jj
-    if (tid == 0) {
-      double xn2 = 0.0, alpha = 0.0;
-      const int owner = ts ? -1 : (j / R);
-      for (int c2 = 0; c2 < kQrCl; ++c2) {
-        const double* sl = cl.map_shared_rank(slot, c2) + par * 2;
-        xn2 += sl[0];
-        if (c2 == owner) alpha = sl[1];
+    if (tid < 32) {
+      double xn2 = 0.0, al = 0.0;
+      if (tid < kQrCl) {
+        const double* sl = cl.map_shared_rank(slot, tid) + par * 2;
+        xn2 = sl[0];
+        al = sl[1];  // only the owner of row j publishes a non-zero alpha
       }
-      if (ts) alpha = rrow[par * kQrMaxSb + jj];
-      double tau = 0.0, beta = alpha, scal = 1.0;
-      if (xn2 != 0.0) {
-        const double xnorm = sqrt(xn2);
-        beta = -copysign(hypot(alpha, xnorm), alpha);
-        tau = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        xn2 += __shfl_xor_sync(0xffffffffu, xn2, o);
+        al += __shfl_xor_sync(0xffffffffu, al, o);
       }
-      s_tau = tau;
-      s_beta = beta;
-      s_scal = scal;
+      if (tid == 0) {
+        double alpha = ts ? rrow[par * kQrMaxSb + jj] : al;
+        double tau = 0.0, beta = alpha, scal = 1.0;
+        if (xn2 != 0.0) {
+          const double xnorm = sqrt(xn2);
+          beta = -copysign(hypot(alpha, xnorm), alpha);
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        s_tau = tau;
+        s_beta = beta;
+        s_scal = scal;
+      }
     }
     __syncthreads();
     const double tau = s_tau, beta = s_beta, scal = s_scal;
-    // scale my part of x; the owner of row j stores beta
+    // scale my part of x (the owner of row j stores beta) and stage v for the products
     for (int r = tid; r < R; r += kQrThreads) {
       int gr = row0 + r;
-      if (ts || gr > j) s[jj * LD + r] *= scal;
-      else if (gr == j) s[jj * LD + r] = beta;
+      double v = 0.0;
+      if (ts || gr > j) {
+        v = s[jj * LD + r] * scal;
+        s[jj * LD + r] = v;
+      } else if (gr == j) {
+        s[jj * LD + r] = beta;
+        v = 1.0;
+      }
+      vv[r] = v;
     }
     __syncthreads();
-    // partial products x^T [V | A] for every panel column c != jj
-    for (int c = warp; c < sb; c += kQrThreads / 32) {
-      double acc = 0.0;
-      if (c != jj) {
-        for (int r = lane; r < R; r += 32) {
-          int gr = row0 + r;
-          double v;
-          if (ts || gr > j) v = s[jj * LD + r];
-          else if (gr == j) v = 1.0;
-          else v = 0.0;
-          if (v != 0.0) {
-            // left columns hold stored reflectors (unit on their diagonal row)
-            double a = s[c * LD + r];
-            if (!ts && c < jj) a = (gr > ii + c) ? a : (gr == ii + c ? 1.0 : 0.0);
-            acc = fma(v, a, acc);
+    // partial products x^T [V | A]: two threads per panel column, each half of my rows.
+    // Left columns need no unit/zero mask: v_r != 0 only for rows >= j > ii + c.
+    {
+      const int c = tid % kQrMaxSb, half = tid / kQrMaxSb;
+      if (c < sb) {
+        const int rb = half * (R / 2), re = rb + R / 2;
+        double acc0 = 0.0, acc1 = 0.0;
+        if (c != jj) {
+          for (int r = rb; r < re; r += 2) {
+            acc0 = fma(vv[r], s[c * LD + r], acc0);
+            acc1 = fma(vv[r + 1], s[c * LD + r + 1], acc1);
           }
         }
+        ph[half * kQrMaxSb + c] = acc0 + acc1;
       }
-      acc = warp_sum(acc);
-      if (lane == 0) pw[par * kQrMaxSb + c] = acc;
     }
+    __syncthreads();
+    for (int c = tid; c < sb; c += kQrThreads) pw[par * kQrMaxSb + c] = ph[c] + ph[kQrMaxSb + c];
     cl.sync();  // barrier 2: partial products
     for (int c = tid; c < sb; c += kQrThreads) {
       double t = 0.0;
-      if (c != jj)
-        for (int c2 = 0; c2 < kQrCl; ++c2) t += cl.map_shared_rank(pw, c2)[par * kQrMaxSb + c];
+      if (c != jj) {
+        double part[kQrCl];
+#pragma unroll
+        for (int c2 = 0; c2 < kQrCl; ++c2) part[c2] = cl.map_shared_rank(pw, c2)[par * kQrMaxSb + c];
+#pragma unroll
+        for (int c2 = 0; c2 < kQrCl; ++c2) t += part[c2];
+      }
       if (ts && c > jj) t += rrow[par * kQrMaxSb + c];  // the unit of v_j sits in R row j
       wv[c] = t;
     }
@@ -366,7 +383,7 @@ static unsigned qr_panel_smem(int nb, int sb) {
   size_t d = size_t(sb) * (R + 1);
   size_t t = size_t(sb) * (sb + 1) + sb + 7 * 256;
   if (t > d) d = t;
-  d += 5 * kQrMaxSb + 4;
+  d += 8 * kQrMaxSb + 8;
   return unsigned(d * sizeof(double));
 }
 
