@@ -126,23 +126,29 @@ class ClockSampler:
 # -- inputs ----------------------------------------------------------------------
 
 def make_input(graph, n, nb, seed, torch):
-    """Synthetic SPD (R + R^T)/2 + n I, R ~ U(-0.5, 0.5) (torch Philox on the GPU),
-    written tile-major into pinned host memory."""
+    """Synthetic input (torch Philox on the GPU), tile-major in pinned host memory:
+    Cholesky: SPD (R + R^T)/2 + n I with R ~ U(-0.5, 0.5); LU / QR: R ~ U(-0.5, 0.5)."""
     gen = torch.Generator(device="cuda")
     gen.manual_seed(seed)
     R = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=gen) - 0.5
-    A = (R + R.T) * 0.5
-    del R
-    A.diagonal().add_(float(n))
+    if graph.layout.family == "cholesky":
+        A = (R + R.T) * 0.5
+        del R
+        A.diagonal().add_(float(n))
+    else:
+        A = R
     count = sum(graph.sizes) // 8
     img = torch.empty(count, dtype=torch.float64, pin_memory=True)
     off = 0
     lay = graph.layout
     for d, size in enumerate(graph.sizes):
         c = size // 8
-        i, j = lay.tiles[d]
-        # column-major tile = row-major transpose
-        img[off:off + c].copy_(A[i * nb:(i + 1) * nb, j * nb:(j + 1) * nb].T.contiguous().view(-1))
+        if d in lay.tiles:
+            i, j = lay.tiles[d]
+            # column-major tile = row-major transpose
+            img[off:off + c].copy_(A[i * nb:(i + 1) * nb, j * nb:(j + 1) * nb].T.contiguous().view(-1))
+        else:
+            img[off:off + c].zero_()
         off += c
     del A
     torch.cuda.empty_cache()
@@ -277,12 +283,12 @@ def run_ours(args, rank, world, local):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     k = world
-    n, nb = args.n, args.nb
-    g = H.gen_cholesky(n // nb, nb)
+    n, nb, fam = args.n, args.nb, args.family
+    g = H.gen_family(fam, n // nb, nb, args.ib)
     plat = H.build_platform(k, k, k, link_bandwidth=NVLINK_BW, link_latency=NVLINK_LAT,
                             switch_cap=math.inf, p2p=True)
     model, model_src = load_model(H, args)
-    flops = H.flops_of("cholesky", n)
+    flops = H.flops_of(fam, n)
     plans = {}
     plan_wall = {}
     for name, sch in (("dada", H.make_scheduler("dada", alpha=args.alpha, cp=True)), ("heft", H.make_scheduler("heft"))):
@@ -375,11 +381,11 @@ def run_ours(args, rank, world, local):
                "h2d_bytes_per_step": int(sum_over_ranks(info.bytes_h2d)),
                "d2h_bytes_per_step": int(sum_over_ranks(info.bytes_d2h)),
                "device_ms_per_step": ms_e2e, "wall_ms_per_step": wall_e2e}
-        if world == 1:
+        if world == 1 and fam == "cholesky":
             relres, _ = factor_check(g, host_in, out.numpy(), nb)
             check = {"randomized_relres": relres, "ok": bool(relres < 1e-12)}
         else:
-            check = {"note": "per-rank write-backs; factor parity covered by tests/test_gpu_multirank.py"}
+            check = {"note": "factor parity covered by tests/test_gpu_*.py (per-rank write-backs / non-Cholesky)"}
 
     # the probe is short: take the better of a cold (pre-run) and a warm (post-run) measurement
     dmma2, dfma2 = _native.fp64_peak(local)
@@ -395,14 +401,16 @@ def run_ours(args, rank, world, local):
                 "step_frac": (flops / (results["dada"]["ms_per_step"] * 1e-3) / 1e12) / dmma_peak,
                 "gemm_launch_us": t_gemm * 1e6}
     cpu = None
-    if not args.no_cpu_baseline and rank == 0 and world == 1:
+    if not args.no_cpu_baseline and rank == 0 and world == 1 and fam == "cholesky":
         cpu = cpu_baseline_sample(args.cpu_n, nb)
     d = results["dada"]
     line = {
         "metric": METRIC, "value": d["gflops"], "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": d["ms_per_step"], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"tiled Cholesky N={n} nb={nb} FP64 (BASELINE configs[1])", "family": "cholesky",
+        "config": {"workload": (f"tiled Cholesky N={n} nb={nb} FP64 (BASELINE configs[1])" if fam == "cholesky"
+                                else f"tiled {fam.upper()} N={n} nb={nb} ib={args.ib} FP64 (BASELINE configs[{2 if fam == 'lu' else 3}])"),
+                   "family": fam,
                    "n": n, "nb": nb, "scheduler": f"DADA(alpha={args.alpha})+CP vs HEFT", "k": k,
                    "cost_model": model_src, "l2": "inputs (tiles) > L2, no flush"},
         "nvlink_bytes": {"dada": d["bytes_d2d"], "heft": results["heft"]["bytes_d2d"]},

@@ -289,6 +289,7 @@ struct LuApplyParams {
   double* top;          // tile whose rows [ii, ii+sb) are transformed
   double* bot;          // GETRF-type: == top; TSTRF-type: the other tile
   int nb, ib, p0, p1, col0, mode;
+  int swap_only;        // 1: row interchanges + inv(L_uu)*top only (the bot update is a separate wide GEMM)
 };
 
 template <int SB>
@@ -370,6 +371,7 @@ __global__ void __launch_bounds__(ApplyCfg<SB>::G::THREADS) k_lu_apply(LuApplyPa
     }
     __threadfence();
     __syncthreads();
+    if (p.swap_only) continue;
     // ---- 3) bot -= L_a * top ------------------------------------------------------
     const int m_begin = ts ? 0 : ii + SB;
     for (int m0 = m_begin; m0 < nb; m0 += SB) {
@@ -385,6 +387,34 @@ __global__ void __launch_bounds__(ApplyCfg<SB>::G::THREADS) k_lu_apply(LuApplyPa
     __syncthreads();
   }
 }
+
+// ---------------------------------------------------------------------------
+// C -= A * B with A M_MAJOR (element (m, k) at A[k*lda + m]) and B K_MAJOR
+// (element (n, k) at B[n*ldb + k]): the trailing "bot -= L_a * top" of one
+// panel as a full-width DMMA GEMM (64x64 CTA tiles).
+using CfgN = GemmCfg<64, 64, 16, 32, 32, 3>;
+
+struct GemmNNParams {
+  const double* A;
+  const double* B;
+  double* C;
+  int lda, ldb, ldc, K;
+};
+
+__global__ void __launch_bounds__(CfgN::THREADS) k_gemm_nn(GemmNNParams p) {
+  extern __shared__ double smem[];
+  const int m0 = blockIdx.x * CfgN::BM, n0 = blockIdx.y * CfgN::BN;
+  double acc[CfgN::FM][CfgN::FN][2];
+  zero_acc<CfgN>(acc);
+  TileLoader<CfgN, M_MAJOR, CfgN::BM> la{p.A, p.lda, m0};
+  TileLoader<CfgN, K_MAJOR, CfgN::BN> lb{p.B, p.ldb, n0};
+  gemm_mainloop<CfgN>(acc, smem, la, lb, 0, p.K);
+  double* C = p.C;
+  const int ldc = p.ldc;
+  for_each_acc<CfgN>(acc, [&](int r, int c, double v) { C[size_t(n0 + c) * ldc + m0 + r] -= v; });
+}
+
+static unsigned nn_smem() { return (unsigned)GemmSmem<CfgN, M_MAJOR, K_MAJOR>::BYTES; }
 
 // ---------------------------------------------------------------------------
 static unsigned panel_smem(int nb, int sb) {
@@ -417,6 +447,7 @@ bool init_lu_attributes() {
   HG_ATTR(k_lu_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
   HG_ATTR(k_lu_apply<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem<128>(1024));
   HG_ATTR(k_lu_apply<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem<64>(1024));
+  HG_ATTR(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, nn_smem());
   return true;
 }
 
@@ -429,6 +460,23 @@ static void push_apply(std::vector<LaunchDesc>& out, int ib, const LuApplyParams
   else
     d.set((const void*)k_lu_apply<64>, dim3(ncols / ApplyCfg<64>::BN), dim3(ApplyCfg<64>::G::THREADS),
           apply_smem<64>(ap.nb), ap);
+  out.push_back(d);
+}
+
+// One panel applied to columns [col0, nb): narrow swap + inv(L_uu) kernel,
+// then the wide bot -= L_a * top GEMM.
+static void push_panel_apply(std::vector<LaunchDesc>& out, int ib, const double* L, const double* side,
+                             double* top, double* bot, int nb, int P, int col0, int mode) {
+  LuApplyParams ap{L, side, top, bot, nb, ib, P, P + 1, col0, mode, 1};
+  push_apply(out, ib, ap);
+  const int ii = P * ib;
+  const bool ts = mode == LU_TSTRF;
+  const int m0 = ts ? 0 : ii + ib;
+  const int M = nb - m0, N = nb - col0;
+  if (M <= 0 || N <= 0) return;
+  GemmNNParams gp{L + size_t(ii) * nb + m0, top + size_t(col0) * nb + ii, bot + size_t(col0) * nb + m0, nb, nb, nb, ib};
+  LaunchDesc d;
+  d.set((const void*)k_gemm_nn, dim3(M / CfgN::BM, N / CfgN::BN), dim3(CfgN::THREADS), nn_smem(), gp);
   out.push_back(d);
 }
 
@@ -452,24 +500,18 @@ bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
         LaunchDesc d;
         d.set((const void*)k_lu_panel, dim3(kLuCl), dim3(kLuThreads), panel_smem(nb, ib), pp);
         out.push_back(d);
-        if (P + 1 < np) {
-          LuApplyParams ap{A, ts ? side(1) : side(0), ts ? o.t[0] : A, A, nb, ib, P, P + 1, (P + 1) * ib,
-                           ts ? LU_TSTRF : LU_GETRF};
-          push_apply(out, ib, ap);
-        }
+        if (P + 1 < np)
+          push_panel_apply(out, ib, A, ts ? side(1) : side(0), ts ? o.t[0] : A, A, nb, P, (P + 1) * ib,
+                           ts ? LU_TSTRF : LU_GETRF);
       }
       return true;
     }
-    case K_GESSM: {
-      LuApplyParams ap{o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF};
-      push_apply(out, ib, ap);
+    case K_GESSM:
+      for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[1], nb, P, 0, LU_GETRF);
       return true;
-    }
-    case K_SSSSM: {
-      LuApplyParams ap{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF};
-      push_apply(out, ib, ap);
+    case K_SSSSM:
+      for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[2], nb, P, 0, LU_TSTRF);
       return true;
-    }
     default:
       set_error("kind %d is not an LU kind", kind);
       return false;
