@@ -218,3 +218,41 @@ HG_DEVICE void gemm_mainloop_bsmem(double (&acc)[Cfg::FM][Cfg::FN][2], double* r
 }
 
 }  // namespace hg
+
+namespace hg {
+
+// C(m0 + r, n0 + c) = (init ? 0 : C) - acc(r, c) for the CTA tile, with all C
+// loads issued before any store (a read-modify-write through a lambda would
+// order every load behind the previous store: one L2 round trip per element).
+// lower: skip r < c of a diagonal tile (m0 == n0).
+template <class Cfg>
+HG_DEVICE void sub_store(double (&acc)[Cfg::FM][Cfg::FN][2], double* __restrict__ C, int ldc, int m0, int n0,
+                         bool lower = false, bool init = false) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+  const bool diag = lower && (m0 == n0);
+  double cv[Cfg::FM][Cfg::FN][2];
+  if (!init) {
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) {
+        const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t;
+        cv[i][j][0] = C[size_t(n0 + c) * ldc + m0 + r];
+        cv[i][j][1] = C[size_t(n0 + c + 1) * ldc + m0 + r];
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) {
+      const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t;
+      const double b0 = init ? 0.0 : cv[i][j][0], b1 = init ? 0.0 : cv[i][j][1];
+      if (!diag || r >= c) C[size_t(n0 + c) * ldc + m0 + r] = b0 - acc[i][j][0];
+      if (!diag || r >= c + 1) C[size_t(n0 + c + 1) * ldc + m0 + r] = b1 - acc[i][j][1];
+    }
+}
+
+}  // namespace hg

@@ -48,14 +48,7 @@ __global__ void __launch_bounds__(CfgG::THREADS) k_gemm_nt(GemmNTParams p) {
   TileLoader<CfgG, M_MAJOR, CfgG::BM> la{p.A, p.ld, m0};
   TileLoader<CfgG, M_MAJOR, CfgG::BN> lb{p.B, p.ld, n0};
   gemm_mainloop<CfgG>(acc, smem, la, lb, 0, p.K);
-  const bool diag = p.lower && (m0 == n0);
-  double* C = p.C;
-  const int ld = p.ld;
-  for_each_acc<CfgG>(acc, [&](int r, int c, double v) {
-    if (diag && r < c) return;
-    size_t idx = size_t(n0 + c) * ld + m0 + r;
-    C[idx] -= v;
-  });
+  sub_store<CfgG>(acc, p.C, p.ld, m0, n0, p.lower != 0, false);
 }
 
 // ---------------------------------------------------------------------------
@@ -124,46 +117,46 @@ __device__ void diag_factor_inverse(double* A, int ld, int j0, int* status, doub
 // __syncthreads inside); the off-diagonal products are spread over 128 threads.
 //   L11, I11 = leaf(A11);  L21 = A21 I11^T;  A22 -= L21 L21^T;
 //   L22, I22 = leaf(A22);  I21 = -I22 (L21 I11)
-__device__ __forceinline__ void leaf32(double* s, int lds, int r0, double* iv, int ldi, int* status) {
+__device__ __noinline__ void leaf32(double* s, int lds, int r0, double* iv, int ldi, int* status) {
+  // one warp; the 32x32 block stays in shared memory (B[c*lds + r] = element (r, c)),
+  // loops stay rolled: small code, no local memory
   const int lane = threadIdx.x & 31;
-  double a[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) a[k] = (k <= lane) ? s[(r0 + k) * lds + r0 + lane] : 0.0;
+  double* B = s + r0 * lds + r0;
   bool bad = false;
-#pragma unroll
   for (int j = 0; j < 32; ++j) {
-    double ajj = __shfl_sync(0xffffffffu, a[j], j);
-    if (!(ajj > 0.0)) {
+    double d = B[j * lds + j];
+    if (!(d > 0.0)) {
       bad = true;
-      ajj = 1.0;
+      d = 1.0;
     }
-    const double d = sqrt(ajj);
+    d = sqrt(d);
     const double rd = 1.0 / d;
-    a[j] = (lane == j) ? d : (lane > j ? a[j] * rd : a[j]);
-#pragma unroll
+    const double lj = lane > j ? B[j * lds + lane] * rd : 0.0;
+    __syncwarp();
+    if (lane == j) B[j * lds + j] = d;
+    if (lane > j) B[j * lds + lane] = lj;
+    __syncwarp();
     for (int k = j + 1; k < 32; ++k) {
-      const double lk = __shfl_sync(0xffffffffu, a[j], k);
-      if (lane >= k) a[k] = fma(-a[j], lk, a[k]);
+      const double lk = B[j * lds + k];
+      if (lane >= k) B[k * lds + lane] = fma(-lj, lk, B[k * lds + lane]);
     }
+    __syncwarp();
   }
   if (bad && lane == 0 && status) atomicOr(status, 1);
-#pragma unroll
-  for (int k = 0; k < 32; ++k)
-    if (k <= lane) s[(r0 + k) * lds + r0 + lane] = a[k];
-  __syncwarp();
-  // inverse: lane c computes column c, x = L^{-1} e_c (broadcast smem reads of L)
-  double x[32];
-#pragma unroll
+  // inverse: lane c computes column c of L^{-1} (stored iv[c*ldi + i] = inv(i, c))
+  const int c = lane;
+  double* x = iv + c * ldi;
   for (int i = 0; i < 32; ++i) {
-    const double rli = 1.0 / s[(r0 + i) * lds + r0 + i];
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < i; ++k)
-      if (k >= lane) acc = fma(s[(r0 + k) * lds + r0 + i], x[k], acc);
-    x[i] = (i == lane) ? rli : (i > lane ? -acc * rli : 0.0);
+    const double rli = 1.0 / B[i * lds + i];
+    double v = 0.0;
+    if (i == c) v = rli;
+    else if (i > c) {
+      double acc = 0.0;
+      for (int k = c; k < i; ++k) acc = fma(B[k * lds + i], x[k], acc);
+      v = -acc * rli;
+    }
+    x[i] = v;
   }
-#pragma unroll
-  for (int i = 0; i < 32; ++i) iv[lane * ldi + i] = x[i];  // iv[c][i] = inv(i, c)
   __syncwarp();
 }
 
@@ -345,11 +338,7 @@ __device__ void block_update(double* Cp, int ld, const LdA& la, const LdB& lb, b
   double acc[CfgG::FM][CfgG::FN][2];
   zero_acc<CfgG>(acc);
   gemm_mainloop<CfgG>(acc, smem, la, lb, 0, kR);
-  for_each_acc<CfgG>(acc, [&](int r, int c, double v) {
-    if (lower && r < c) return;
-    double* q = Cp + size_t(c) * ld + r;
-    *q = init ? -v : *q - v;
-  });
+  sub_store<CfgG>(acc, Cp, ld, 0, 0, lower, init);
   __syncthreads();
 }
 

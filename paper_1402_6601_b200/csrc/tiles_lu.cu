@@ -91,9 +91,21 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
     for (int e = tid; e < ib * sb; e += kLuThreads) inv[e] = 0.0;
   __syncthreads();
 
+  // Per column: 1 CTA barrier + 1 cluster barrier (phase A), 2 CTA barriers
+  // (phase B).  The scaled multiplier of column jj is written back to smem at
+  // the start of column jj+1 (before its first barrier), so the update never
+  // races with the read of the unscaled value.
+  const int ngroup = kLuThreads / R;
+  const int my_r = tid % R, my_grp = tid / R;
+  double pend_l = 0.0;
+  int pend_c = -1;
   for (int jj = 0; jj < sb; ++jj) {
     const int j = ii + jj;
     const int par = jj & 1;
+    if (pend_c >= 0) {
+      s[pend_c * LD + my_r] = pend_l;
+      pend_c = -1;
+    }
     // ---- phase A: local arg-max, publish candidate row --------------------
     if (ts)  // U row j (columns >= jj): issued first so its latency hides behind the arg-max
       for (int c = tid; c < sb; c += kLuThreads) urow[par * kLuMaxSb + c] = c >= jj ? p.U[size_t(ii + c) * nb + j] : 0.0;
@@ -124,20 +136,19 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
       red_r[tid >> 5] = br;
     }
     __syncthreads();
-    if (tid == 0) {
+    {
       double v = red_v[0];
       int r = red_r[0];
+#pragma unroll
       for (int w = 1; w < kLuThreads / 32; ++w)
         if (better(red_v[w], red_r[w], v, r)) {
           v = red_v[w];
           r = red_r[w];
         }
-      slot_v[par] = v;
-      slot_r[par] = r;
-    }
-    __syncthreads();
-    {
-      const int r = slot_r[par];
+      if (tid == 0) {
+        slot_v[par] = v;
+        slot_r[par] = r;
+      }
       const bool mine = r >= row0 && r < row0 + R;
       for (int c = tid; c < sb; c += kLuThreads) {
         cand[par * kLuMaxSb + c] = mine ? s[c * LD + (r - row0)] : 0.0;
@@ -145,13 +156,17 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
       }
     }
     cl.sync();
-    // ---- phase B: global pivot decision (identical in every CTA) ------------
-    if (tid < 32) {
+    // ---- phase B: every warp resolves the global pivot itself ---------------
+    int wr, wc;
+    bool swap;
+    {
       double v = -1.0;
-      int r = 0x7fffffff, who = tid;
-      if (tid < kLuCl) {
-        v = cl.map_shared_rank(slot_v, tid)[par];
-        r = cl.map_shared_rank(slot_r, tid)[par];
+      int r = 0x7fffffff, who = 0;
+      const int l8 = tid & 31;
+      if (l8 < kLuCl) {
+        v = cl.map_shared_rank(slot_v, l8)[par];
+        r = cl.map_shared_rank(slot_r, l8)[par];
+        who = l8;
       }
 #pragma unroll
       for (int o = 4; o > 0; o >>= 1) {
@@ -164,32 +179,15 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
           who = ow;
         }
       }
-      if (tid == 0) {
-        s_win_row = r;
-        s_win_cta = who;
-        if (ts) s_swap = v > fabs(urow[par * kLuMaxSb + jj]) ? 1 : 0;
-        else s_swap = (r != j) ? 1 : 0;
-      }
+      wr = __shfl_sync(0xffffffffu, r, 0);
+      wc = __shfl_sync(0xffffffffu, who, 0);
+      v = __shfl_sync(0xffffffffu, v, 0);
+      swap = ts ? (v > fabs(urow[par * kLuMaxSb + jj])) : (wr != j);
     }
-    __syncthreads();
-    const int wr = s_win_row, wc = s_win_cta;
-    const bool swap = s_swap != 0;
-    {
-      const double* wc_cand = cl.map_shared_rank(cand, wc) + par * kLuMaxSb;
-      for (int c = tid; c < sb; c += kLuThreads) {
-        double v;
-        if (ts) v = swap ? wc_cand[c] : urow[par * kLuMaxSb + c];
-        else v = wc_cand[c];
-        prow[c] = v;
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      s_piv = prow[jj];
-      if (q == 0) ipiv[j] = ts ? (swap ? wr : -1) : wr;
-      if (s_piv == 0.0 && q == 0 && p.status) atomicOr(p.status, 2);
-    }
-    // swaps by the owners
+    const double* wcand = cl.map_shared_rank(cand, wc) + par * kLuMaxSb;
+    for (int c = tid; c < sb; c += kLuThreads) prow[c] = (ts && !swap) ? urow[par * kLuMaxSb + c] : wcand[c];
+    if (tid == 0 && q == 0) ipiv[j] = ts ? (swap ? wr : -1) : wr;
+    // swaps by the owners, straight from the published (pre-swap) buffers
     if (ts) {
       if (swap && wr >= row0 && wr < row0 + R) {
         const int lr = wr - row0;
@@ -198,39 +196,39 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
             inv[size_t(c) * ib + jj] = s[c * LD + lr];  // dL(jj, c), inverted at panel end
             s[c * LD + lr] = 0.0;
           } else {
-            p.U[size_t(ii + c) * nb + j] = prow[c];
+            p.U[size_t(ii + c) * nb + j] = wcand[c];
             s[c * LD + lr] = urow[par * kLuMaxSb + c];
           }
         }
       }
     } else if (swap) {
       if (wr >= row0 && wr < row0 + R) {  // row p <- old row j
-        const int oj = (j - j % R) / R;   // owner CTA of row j
-        const double* src = cl.map_shared_rank(rowj, oj) + par * kLuMaxSb;
+        const double* src = cl.map_shared_rank(rowj, j / R) + par * kLuMaxSb;
         for (int c = tid; c < sb; c += kLuThreads) s[c * LD + (wr - row0)] = src[c];
       }
       if (j >= row0 && j < row0 + R)
-        for (int c = tid; c < sb; c += kLuThreads) s[c * LD + (j - row0)] = prow[c];
+        for (int c = tid; c < sb; c += kLuThreads) s[c * LD + (j - row0)] = wcand[c];
     }
     __syncthreads();
-    const double piv = s_piv;
-    if (piv != 0.0) {
-      // each thread owns one row r and a 1/ngroup share of the columns; the
-      // multiplier is recomputed per group, so no barrier between scale and update
+    const double piv = prow[jj];
+    if (piv == 0.0) {
+      if (tid == 0 && q == 0 && p.status) atomicOr(p.status, 2);
+    } else {
       const double rcp = 1.0 / piv;
-      const int ngroup = kLuThreads / R;
-      const int r = tid % R, grp = tid / R;
-      const int gr = row0 + r;
-      const bool act = grp < ngroup && (ts || gr > j);
-      const double l = act ? s[jj * LD + r] * rcp : 0.0;
-      __syncthreads();  // every group has read the unscaled value
-      if (act) {
-        for (int c = jj + 1 + grp; c < sb; c += ngroup) s[c * LD + r] = fma(-l, prow[c], s[c * LD + r]);
-        if (grp == 0) s[jj * LD + r] = l;
+      const int gr = row0 + my_r;
+      if (my_grp < ngroup && (ts || gr > j)) {
+        const double l = s[jj * LD + my_r] * rcp;
+        for (int c = jj + 1 + my_grp; c < sb; c += ngroup) s[c * LD + my_r] = fma(-l, prow[c], s[c * LD + my_r]);
+        if (my_grp == 0) {
+          pend_l = l;
+          pend_c = jj;
+        }
       }
     }
     __syncthreads();
   }
+  if (pend_c >= 0) s[pend_c * LD + my_r] = pend_l;
+  __syncthreads();
   cl.sync();
   // ---- write the panel back ----------------------------------------------------
   for (int e = tid; e < sb * R; e += kLuThreads) {
@@ -380,8 +378,7 @@ __global__ void __launch_bounds__(ApplyCfg<SB>::G::THREADS) k_lu_apply(LuApplyPa
       TileLoader<G, M_MAJOR, G::BM> la{p.L + size_t(ii) * nb, nb, m0};
       TileLoader<G, K_MAJOR, G::BN> lb{p.top + ii, nb, n0};
       gemm_mainloop<G>(acc, sm, la, lb, 0, SB);
-      double* bot = p.bot;
-      for_each_acc<G>(acc, [&](int r, int c, double v) { bot[size_t(n0 + c) * nb + m0 + r] -= v; });
+      sub_store<G>(acc, p.bot, nb, m0, n0);
     }
     __threadfence();
     __syncthreads();
@@ -409,9 +406,7 @@ __global__ void __launch_bounds__(CfgN::THREADS) k_gemm_nn(GemmNNParams p) {
   TileLoader<CfgN, M_MAJOR, CfgN::BM> la{p.A, p.lda, m0};
   TileLoader<CfgN, K_MAJOR, CfgN::BN> lb{p.B, p.ldb, n0};
   gemm_mainloop<CfgN>(acc, smem, la, lb, 0, p.K);
-  double* C = p.C;
-  const int ldc = p.ldc;
-  for_each_acc<CfgN>(acc, [&](int r, int c, double v) { C[size_t(n0 + c) * ldc + m0 + r] -= v; });
+  sub_store<CfgN>(acc, p.C, p.ldc, m0, n0);
 }
 
 static unsigned nn_smem() { return (unsigned)GemmSmem<CfgN, M_MAJOR, K_MAJOR>::BYTES; }

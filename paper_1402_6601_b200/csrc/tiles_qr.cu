@@ -369,8 +369,7 @@ __global__ void __launch_bounds__(CfgQ::THREADS) k_qr_apply(QrApplyParams p) {
       zero_acc<CfgQ>(acc);
       VLoader<CfgQ, M_MAJOR, 128> la{Vp, nb, m0, ii, ts ? 0 : 1};
       gemm_mainloop_bsmem<CfgQ>(acc, ring, la, W, kWld, 0, 128);
-      double* C = ts ? p.bot : p.top;
-      for_each_acc<CfgQ>(acc, [&](int r, int c, double v) { C[size_t(n0 + c) * nb + m0 + r] -= v; });
+      sub_store<CfgQ>(acc, ts ? p.bot : p.top, nb, m0, n0);
     }
     __threadfence();
     __syncthreads();

@@ -46,10 +46,7 @@ __global__ void __launch_bounds__(Cfg::THREADS) gemm_nt_bench(const double* A, c
   hg::TileLoader<Cfg, hg::M_MAJOR, Cfg::BM> la{a, nb, m0};
   hg::TileLoader<Cfg, hg::M_MAJOR, Cfg::BN> lb{b, nb, n0};
   hg::gemm_mainloop<Cfg>(acc, smem, la, lb, 0, nb);
-  hg::for_each_acc<Cfg>(acc, [&](int r, int cc, double v) {
-    size_t idx = size_t(n0 + cc) * nb + m0 + r;
-    c[idx] -= v;
-  });
+  hg::sub_store<Cfg>(acc, c, nb, m0, n0);
 }
 
 __global__ void gemm_nt_ref(const double* A, const double* B, double* C, int nb) {
