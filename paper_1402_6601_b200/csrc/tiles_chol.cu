@@ -236,6 +236,58 @@ __device__ void diag_factor_inverse_fast(double* A, int ld, int j0, int* status,
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// 64x64 Cholesky + inverse by 128 threads with two barriers per column.
+// X = L^{-1} is built row by row in the same sweep: with R = I initially,
+//   X(j, :) = R(j, :) / L(j, j)   and   R(i, c) -= L(i, j) X(j, c)  (i > j, c <= j),
+// the second update riding in the same pass as the Cholesky trailing update.
+// Two threads per row; the reciprocal square root gives both L(j,j) and 1/L(j,j).
+__device__ void diag64_coop(double* A, int ld, int j0, int* status, double (*s)[kR + 1], double (*iv)[kR + 1]) {
+  double* blk = A + size_t(j0) * ld + j0;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kR * kR; e += 128) {
+    int c = e / kR, r = e % kR;
+    s[c][r] = __ldcg(blk + size_t(c) * ld + r);
+    iv[c][r] = (r == c) ? 1.0 : 0.0;  // R = I  (iv[c][i] = R(i, c))
+  }
+  __syncthreads();
+  const int row = tid >> 1, half = tid & 1;
+  bool bad = false;
+  for (int j = 0; j < kR; ++j) {
+    double ajj = s[j][j];
+    if (!(ajj > 0.0)) {
+      bad = true;
+      ajj = 1.0;
+    }
+    const double rj = rsqrt(ajj);
+    // phase 1: column j of L, row j of X
+    if (tid < kR) {
+      if (tid > j) s[j][tid] *= rj;
+      else if (tid == j) s[j][j] = ajj * rj;
+    } else {
+      const int c = tid - kR;
+      if (c <= j) iv[c][j] *= rj;
+    }
+    __syncthreads();
+    // phase 2: trailing Cholesky update of row i and the R update of row i
+    if (row > j) {
+      const double li = s[j][row];
+      for (int k = half; k <= row; k += 2) {
+        if (k <= j) iv[k][row] = fma(-li, iv[k][j], iv[k][row]);
+        else s[k][row] = fma(-li, s[j][k], s[k][row]);
+      }
+    }
+    __syncthreads();
+  }
+  if (bad && tid == 0 && status) atomicOr(status, 1);
+  // L (lower) and inv^T (strict upper: inv(i, c), i > c, at block (row c, col i))
+  for (int e = tid; e < kR * kR; e += 128) {
+    int c = e / kR, r = e % kR;
+    blk[size_t(c) * ld + r] = (r >= c) ? s[c][r] : iv[r][c];
+  }
+  __syncthreads();
+}
+
 struct PotrfDiagParams {
   double* A;
   int ld, j0;
@@ -278,14 +330,22 @@ __device__ void apply_inv_right(double* blk, int ld, const double* Lb, double* s
   double* sS = smem;            // [k][row], ld kR+4
   double* sI = smem + kSolveS;  // [j][k],  ld kR+4
   const int tid = threadIdx.x;
+  // both 64x64 blocks are column-contiguous in global: stage them with cp.async
+  for (int e = tid; e < kR * (kR / 2); e += CfgG::THREADS) {
+    int c = e / (kR / 2), r = (e % (kR / 2)) * 2;
+    cp_async16(sS + c * (kR + 4) + r, blk + size_t(c) * ld + r);
+    cp_async16(sI + c * (kR + 4) + r, Lb + size_t(c) * ld + r);  // row j=c holds inv(j, k<j) at k=r
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  // the raw rows hold L(k, j) for k >= j: diagonal -> 1/L(j, j), below -> 0
   for (int e = tid; e < kR * kR; e += CfgG::THREADS) {
-    int c = e / kR, r = e % kR;
-    sS[c * (kR + 4) + r] = __ldcg(blk + size_t(c) * ld + r);
-    double v;
-    if (r < c) v = __ldcg(Lb + size_t(c) * ld + r);
-    else if (r == c) v = 1.0 / __ldcg(Lb + size_t(c) * ld + c);
-    else v = 0.0;
-    sI[c * (kR + 4) + r] = v;
+    int j = e / kR, k = e % kR;
+    if (k >= j) {
+      double* q = sI + j * (kR + 4) + k;
+      *q = (k == j) ? 1.0 / *q : 0.0;
+    }
   }
   __syncthreads();
   const int warp = tid >> 5, lane = tid & 31;
@@ -353,7 +413,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
   const int nb = p.nb, nJ = nb / kR, ld = nb;
   double* A = p.A;
   auto blk = [&](int I, int K) { return A + size_t(K) * kR * ld + size_t(I) * kR; };  // block (I, K)
-  if (q == 0) diag_factor_inverse_fast<CfgG::THREADS>(A, nb, 0, p.status, s, iv, tm);
+  if (q == 0) diag64_coop(A, nb, 0, p.status, s, iv);
   __threadfence();
   cl.sync();
   for (int J = 0; J < nJ; ++J) {
@@ -370,7 +430,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
       TileLoader<CfgG, M_MAJOR, kR> la{blk(0, J), ld, (J + 1) * kR};
       block_update(blk(J + 1, J + 1), ld, la, la, true, false, smem);
       __threadfence();
-      diag_factor_inverse_fast<CfgG::THREADS>(A, nb, (J + 1) * kR, p.status, s, iv, tm);
+      diag64_coop(A, nb, (J + 1) * kR, p.status, s, iv);
     } else {
       int t = 0;
       const int others = kPotrfCl - 1;
