@@ -237,53 +237,83 @@ __device__ void diag_factor_inverse_fast(double* A, int ld, int j0, int* status,
 }
 
 // ---------------------------------------------------------------------------
-// 64x64 Cholesky + inverse by 128 threads with two barriers per column.
-// X = L^{-1} is built row by row in the same sweep: with R = I initially,
-//   X(j, :) = R(j, :) / L(j, j)   and   R(i, c) -= L(i, j) X(j, c)  (i > j, c <= j),
-// the second update riding in the same pass as the Cholesky trailing update.
-// Two threads per row; the reciprocal square root gives both L(j,j) and 1/L(j,j).
-__device__ void diag64_coop(double* A, int ld, int j0, int* status, double (*s)[kR + 1], double (*iv)[kR + 1]) {
+// 64x64 Cholesky + inverse by 128 threads, register resident.  Thread t owns
+// row i = t/2, columns k = 2m + (t&1) (m < 32) of both A (-> L) and R (-> X =
+// L^{-1}; R = I initially).  Per column j, two barriers:
+//   1: column-j owners scale L(i, j) = A(i, j) / sqrt(A(j, j)) and publish it;
+//      the two owners of row j publish X(j, :) = R(j, :) / L(j, j)
+//   2: every thread updates its registers from the published column / row
+//      (independent smem loads), the owner of (j+1, j+1) publishes the next pivot.
+// Broadcast buffers are double-buffered by column parity.
+__device__ void diag64_reg(double* A, int ld, int j0, int* status, double* bufs) {
   double* blk = A + size_t(j0) * ld + j0;
   const int tid = threadIdx.x;
-  for (int e = tid; e < kR * kR; e += 128) {
-    int c = e / kR, r = e % kR;
-    s[c][r] = __ldcg(blk + size_t(c) * ld + r);
-    iv[c][r] = (r == c) ? 1.0 : 0.0;  // R = I  (iv[c][i] = R(i, c))
+  const int i = tid >> 1, h = tid & 1;
+  double* colj = bufs;              // [2][64]
+  double* rowx = bufs + 2 * kR;     // [2][64]
+  double* diag = bufs + 4 * kR;     // [2]
+  double a[32], r[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int k = 2 * m + h;
+    a[m] = (k <= i) ? __ldcg(blk + size_t(k) * ld + i) : 0.0;
+    r[m] = (k == i) ? 1.0 : 0.0;
   }
-  __syncthreads();
-  const int row = tid >> 1, half = tid & 1;
+  if (tid == 0) diag[0] = a[0];
   bool bad = false;
+  __syncthreads();
   for (int j = 0; j < kR; ++j) {
-    double ajj = s[j][j];
-    if (!(ajj > 0.0)) {
+    const int par = j & 1;
+    double djj = diag[par];
+    if (!(djj > 0.0)) {
       bad = true;
-      ajj = 1.0;
+      djj = 1.0;
     }
-    const double rj = rsqrt(ajj);
-    // phase 1: column j of L, row j of X
-    if (tid < kR) {
-      if (tid > j) s[j][tid] *= rj;
-      else if (tid == j) s[j][j] = ajj * rj;
-    } else {
-      const int c = tid - kR;
-      if (c <= j) iv[c][j] *= rj;
+    const double rj = rsqrt(djj);
+    if (h == (j & 1)) {
+#pragma unroll
+      for (int m = 0; m < 32; ++m)
+        if (2 * m + h == j) {
+          if (i > j) {
+            a[m] *= rj;
+            colj[par * kR + i] = a[m];
+          } else if (i == j) {
+            a[m] = djj * rj;
+          }
+        }
+    }
+    if (i == j) {
+#pragma unroll
+      for (int m = 0; m < 32; ++m)
+        if (2 * m + h <= j) {
+          r[m] *= rj;
+          rowx[par * kR + 2 * m + h] = r[m];
+        }
     }
     __syncthreads();
-    // phase 2: trailing Cholesky update of row i and the R update of row i
-    if (row > j) {
-      const double li = s[j][row];
-      for (int k = half; k <= row; k += 2) {
-        if (k <= j) iv[k][row] = fma(-li, iv[k][j], iv[k][row]);
-        else s[k][row] = fma(-li, s[j][k], s[k][row]);
+    if (i > j) {
+      const double li = colj[par * kR + i];
+#pragma unroll
+      for (int m = 0; m < 32; ++m) {
+        const int k = 2 * m + h;
+        if (k > j && k <= i) a[m] = fma(-li, colj[par * kR + k], a[m]);
+        if (k <= j) r[m] = fma(-li, rowx[par * kR + k], r[m]);
       }
+    }
+    if (i == j + 1 && h == ((j + 1) & 1)) {
+#pragma unroll
+      for (int m = 0; m < 32; ++m)
+        if (2 * m + h == j + 1) diag[par ^ 1] = a[m];
     }
     __syncthreads();
   }
   if (bad && tid == 0 && status) atomicOr(status, 1);
-  // L (lower) and inv^T (strict upper: inv(i, c), i > c, at block (row c, col i))
-  for (int e = tid; e < kR * kR; e += 128) {
-    int c = e / kR, r = e % kR;
-    blk[size_t(c) * ld + r] = (r >= c) ? s[c][r] : iv[r][c];
+  // L (lower) and X^T in the strict upper triangle: position (row c, col i) <- X(i, c), c < i
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int k = 2 * m + h;
+    if (k <= i) blk[size_t(k) * ld + i] = a[m];
+    if (k < i) blk[size_t(i) * ld + k] = r[m];
   }
   __syncthreads();
 }
@@ -413,7 +443,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
   const int nb = p.nb, nJ = nb / kR, ld = nb;
   double* A = p.A;
   auto blk = [&](int I, int K) { return A + size_t(K) * kR * ld + size_t(I) * kR; };  // block (I, K)
-  if (q == 0) diag64_coop(A, nb, 0, p.status, s, iv);
+  if (q == 0) diag64_reg(A, nb, 0, p.status, &s[0][0]);
   __threadfence();
   cl.sync();
   for (int J = 0; J < nJ; ++J) {
@@ -430,7 +460,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
       TileLoader<CfgG, M_MAJOR, kR> la{blk(0, J), ld, (J + 1) * kR};
       block_update(blk(J + 1, J + 1), ld, la, la, true, false, smem);
       __threadfence();
-      diag64_coop(A, nb, (J + 1) * kR, p.status, s, iv);
+      diag64_reg(A, nb, (J + 1) * kR, p.status, &s[0][0]);
     } else {
       int t = 0;
       const int others = kPotrfCl - 1;
