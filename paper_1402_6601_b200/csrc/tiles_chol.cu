@@ -292,12 +292,18 @@ __device__ void diag64_reg(double* A, int ld, int j0, int* status, double* bufs)
     }
     __syncthreads();
     if (i > j) {
+      // one base register + immediate offsets, unconditional loads, selects: the
+      // upper part (k > i) of a[] is never read back, so only k > j matters
       const double li = colj[par * kR + i];
+      const double* cb = colj + par * kR + h;
+      const double* rb = rowx + par * kR + h;
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
-        const int k = 2 * m + h;
-        if (k > j && k <= i) a[m] = fma(-li, colj[par * kR + k], a[m]);
-        if (k <= j) r[m] = fma(-li, rowx[par * kR + k], r[m]);
+        const double cv = cb[2 * m], rv = rb[2 * m];
+        const bool up = (2 * m + h) > j;
+        const double am = fma(-li, cv, a[m]), rm = fma(-li, rv, r[m]);
+        a[m] = up ? am : a[m];
+        r[m] = up ? r[m] : rm;
       }
     }
     if (i == j + 1 && h == ((j + 1) & 1)) {
