@@ -54,73 +54,60 @@ __device__ __forceinline__ bool better(double v, int r, double bv, int br) {
   return v > bv || (v == bv && r < br);
 }
 
+// Register-resident panel: CTA q owns rows [q*R, (q+1)*R) of the panel; thread
+// t owns row lr = t % R and the NC columns c = g + NG*m (g = t / R, NG = 256/R).
+// Per column: 1 CTA barrier + 1 cluster barrier (local arg-max, candidate row
+// published over DSMEM), then 2 CTA barriers (pivot row staged, multipliers
+// published); the rank-1 update is NC independent register FMAs.
+template <int R, int SB>
 __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu_panel(LuPanelParams p) {
+  constexpr int NG = kLuThreads / R, NC = SB / NG;
   extern __shared__ double sm[];
   cg::cluster_group cl = cg::this_cluster();
   const int q = (int)cl.block_rank();
-  const int nb = p.nb, sb = p.sb, ii = p.ii, ib = p.ib;
-  const int R = nb / kLuCl;  // rows per CTA
+  const int nb = p.nb, ii = p.ii, ib = p.ib;
   const int row0 = q * R;
-  const int LD = R + 1;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lr = tid % R, grp = tid / R;
+  const int gr = row0 + lr;
   const bool ts = p.mode == LU_TSTRF;
-  double* s = sm;                                 // s[c*LD + r]: panel column c, local row r
-  double* cand = s + sb * LD;                     // [2][sb]  candidate (local arg-max) row
-  double* rowj = cand + 2 * kLuMaxSb;             // [2][sb]  GETRF: row j before the swap
-  double* urow = rowj + 2 * kLuMaxSb;             // [2][sb]  TSTRF: U row j (cols >= jj)
-  double* prow = urow + 2 * kLuMaxSb;             // [sb]     pivot row used for the update
-  double* slot_v = prow + kLuMaxSb;               // [2]
+  double* cand = sm;                   // [2][SB]
+  double* rowj = cand + 2 * SB;        // [2][SB]
+  double* urow = rowj + 2 * SB;        // [2][SB]
+  double* prow = urow + 2 * SB;        // [SB]
+  double* lv = prow + SB;              // [R]
+  double* slot_v = lv + R;             // [2]
   int* slot_r = reinterpret_cast<int*>(slot_v + 2);  // [2]
+  double* Ls = sm;                     // reused after the sweep: [SB][SB+1]
   __shared__ double red_v[kLuThreads / 32];
   __shared__ int red_r[kLuThreads / 32];
-  __shared__ int s_win_row, s_win_cta, s_swap;
-  __shared__ double s_piv;
   int* ipiv = reinterpret_cast<int*>(p.side + size_t(ib) * nb);
-  double* inv = p.side + size_t(ii) * ib;  // this panel's ib x sb block (ld = ib)
+  double* inv = p.side + size_t(ii) * ib;
   double* A = p.A;
+  const bool row_live = ts || gr >= ii;
 
-  // rows this CTA stages: GETRF touches rows >= ii only
-  for (int e = tid; e < sb * R; e += kLuThreads) {
-    int c = e / R, r = e % R;
-    int gr = row0 + r;
-    s[c * LD + r] = (ts || gr >= ii) ? A[size_t(ii + c) * nb + gr] : 0.0;
-  }
-  // dL (TSTRF) is written only for swapped rows: clear this panel's block first
-  // (ordered before any owner's write by the first cluster barrier)
+  double a[NC];
+#pragma unroll
+  for (int m = 0; m < NC; ++m) a[m] = row_live ? A[size_t(ii + grp + NG * m) * nb + gr] : 0.0;
   if (ts && q == 0)
-    for (int e = tid; e < ib * sb; e += kLuThreads) inv[e] = 0.0;
+    for (int e = tid; e < ib * SB; e += kLuThreads) inv[e] = 0.0;  // dL written only for swapped rows
   __syncthreads();
 
-  // Per column: 1 CTA barrier + 1 cluster barrier (phase A), 2 CTA barriers
-  // (phase B).  The scaled multiplier of column jj is written back to smem at
-  // the start of column jj+1 (before its first barrier), so the update never
-  // races with the read of the unscaled value.
-  const int ngroup = kLuThreads / R;
-  const int my_r = tid % R, my_grp = tid / R;
-  double pend_l = 0.0;
-  int pend_c = -1;
-  for (int jj = 0; jj < sb; ++jj) {
+  for (int jj = 0; jj < SB; ++jj) {
     const int j = ii + jj;
     const int par = jj & 1;
-    if (pend_c >= 0) {
-      s[pend_c * LD + my_r] = pend_l;
-      pend_c = -1;
-    }
-    // ---- phase A: local arg-max, publish candidate row --------------------
-    if (ts)  // U row j (columns >= jj): issued first so its latency hides behind the arg-max
-      for (int c = tid; c < sb; c += kLuThreads) urow[par * kLuMaxSb + c] = c >= jj ? p.U[size_t(ii + c) * nb + j] : 0.0;
+    const int gj = jj % NG, mj = jj / NG;
+    if (ts)
+      for (int c = tid; c < SB; c += kLuThreads) urow[par * SB + c] = c >= jj ? p.U[size_t(ii + c) * nb + j] : 0.0;
+    // ---- phase A: local arg-max over column jj -------------------------------
     double bv = -1.0;
     int br = 0x7fffffff;
-    for (int r = tid; r < R; r += kLuThreads) {
-      int gr = row0 + r;
-      bool active = ts ? true : (gr >= j);
-      if (active) {
-        double v = fabs(s[jj * LD + r]);
-        if (better(v, gr, bv, br)) {
-          bv = v;
-          br = gr;
-        }
-      }
+    if (grp == gj && (ts || gr >= j)) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < NC; ++m)
+        if (m == mj) v = a[m];
+      bv = fabs(v);
+      br = gr;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -149,14 +136,17 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
         slot_v[par] = v;
         slot_r[par] = r;
       }
-      const bool mine = r >= row0 && r < row0 + R;
-      for (int c = tid; c < sb; c += kLuThreads) {
-        cand[par * kLuMaxSb + c] = mine ? s[c * LD + (r - row0)] : 0.0;
-        if (!ts && j >= row0 && j < row0 + R) rowj[par * kLuMaxSb + c] = s[c * LD + (j - row0)];
+      if (gr == r) {
+#pragma unroll
+        for (int m = 0; m < NC; ++m) cand[par * SB + grp + NG * m] = a[m];
+      }
+      if (!ts && gr == j) {
+#pragma unroll
+        for (int m = 0; m < NC; ++m) rowj[par * SB + grp + NG * m] = a[m];
       }
     }
     cl.sync();
-    // ---- phase B: every warp resolves the global pivot itself ---------------
+    // ---- phase B: global pivot (every warp resolves it) ---------------------
     int wr, wc;
     bool swap;
     {
@@ -182,65 +172,77 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
       wr = __shfl_sync(0xffffffffu, r, 0);
       wc = __shfl_sync(0xffffffffu, who, 0);
       v = __shfl_sync(0xffffffffu, v, 0);
-      swap = ts ? (v > fabs(urow[par * kLuMaxSb + jj])) : (wr != j);
+      swap = ts ? (v > fabs(urow[par * SB + jj])) : (wr != j);
     }
-    const double* wcand = cl.map_shared_rank(cand, wc) + par * kLuMaxSb;
-    for (int c = tid; c < sb; c += kLuThreads) prow[c] = (ts && !swap) ? urow[par * kLuMaxSb + c] : wcand[c];
+    const double* wcand = cl.map_shared_rank(cand, wc) + par * SB;
+    for (int c = tid; c < SB; c += kLuThreads) prow[c] = (ts && !swap) ? urow[par * SB + c] : wcand[c];
     if (tid == 0 && q == 0) ipiv[j] = ts ? (swap ? wr : -1) : wr;
-    // swaps by the owners, straight from the published (pre-swap) buffers
-    if (ts) {
-      if (swap && wr >= row0 && wr < row0 + R) {
-        const int lr = wr - row0;
-        for (int c = tid; c < sb; c += kLuThreads) {
-          if (c < jj) {
-            inv[size_t(c) * ib + jj] = s[c * LD + lr];  // dL(jj, c), inverted at panel end
-            s[c * LD + lr] = 0.0;
-          } else {
-            p.U[size_t(ii + c) * nb + j] = wcand[c];
-            s[c * LD + lr] = urow[par * kLuMaxSb + c];
+    if (swap) {
+      if (ts) {
+        if (gr == wr) {
+#pragma unroll
+          for (int m = 0; m < NC; ++m) {
+            const int c = grp + NG * m;
+            if (c < jj) {
+              inv[size_t(c) * ib + jj] = a[m];  // dL(jj, c), inverted at the end
+              a[m] = 0.0;
+            } else {
+              p.U[size_t(ii + c) * nb + j] = wcand[c];
+              a[m] = urow[par * SB + c];
+            }
           }
         }
+      } else {
+        if (gr == wr) {  // row p <- old row j
+          const double* src = cl.map_shared_rank(rowj, j / R) + par * SB;
+#pragma unroll
+          for (int m = 0; m < NC; ++m) a[m] = src[grp + NG * m];
+        }
+        if (gr == j) {
+#pragma unroll
+          for (int m = 0; m < NC; ++m) a[m] = wcand[grp + NG * m];
+        }
       }
-    } else if (swap) {
-      if (wr >= row0 && wr < row0 + R) {  // row p <- old row j
-        const double* src = cl.map_shared_rank(rowj, j / R) + par * kLuMaxSb;
-        for (int c = tid; c < sb; c += kLuThreads) s[c * LD + (wr - row0)] = src[c];
-      }
-      if (j >= row0 && j < row0 + R)
-        for (int c = tid; c < sb; c += kLuThreads) s[c * LD + (j - row0)] = wcand[c];
     }
     __syncthreads();
     const double piv = prow[jj];
+    const bool act = ts || gr > j;
     if (piv == 0.0) {
       if (tid == 0 && q == 0 && p.status) atomicOr(p.status, 2);
-    } else {
-      const double rcp = 1.0 / piv;
-      const int gr = row0 + my_r;
-      if (my_grp < ngroup && (ts || gr > j)) {
-        const double l = s[jj * LD + my_r] * rcp;
-        for (int c = jj + 1 + my_grp; c < sb; c += ngroup) s[c * LD + my_r] = fma(-l, prow[c], s[c * LD + my_r]);
-        if (my_grp == 0) {
-          pend_l = l;
-          pend_c = jj;
-        }
-      }
+      continue;  // uniform across the cluster: nothing to eliminate
+    }
+    const double rcp = 1.0 / piv;
+    if (grp == gj && act) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < NC; ++m)
+        if (m == mj) v = a[m];
+      v *= rcp;
+#pragma unroll
+      for (int m = 0; m < NC; ++m)
+        if (m == mj) a[m] = v;
+      lv[lr] = v;
     }
     __syncthreads();
+    if (act) {
+      const double l = lv[lr];
+      const double* pb = prow + grp;
+#pragma unroll
+      for (int m = 0; m < NC; ++m) {
+        const double nv = fma(-l, pb[NG * m], a[m]);
+        a[m] = (grp + NG * m > jj) ? nv : a[m];
+      }
+    }
   }
-  if (pend_c >= 0) s[pend_c * LD + my_r] = pend_l;
-  __syncthreads();
-  cl.sync();
   // ---- write the panel back ----------------------------------------------------
-  for (int e = tid; e < sb * R; e += kLuThreads) {
-    int c = e / R, r = e % R;
-    int gr = row0 + r;
-    if (ts || gr >= ii) A[size_t(ii + c) * nb + gr] = s[c * LD + r];
+  if (row_live) {
+#pragma unroll
+    for (int m = 0; m < NC; ++m) A[size_t(ii + grp + NG * m) * nb + gr] = a[m];
   }
   __threadfence();
   cl.sync();
   // ---- inv(L_uu) into the side area (columns distributed over the cluster) ----
-  // L_uu(r, c), r > c: GETRF: tile rows [ii, ii+sb) of the panel; TSTRF: dL (side)
-  double* Ls = s;  // [sb][sb+1], Ls[c*(sb+1) + r]
+  const int sb = SB;
   const int LL = sb + 1;
   for (int e = tid; e < sb * sb; e += kLuThreads) {
     int c = e / sb, r = e % sb;
@@ -259,7 +261,11 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kLuThreads) k_lu
       x[m] = (i == c) ? 1.0 : 0.0;
     }
     for (int k = c; k < sb; ++k) {
-      double xk = __shfl_sync(0xffffffffu, x[k / 32], k % 32);
+      double xk = 0.0;
+#pragma unroll
+      for (int m = 0; m < kLuMaxSb / 32; ++m)
+        if (m == k / 32) xk = x[m];
+      xk = __shfl_sync(0xffffffffu, xk, k % 32);
 #pragma unroll
       for (int m = 0; m < kLuMaxSb / 32; ++m) {
         int i = lane + 32 * m;
@@ -414,11 +420,17 @@ static unsigned nn_smem() { return (unsigned)GemmSmem<CfgN, M_MAJOR, K_MAJOR>::B
 // ---------------------------------------------------------------------------
 static unsigned panel_smem(int nb, int sb) {
   const int R = nb / kLuCl;
-  size_t d = size_t(sb) * (R + 1);
+  size_t bufs = 7 * size_t(sb) + R + 4;
   size_t inv = size_t(sb) * (sb + 1);
-  if (inv > d) d = inv;
-  d += 7 * kLuMaxSb + 4;
-  return unsigned(d * sizeof(double));
+  return unsigned((bufs > inv ? bufs : inv) * sizeof(double));
+}
+
+static const void* panel_kernel(int nb, int ib) {
+  if (nb == 1024 && ib == 128) return (const void*)k_lu_panel<128, 128>;
+  if (nb == 1024 && ib == 64) return (const void*)k_lu_panel<128, 64>;
+  if (nb == 512 && ib == 128) return (const void*)k_lu_panel<64, 128>;
+  if (nb == 512 && ib == 64) return (const void*)k_lu_panel<64, 64>;
+  return nullptr;
 }
 
 template <int SB>
@@ -439,7 +451,10 @@ static unsigned apply_smem(int nb) {
   } while (0)
 
 bool init_lu_attributes() {
-  HG_ATTR(k_lu_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
+  HG_ATTR((k_lu_panel<128, 128>), cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
+  HG_ATTR((k_lu_panel<128, 64>), cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
+  HG_ATTR((k_lu_panel<64, 128>), cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
+  HG_ATTR((k_lu_panel<64, 64>), cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
   HG_ATTR(k_lu_apply<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem<128>(1024));
   HG_ATTR(k_lu_apply<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem<64>(1024));
   HG_ATTR(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, nn_smem());
@@ -477,8 +492,8 @@ static void push_panel_apply(std::vector<LaunchDesc>& out, int ib, const double*
 
 bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out) {
   const int nb = o.nb, ib = o.ib;
-  if (nb % 128 != 0 || nb > 1024 || (ib != 64 && ib != 128) || nb % ib != 0) {
-    set_error("LU tile kernels need nb %% 128 == 0, nb <= 1024 and ib in {64, 128}; got nb=%d ib=%d", nb, ib);
+  if ((nb != 512 && nb != 1024) || (ib != 64 && ib != 128)) {
+    set_error("LU tile kernels need nb in {512, 1024} and ib in {64, 128}; got nb=%d ib=%d", nb, ib);
     return false;
   }
   const size_t tile = size_t(nb) * nb;
@@ -493,7 +508,7 @@ bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
         LuPanelParams pp{A, ts ? o.t[0] : nullptr, ts ? side(1) : side(0), nb, ib, P * ib, ib,
                          ts ? LU_TSTRF : LU_GETRF, o.status};
         LaunchDesc d;
-        d.set((const void*)k_lu_panel, dim3(kLuCl), dim3(kLuThreads), panel_smem(nb, ib), pp);
+        d.set(panel_kernel(nb, ib), dim3(kLuCl), dim3(kLuThreads), panel_smem(nb, ib), pp);
         out.push_back(d);
         if (P + 1 < np)
           push_panel_apply(out, ib, A, ts ? side(1) : side(0), ts ? o.t[0] : A, A, nb, P, (P + 1) * ib,

@@ -118,20 +118,20 @@ int main() {
     printf("{\"bench\":\"dfma_peak\",\"blocks_per_sm\":%d,\"tflops\":%.3f,\"ms\":%.3f}\n", blocksPerSm, flops / (ms * 1e-3) / 1e12, ms);
   }
   using C64 = hg::GemmCfg<64, 64, 16, 32, 32, 3>;
-  using C64b32 = hg::GemmCfg<64, 64, 32, 32, 32, 3>;
-  using C64s4 = hg::GemmCfg<64, 64, 16, 32, 32, 4>;
-  using C64w2 = hg::GemmCfg<64, 64, 16, 32, 64, 3>;
-  using C128x64 = hg::GemmCfg<128, 64, 16, 32, 32, 3>;
-  using C128w16 = hg::GemmCfg<128, 128, 16, 32, 32, 3>;
+  using C64s2 = hg::GemmCfg<64, 64, 16, 32, 32, 2>;
+  using C64k8s4 = hg::GemmCfg<64, 64, 8, 32, 32, 4>;
+  using C64w8 = hg::GemmCfg<64, 64, 16, 32, 16, 3>;
+  using C64k32s2 = hg::GemmCfg<64, 64, 32, 32, 32, 2>;
   using C128x64w64 = hg::GemmCfg<128, 64, 16, 64, 32, 3>;
-  for (int batch : {1, 8, 32}) {
+  using C128x64w64s2 = hg::GemmCfg<128, 64, 16, 64, 32, 2>;
+  for (int batch : {1, 32}) {
     bench_cfg<C64>("64x64x16_w32x32_s3", 1024, batch);
-    bench_cfg<C64b32>("64x64x32_w32x32_s3", 1024, batch);
-    bench_cfg<C64s4>("64x64x16_w32x32_s4", 1024, batch);
-    bench_cfg<C64w2>("64x64x16_w32x64_s3", 1024, batch);
-    bench_cfg<C128x64>("128x64x16_w32x32_s3", 1024, batch);
-    bench_cfg<C128w16>("128x128x16_w32x32_s3", 1024, batch);
+    bench_cfg<C64s2>("64x64x16_w32x32_s2", 1024, batch);
+    bench_cfg<C64k8s4>("64x64x8_w32x32_s4", 1024, batch);
+    bench_cfg<C64w8>("64x64x16_w32x16_s3", 1024, batch);
+    bench_cfg<C64k32s2>("64x64x32_w32x32_s2", 1024, batch);
     bench_cfg<C128x64w64>("128x64x16_w64x32_s3", 1024, batch);
+    bench_cfg<C128x64w64s2>("128x64x16_w64x32_s2", 1024, batch);
   }
   return 0;
 }
