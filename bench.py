@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--ib", type=int, default=128)
     ap.add_argument("--alpha", type=float, default=0.5)
     ap.add_argument("--timings", default=None)
+    ap.add_argument("--priority-levels", type=int, default=6,
+                    help="CUDA node priority levels from task slack (0 = off); never changes the plan")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=16384, help="CPU baseline sample order")
@@ -298,9 +300,10 @@ def run_ours(args, rank, world, local):
 
     def make_exec(plan, host_in, host_out, device_input):
         if world == 1:
-            return runtime.Executor(g, plat, plan, host_in, host_out, devices=[local], device_input=device_input)
+            return runtime.Executor(g, plat, plan, host_in, host_out, devices=[local], device_input=device_input,
+                                    priority_levels=args.priority_levels)
         return runtime.DistributedExecutor(g, plat, plan, host_in, host_out, rank=rank, world=world, device=local,
-                                           device_input=device_input)
+                                           device_input=device_input, priority_levels=args.priority_levels)
 
     def max_over_ranks(x):
         if world == 1:
@@ -412,7 +415,8 @@ def run_ours(args, rank, world, local):
                                 else f"tiled {fam.upper()} N={n} nb={nb} ib={args.ib} FP64 (BASELINE configs[{2 if fam == 'lu' else 3}])"),
                    "family": fam,
                    "n": n, "nb": nb, "scheduler": f"DADA(alpha={args.alpha})+CP vs HEFT", "k": k,
-                   "cost_model": model_src, "l2": "inputs (tiles) > L2, no flush"},
+                   "cost_model": model_src, "l2": "inputs (tiles) > L2, no flush",
+                   "priority_levels": args.priority_levels},
         "nvlink_bytes": {"dada": d["bytes_d2d"], "heft": results["heft"]["bytes_d2d"]},
         "h2d_bytes": {"dada": d["bytes_h2d"], "heft": results["heft"]["bytes_h2d"]},
         "heft": {"value": results["heft"]["gflops"], "ms_per_step": results["heft"]["ms_per_step"],

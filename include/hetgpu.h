@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define HG_ABI_VERSION 1
+#define HG_ABI_VERSION 2
 
 /* error codes */
 #define HG_OK 0
@@ -174,6 +174,13 @@ typedef struct hg_exec_opts {
                                  devices).  r+1: one process per GPU -- this process executes
                                  node r+1 only; exchange pools with hg_exec_ipc_handle /
                                  hg_exec_ipc_open, then hg_exec_build */
+  const double* task_weight;  /* optional [n_tasks] predicted seconds per task (the plan's
+                                 end - start); NULL = no node priorities */
+  int32_t priority_levels;    /* >0: kernel nodes get CUDA priorities from the task's slack
+                                 (longest path through it vs the DAG's critical path, weights
+                                 task_weight) quantised to min(levels, device range) levels;
+                                 0 = every node at default priority.  Never changes the plan,
+                                 only the order in which ready kernels get SMs. */
 } hg_exec_opts;
 
 typedef struct hg_exec hg_exec;

@@ -71,7 +71,8 @@ class ExecPlan(C.Structure):
 
 class ExecOpts(C.Structure):
     _fields_ = [("devices", _i32p), ("host_in", _f64p), ("host_out", _f64p), ("host_side_out", _f64p),
-                ("device_input", C.c_int32), ("rank_node", C.c_int32)]
+                ("device_input", C.c_int32), ("rank_node", C.c_int32),
+                ("task_weight", _f64p), ("priority_levels", C.c_int32)]
 
 
 class ExecStats(C.Structure):

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -224,6 +225,8 @@ struct hg_exec {
   double* host_out = nullptr;
   double* host_side_out = nullptr;
   int device_input = 0;
+  std::vector<double> task_weight;     // predicted seconds per task (node priorities)
+  int priority_levels = 0;
   // memory
   std::vector<int> dev;                 // node g+1 -> device
   std::vector<double*> base;            // per node: pool base (local allocation or IPC mapping)
@@ -369,6 +372,51 @@ static int add_flag_kernel(cudaGraph_t g, cudaGraphNode_t* out, const cudaGraphN
   return HG_OK;
 }
 
+// CUDA priority of each task's kernel nodes from its slack: the longest path
+// through the task (top level + bottom level, weights = predicted durations)
+// against the DAG's critical path.  Zero-slack tasks (the POTRF / panel chain
+// and what feeds it) get the device's greatest priority; ready work with slack
+// fills the SMs behind them.  Task ids are a topological order (every DAG edge
+// goes from a lower to a higher id, graph.py:58-84).
+static std::vector<int> task_priorities(const hg_exec* ex, int dev) {
+  const int n = ex->n_tasks;
+  std::vector<int> prio(n, 0);
+  if (ex->priority_levels <= 0 || (int)ex->task_weight.size() != n) return prio;
+  int least = 0, greatest = 0;
+  if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) {
+    cudaGetLastError();
+    return prio;
+  }
+  const int range = least - greatest + 1;  // greatest is numerically smallest
+  const int levels = std::min(ex->priority_levels, range);
+  if (levels <= 1) return prio;
+  (void)dev;
+  std::vector<double> top(n, 0.0), bot(n, 0.0);
+  for (int t = 0; t < n; ++t)
+    for (int64_t q = ex->pred_ptr[t]; q < ex->pred_ptr[t + 1]; ++q) {
+      const int u = ex->pred[q];
+      top[t] = std::max(top[t], top[u] + ex->task_weight[u]);
+    }
+  for (int t = n - 1; t >= 0; --t) {
+    bot[t] += ex->task_weight[t];
+    for (int64_t q = ex->pred_ptr[t]; q < ex->pred_ptr[t + 1]; ++q) {
+      const int u = ex->pred[q];
+      bot[u] = std::max(bot[u], bot[t]);
+    }
+  }
+  double cp = 0.0;
+  for (int t = 0; t < n; ++t) cp = std::max(cp, top[t] + bot[t]);
+  if (!(cp > 0.0)) return prio;
+  // level 0 (most urgent) for slack < cp / (2 levels), then bands of the same width
+  const double band = cp / (2.0 * levels);
+  for (int t = 0; t < n; ++t) {
+    const double slack = std::max(0.0, cp - top[t] - bot[t]);
+    const int lvl = std::min(levels - 1, int(slack / band));
+    prio[t] = greatest + lvl;
+  }
+  return prio;
+}
+
 static int build_graph(hg_exec* ex) {
   const int n = ex->n_tasks;
   const Partition part = partition(ex);
@@ -383,6 +431,12 @@ static int build_graph(hg_exec* ex) {
   int64_t side_bytes = 0;
   std::vector<int64_t> scratch_used(ex->k, 0);
   hg_exec_stats& st = ex->stats;
+  {
+    const int first = ex->rank_node ? ex->rank_node : 1;
+    HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
+  }
+  const std::vector<int> prio = task_priorities(ex, 0);
+  const bool use_prio = ex->priority_levels > 0 && !ex->task_weight.empty();
 
   // dependency on the producer of a task output / job delivery for a consumer on cons_node
   auto dep_task = [&](int u, int cons_node) -> int {
@@ -505,6 +559,11 @@ static int build_graph(hg_exec* ex) {
       cudaGraphNode_t nd;
       if (li == 0) HG_CUDA(cudaGraphAddKernelNode(&nd, ex->graph, deps.data(), deps.size(), &kp));
       else HG_CUDA(cudaGraphAddKernelNode(&nd, ex->graph, &prev, 1, &kp));
+      if (use_prio) {
+        cudaKernelNodeAttrValue v{};
+        v.priority = prio[t];
+        HG_CUDA(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributePriority, &v));
+      }
       prev = nd;
       st.n_kernel_nodes++;
     }
@@ -542,7 +601,7 @@ static int build_graph(hg_exec* ex) {
   st.bytes_side = side_bytes;
   int first = ex->rank_node ? ex->rank_node : 1;
   HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
-  HG_CUDA(cudaGraphInstantiate(&ex->exec, ex->graph, 0));
+  HG_CUDA(cudaGraphInstantiate(&ex->exec, ex->graph, use_prio ? cudaGraphInstantiateFlagUseNodePriority : 0));
   ex->built = true;
   return HG_OK;
 }
@@ -596,6 +655,8 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
   ex->host_out = O->host_out;
   ex->host_side_out = O->host_side_out;
   ex->device_input = O->device_input;
+  ex->task_weight = vcopy(O->task_weight, n);
+  ex->priority_levels = O->task_weight ? O->priority_levels : 0;
   ex->dev.assign(O->devices, O->devices + P->k);
   ex->base.assign(P->k, nullptr);
   ex->ipc.assign(P->k, 0);

@@ -28,6 +28,7 @@
 // (GETRF: absolute row swapped with row j; TSTRF: A row swapped with U row j,
 // or -1).
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "dgemm_dmma.cuh"
 #include "tiles.h"
@@ -418,6 +419,634 @@ __global__ void __launch_bounds__(CfgN::THREADS) k_gemm_nn(GemmNNParams p) {
 static unsigned nn_smem() { return (unsigned)GemmSmem<CfgN, M_MAJOR, K_MAJOR>::BYTES; }
 
 // ---------------------------------------------------------------------------
+// k_lu_apply_cl -- applies panels [p0, p1) of an LU factor to a column strip
+// with the bottom rows split over a 4-CTA cluster (CTA q owns tile rows
+// [q*nb/4, (q+1)*nb/4) of bot and 8 of the strip's 32 columns for the row
+// interchanges), so one GESSM / SSSSM spreads over (N/32) x 4 SMs.  Per panel:
+//   0. every CTA turns the panel's ipiv into a list of row moves (dst <- src,
+//      values as they were before the panel; see lu_moves below);
+//   1. CTA q performs the moves of its 8 columns; cluster barrier;
+//   2. every CTA loads the 128 top rows, forms its 32-row slice of
+//      top' = inv(L_uu) top; cluster barrier;
+//   3. every CTA gathers top' over DSMEM, CTA q stores its slice, and
+//      bot[rows_q] -= L_a[rows_q] top' on the DMMA engine; cluster barrier.
+constexpr int kLcCl = 4;
+constexpr int kLcBN = 32;
+constexpr int kLcLd = kLuMaxSb + 4;             // smem [col][row] buffers
+constexpr int kLcMaxMoves = 2 * kLuMaxSb;
+using CfgLC = GemmCfg<128, kLcBN, 16, 32, 16, 3>;  // 8 warps
+
+// Row moves of one panel (values before the panel -> positions after it).
+// GETRF (rows of one tile): step j swaps rows j and p_j >= j.  Positions < j
+// are final after step j, so with V(j) = the row pushed out of j at step j
+//   V(j)            = V(j'') for the last j'' < j with p_j'' == j, else j
+//   final row j     = V(j') for the last j' < j with p_j' == p_j, else p_j
+//   final row x     = V(j') for the last j' with p_j' == x     (x >= ii+sb)
+// TSTRF (top slot jj <-> bot row r_jj, or -1): with jp the last earlier step
+// that swapped the same bot row,
+//   final top jj    = T(jp) if jp exists else B(r_jj)
+//   final bot r     = T(jj) for the last jj that swapped r.
+// Encoding: bot rows >= 0, top slots -1-jj.  Returns the move count.
+__device__ int lu_moves(const int* steps, int ii, int sb, bool ts, int* sp, int* mv_dst, int* mv_src,
+                        int* cnt) {
+  // steps[j]: pivot of step j (GETRF: absolute row p_j; TSTRF: bot row or -1);
+  // ii: tile row of step 0 (GETRF)
+  const int tid = threadIdx.x;
+  if (tid == 0) *cnt = 0;
+  for (int j = tid; j < sb; j += blockDim.x) sp[j] = steps[j];
+  __syncthreads();
+  if (ts) {
+    for (int j = tid; j < sb; j += blockDim.x) {
+      const int r = sp[j];
+      if (r < 0) continue;
+      int jp = -1;
+      for (int k = 0; k < j; ++k) jp = (sp[k] == r) ? k : jp;
+      bool last = true;
+      for (int k = j + 1; k < sb; ++k) last = last && (sp[k] != r);
+      int n = atomicAdd(cnt, last ? 2 : 1);
+      mv_dst[n] = -1 - j;
+      mv_src[n] = jp >= 0 ? -1 - jp : r;
+      if (last) {
+        mv_dst[n + 1] = r;
+        mv_src[n + 1] = -1 - j;
+      }
+    }
+  } else {
+    // pred[j]: last earlier step whose target is row j (panel rows only)
+    int* pred = sp + sb;
+    int* V = pred + sb;
+    for (int j = tid; j < sb; j += blockDim.x) {
+      int pr = -1;
+      for (int k = 0; k < j; ++k) pr = (sp[k] == ii + j) ? k : pr;
+      pred[j] = pr;
+    }
+    __syncthreads();
+    for (int j = tid; j < sb; j += blockDim.x) {
+      int k = j;
+      while (pred[k] >= 0) k = pred[k];
+      V[j] = ii + k;
+    }
+    __syncthreads();
+    for (int j = tid; j < sb; j += blockDim.x) {
+      const int pj = sp[j];
+      int jl = -1;
+      for (int k = 0; k < j; ++k) jl = (sp[k] == pj) ? k : jl;
+      const int src = (pj == ii + j) ? V[j] : (jl >= 0 ? V[jl] : pj);
+      if (src != ii + j) {
+        int n = atomicAdd(cnt, 1);
+        mv_dst[n] = ii + j;
+        mv_src[n] = src;
+      }
+      if (pj >= ii + sb) {  // rows below the panel: the last step targeting them moves V into them
+        bool last = true;
+        for (int k = j + 1; k < sb; ++k) last = last && (sp[k] != pj);
+        if (last) {
+          int n = atomicAdd(cnt, 1);
+          mv_dst[n] = pj;
+          mv_src[n] = V[j];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return *cnt;
+}
+
+__global__ void __cluster_dims__(kLcCl, 1, 1) __launch_bounds__(CfgLC::THREADS) k_lu_apply_cl(LuApplyParams p) {
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  constexpr int RING = GemmSmem<CfgLC, M_MAJOR, K_MAJOR>::DOUBLES;
+  constexpr int WBUF = kLcBN * kLcLd;
+  double* ring = sm;
+  double* Wp = sm + RING;            // [2][WBUF] top' slices by panel parity
+  double* Ts = Wp + 2 * WBUF;        // top rows after the moves, then gathered top'
+  double* mvv = Ts + WBUF;           // [kLcMaxMoves][8] moved values
+  int* mv_dst = reinterpret_cast<int*>(mvv + kLcMaxMoves * 8);
+  int* mv_src = mv_dst + kLcMaxMoves;
+  int* sp = mv_src + kLcMaxMoves;    // [3 * sb]
+  __shared__ int n_moves;
+  const int nb = p.nb, ib = p.ib, sb = ib;
+  const int n0 = p.col0 + (blockIdx.x / kLcCl) * kLcBN;
+  const int rows = nb / kLcCl;
+  const int r_begin = q * rows, r_end = r_begin + rows;
+  const bool ts = p.mode == LU_TSTRF;
+  const int tid = threadIdx.x;
+  const int* ipiv = reinterpret_cast<const int*>(p.side + size_t(ib) * nb);
+  double* top = p.top;
+  double* bot = ts ? p.bot : p.top;
+  for (int P = p.p0; P < p.p1; ++P) {
+    const int ii = P * ib;
+    double* wp = Wp + (P & 1) * WBUF;
+    // ---- 0/1. row moves of my 8 columns ------------------------------------------
+    const int nm = lu_moves(ipiv + ii, ii, sb, ts, sp, mv_dst, mv_src, &n_moves);
+    const int c8 = n0 + q * 8;
+    auto at = [&](int code, int c) -> double* {
+      return code >= 0 ? bot + size_t(c) * nb + code : top + size_t(c) * nb + ii + (-1 - code);
+    };
+    for (int e = tid; e < nm * 8; e += CfgLC::THREADS) {
+      const int m = e >> 3, c = c8 + (e & 7);
+      mvv[e] = __ldcg(at(mv_src[m], c));
+    }
+    __syncthreads();
+    for (int e = tid; e < nm * 8; e += CfgLC::THREADS) {
+      const int m = e >> 3, c = c8 + (e & 7);
+      *at(mv_dst[m], c) = mvv[e];
+    }
+    cl.sync();
+    // ---- 2. top rows -> smem, my slice of top' = inv(L_uu) top ---------------------
+    for (int e = tid; e < sb * kLcBN; e += CfgLC::THREADS) {
+      const int c = e / sb, r = e % sb;
+      Ts[c * kLcLd + r] = __ldcg(top + size_t(n0 + c) * nb + ii + r);
+    }
+    __syncthreads();
+    {
+      const double* inv = p.side + size_t(ii) * ib;  // inv(r, k) at inv[k*ib + r], unit lower
+      constexpr int SL = kLuMaxSb / kLcCl;
+      const int s0 = q * SL;
+      for (int e = tid; e < SL * kLcBN; e += CfgLC::THREADS) {
+        const int c = e / SL, r = s0 + e % SL;
+        const double* tc = Ts + c * kLcLd;
+        double a0 = tc[r], a1 = 0.0;
+        int k = 0;
+        for (; k + 1 < r; k += 2) {
+          a0 = fma(__ldg(inv + size_t(k) * ib + r), tc[k], a0);
+          a1 = fma(__ldg(inv + size_t(k + 1) * ib + r), tc[k + 1], a1);
+        }
+        if (k < r) a0 = fma(__ldg(inv + size_t(k) * ib + r), tc[k], a0);
+        wp[c * kLcLd + r] = a0 + a1;
+      }
+    }
+    cl.sync();
+    // ---- 3. gather top', store my slice, bot[rows] -= L_a top' ----------------------
+    {
+      constexpr int SL = kLuMaxSb / kLcCl;
+      for (int c2 = 0; c2 < kLcCl; ++c2) {
+        const double* src = cl.map_shared_rank(wp, c2);
+        for (int e = tid; e < SL * kLcBN; e += CfgLC::THREADS) {
+          const int c = e / SL, r = c2 * SL + e % SL;
+          const double v = src[c * kLcLd + r];
+          Ts[c * kLcLd + r] = v;
+          if (c2 == q) top[size_t(n0 + c) * nb + ii + r] = v;
+        }
+      }
+    }
+    __syncthreads();
+    if (!p.swap_only) {
+      const int m_lo = ts ? r_begin : max(r_begin, ii + sb);
+      for (int m0 = m_lo; m0 < r_end; m0 += 128) {
+        double acc[CfgLC::FM][CfgLC::FN][2];
+        zero_acc<CfgLC>(acc);
+        TileLoader<CfgLC, M_MAJOR, 128> la{p.L + size_t(ii) * nb, nb, m0};
+        gemm_mainloop_bsmem<CfgLC>(acc, ring, la, Ts, kLcLd, 0, sb);
+        sub_store<CfgLC>(acc, bot, nb, m0, n0);
+      }
+    }
+    cl.sync();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_lu_panel_sp -- one ib-wide panel factorisation (the GETRF / TSTRF
+// semantics of k_lu_panel) blocked into W = 16-column sub-panels, so the
+// per-column critical path only touches 16 registers per row:
+//   * the 8-CTA cluster keeps the panel rows in shared memory (CTA q owns
+//     rows [q*R, (q+1)*R), one row per thread);
+//   * per column: local arg-max -> ONE cluster barrier -> every thread reads
+//     the 8 candidates and the winner's 16 sub-panel values over DSMEM, swaps
+//     and eliminates inside its registers (no further barrier);
+//   * per sub-panel: the 16 row interchanges are applied to the panel columns
+//     outside the sub-panel as one composed move list (lu_moves) over DSMEM;
+//     TSTRF moves the swapped rows' earlier multipliers to dL; then the
+//     right-hand columns get U12 = L11^-1 A12 (owner of the 16 pivot rows /
+//     CTA 0 for TSTRF) and A22 -= L21 U12 (every row, registers x broadcast).
+// Same outputs as k_lu_panel (ipiv, dL, panel values, inv(L_uu) in the side area).
+constexpr int kSpW = 16;
+constexpr int kSpThreads = 128;
+constexpr int kSpSB = kLuMaxSb;
+
+template <int R>
+struct SpSmem {
+  static constexpr int LDP = R + 1;
+  static constexpr int PS = kSpSB * LDP;                  // panel [col][row]
+  static constexpr int STG = 2 * kSpW * kSpSB;            // phase-S staging rows
+  static constexpr int U12 = kSpW * kSpSB;                // [v][col]
+  static constexpr int MISC = 4 * kSpW + 4 + kSpW * kSpW; // cand, rowj, slots, Ublk
+  static constexpr int DOUBLES = PS + STG + U12 + MISC;
+  static constexpr int INTS = kSpSB + 4 * kSpW + 3 * kSpW + 4;
+  static constexpr size_t BYTES = size_t(DOUBLES) * 8 + size_t(INTS) * 4;
+};
+
+template <int R>
+__global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu_panel_sp(LuPanelParams p) {
+  constexpr int W = kSpW, SB = kSpSB;
+  using S = SpSmem<R>;
+  constexpr int LDP = S::LDP;
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const int nb = p.nb, ii = p.ii, ib = p.ib;
+  const int row0 = q * R;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool ts = p.mode == LU_TSTRF;
+  const bool mine = tid < R;
+  const int gr = row0 + tid;
+  const bool live = mine && (ts || gr >= ii);
+  double* Ps = sm;
+  double* stg = Ps + S::PS;
+  double* U12 = stg + S::STG;
+  double* cand = U12 + S::U12;          // [2][W]
+  double* rowj = cand + 2 * W;          // [2][W]
+  double* slot_v = rowj + 2 * W;        // [2] (+2 pad)
+  double* Ublk = slot_v + 4;            // [W][W]
+  int* swp = reinterpret_cast<int*>(sm + S::DOUBLES);  // [SB]
+  int* mvd = swp + SB;                  // [2W]
+  int* mvs = mvd + 2 * W;               // [2W]
+  int* sp = mvs + 2 * W;                // [3W]
+  int* slot_r = sp + 3 * W;             // [2]
+  __shared__ double red_v[kSpThreads / 32];
+  __shared__ int red_r[kSpThreads / 32];
+  __shared__ int n_mv;
+  int* ipiv = reinterpret_cast<int*>(p.side + size_t(ib) * nb);
+  double* inv = p.side + size_t(ii) * ib;  // dL(jj, c) at inv[c*ib + jj]
+  double* A = p.A;
+
+  for (int e = tid; e < SB * R; e += kSpThreads) {
+    const int c = e / R, r = e % R;
+    Ps[c * LDP + r] = (ts || row0 + r >= ii) ? A[size_t(ii + c) * nb + row0 + r] : 0.0;
+  }
+  if (ts && q == 0)
+    for (int e = tid; e < ib * SB; e += kSpThreads) inv[e] = 0.0;
+  __threadfence();
+  cl.sync();
+
+  for (int c0 = 0; c0 < SB; c0 += W) {
+    if (ts)
+      for (int e = tid; e < W * W; e += kSpThreads) {
+        const int u = e / W, v = e % W;
+        Ublk[e] = v >= u ? __ldcg(p.U + size_t(ii + c0 + v) * nb + ii + c0 + u) : 0.0;
+      }
+    double a[W];
+#pragma unroll
+    for (int v = 0; v < W; ++v) a[v] = mine ? Ps[(c0 + v) * LDP + tid] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      const int jj = c0 + u, j = ii + jj, par = jj & 1;
+      // ---- A: local arg-max, publish candidate row (+ row j for GETRF) -------------
+      double bv = -1.0;
+      int br = 0x7fffffff;
+      if (live && (ts || gr >= j)) {
+        bv = fabs(a[u]);
+        br = gr;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+        if (better(ov, orr, bv, br)) {
+          bv = ov;
+          br = orr;
+        }
+      }
+      if (lane == 0) {
+        red_v[warp] = bv;
+        red_r[warp] = br;
+      }
+      __syncthreads();
+      {
+        double v = red_v[0];
+        int r = red_r[0];
+#pragma unroll
+        for (int w = 1; w < kSpThreads / 32; ++w)
+          if (better(red_v[w], red_r[w], v, r)) {
+            v = red_v[w];
+            r = red_r[w];
+          }
+        if (tid == 0) {
+          slot_v[par] = v;
+          slot_r[par] = r;
+        }
+        if (mine && gr == r) {
+#pragma unroll
+          for (int v2 = 0; v2 < W; ++v2) cand[par * W + v2] = a[v2];
+        }
+        if (!ts && mine && gr == j) {
+#pragma unroll
+          for (int v2 = 0; v2 < W; ++v2) rowj[par * W + v2] = a[v2];
+        }
+      }
+      cl.sync();
+      // ---- B: global pivot, pivot row, interchange ---------------------------------
+      int wr, wc;
+      double wv;
+      {
+        double v = -1.0;
+        int r = 0x7fffffff, who = 0;
+        if (lane < kLuCl) {
+          v = cl.map_shared_rank(slot_v, lane)[par];
+          r = cl.map_shared_rank(slot_r, lane)[par];
+          who = lane;
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+          const int orr = __shfl_xor_sync(0xffffffffu, r, o);
+          const int ow = __shfl_xor_sync(0xffffffffu, who, o);
+          if (better(ov, orr, v, r)) {
+            v = ov;
+            r = orr;
+            who = ow;
+          }
+        }
+        wr = __shfl_sync(0xffffffffu, r, 0);
+        wc = __shfl_sync(0xffffffffu, who, 0);
+        wv = __shfl_sync(0xffffffffu, v, 0);
+      }
+      const bool swap = ts ? (wv > fabs(Ublk[u * W + u])) : (wr != j);
+      const bool from_cand = !ts || swap;
+      const double* cw = cl.map_shared_rank(cand, wc) + par * W;
+      double prow[W];
+#pragma unroll
+      for (int v2 = 0; v2 < W; ++v2) prow[v2] = 0.0;
+#pragma unroll
+      for (int v2 = u; v2 < W; ++v2) prow[v2] = from_cand ? cw[v2] : Ublk[u * W + v2];
+      if (tid == 0) swp[jj] = ts ? (swap ? wr : -1) : wr;
+      if (q == 0 && tid == 0) ipiv[j] = ts ? (swap ? wr : -1) : wr;
+      if (swap) {
+        if (ts) {
+          if (mine && gr == wr) {
+#pragma unroll
+            for (int v2 = 0; v2 < W; ++v2) {
+              if (v2 < u) {
+                inv[size_t(c0 + v2) * ib + jj] = a[v2];  // dL(jj, c0 + v2)
+                a[v2] = 0.0;
+              } else {
+                a[v2] = Ublk[u * W + v2];
+              }
+            }
+          }
+          if (q == 0 && tid >= u && tid < W) p.U[size_t(ii + c0 + tid) * nb + j] = cw[tid];
+        } else {
+          if (mine && gr == wr) {
+            const double* rj = cl.map_shared_rank(rowj, j / R) + par * W;
+#pragma unroll
+            for (int v2 = 0; v2 < W; ++v2) a[v2] = rj[v2];
+          }
+          if (mine && gr == j) {
+#pragma unroll
+            for (int v2 = 0; v2 < W; ++v2) a[v2] = cw[v2];
+          }
+        }
+      }
+      // ---- C: scale and eliminate inside the sub-panel -----------------------------
+      const double piv = prow[u];
+      if (piv == 0.0) {
+        if (tid == 0 && q == 0 && p.status) atomicOr(p.status, 2);
+        continue;
+      }
+      const double rcp = 1.0 / piv;
+      if (live && (ts || gr > j)) {
+        const double l = a[u] * rcp;
+        a[u] = l;
+#pragma unroll
+        for (int v2 = u + 1; v2 < W; ++v2) a[v2] = fma(-l, prow[v2], a[v2]);
+      }
+    }
+    if (mine) {
+#pragma unroll
+      for (int v = 0; v < W; ++v) Ps[(c0 + v) * LDP + tid] = a[v];
+    }
+    __syncthreads();
+    // ---- S: the sub-panel's interchanges on the columns outside it ----------------------
+    const int cR = c0 + W;  // first right-hand column
+    if (ts) {
+      // (i) a swapped A row's multipliers left of the sub-panel move to dL(jj, .) (first swap only)
+      for (int u = 0; u < W; ++u) {
+        const int r = swp[c0 + u];
+        if (r < row0 || r >= row0 + R) continue;
+        bool first = true;
+        for (int u2 = 0; u2 < u; ++u2) first = first && (swp[c0 + u2] != r);
+        if (!first) continue;
+        for (int c = tid; c < c0; c += kSpThreads) {
+          inv[size_t(c) * ib + c0 + u] = Ps[c * LDP + (r - row0)];
+          Ps[c * LDP + (r - row0)] = 0.0;
+        }
+      }
+    }
+    const int nm = lu_moves(swp + c0, ii + c0, W, ts, sp, mvd, mvs, &n_mv);
+    // read phase: sources of the moves whose destination I write
+    //   GETRF: dst rows in my range, columns outside the sub-panel
+    //   TSTRF: dst A rows in my range (src: U rows, global); CTA 0 also the dst U rows
+    const int ncol_out = SB - W;
+    auto out_col = [&](int k) { return k < c0 ? k : k + W; };
+    for (int m = 0; m < nm; ++m) {
+      const int d = mvd[m], sidx = mvs[m];
+      const bool d_top = d < 0;
+      const bool writer = d_top ? (q == 0) : (d >= row0 && d < row0 + R);
+      if (!writer) continue;
+      if (!ts) {
+        const double* src = cl.map_shared_rank(Ps, sidx / R) + (sidx % R);
+        for (int k = tid; k < ncol_out; k += kSpThreads) stg[m * SB + k] = src[out_col(k) * LDP];
+      } else {
+        for (int c = cR + tid; c < SB; c += kSpThreads) {
+          double v;
+          if (sidx < 0) v = __ldcg(p.U + size_t(ii + c) * nb + ii + c0 + (-1 - sidx));
+          else v = cl.map_shared_rank(Ps, sidx / R)[c * LDP + (sidx % R)];
+          stg[m * SB + c] = v;
+        }
+      }
+    }
+    cl.sync();
+    for (int m = 0; m < nm; ++m) {
+      const int d = mvd[m];
+      const bool d_top = d < 0;
+      const bool writer = d_top ? (q == 0) : (d >= row0 && d < row0 + R);
+      if (!writer) continue;
+      if (!ts) {
+        for (int k = tid; k < ncol_out; k += kSpThreads) Ps[out_col(k) * LDP + (d - row0)] = stg[m * SB + k];
+      } else if (d_top) {
+        for (int c = cR + tid; c < SB; c += kSpThreads) p.U[size_t(ii + c) * nb + ii + c0 + (-1 - d)] = stg[m * SB + c];
+      } else {
+        for (int c = cR + tid; c < SB; c += kSpThreads) Ps[c * LDP + (d - row0)] = stg[m * SB + c];
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (cR >= SB) break;
+    // ---- U: right-hand columns: U12 = L11^-1 A12, A22 -= L21 U12 --------------------------
+    const int nR = SB - cR;
+    const int owner = ts ? 0 : (ii + c0) / R;
+    cl.sync();  // moved rows / U rows visible everywhere
+    if (q == owner) {
+      // forward substitution, one thread per right-hand column
+      for (int c = tid; c < nR; c += kSpThreads) {
+        double x[W];
+#pragma unroll
+        for (int v = 0; v < W; ++v) {
+          double t = ts ? __ldcg(p.U + size_t(ii + cR + c) * nb + ii + c0 + v)
+                        : Ps[(cR + c) * LDP + (ii + c0 + v - row0)];
+#pragma unroll
+          for (int w = 0; w < v; ++w) {
+            const double l = ts ? __ldcg(inv + size_t(c0 + w) * ib + c0 + v) : Ps[(c0 + w) * LDP + (ii + c0 + v - row0)];
+            t = fma(-l, x[w], t);
+          }
+          x[v] = t;
+          U12[v * SB + c] = t;
+          if (ts) p.U[size_t(ii + cR + c) * nb + ii + c0 + v] = t;
+          else Ps[(cR + c) * LDP + (ii + c0 + v - row0)] = t;
+        }
+      }
+    }
+    cl.sync();
+    if (q != owner) {
+      const double* src = cl.map_shared_rank(U12, owner);
+      for (int e = tid; e < W * nR; e += kSpThreads) {
+        const int v = e / nR, c = e % nR;
+        U12[v * SB + c] = src[v * SB + c];
+      }
+    }
+    __syncthreads();
+    if (live && (ts || gr >= ii + cR)) {
+      for (int c = 0; c < nR; ++c) {
+        double t = Ps[(cR + c) * LDP + tid];
+#pragma unroll
+        for (int v = 0; v < W; ++v) t = fma(-a[v], U12[v * SB + c], t);
+        Ps[(cR + c) * LDP + tid] = t;
+      }
+    }
+    cl.sync();  // U12 of the owner is not overwritten before every CTA copied it
+  }
+  // ---- write the panel back ------------------------------------------------------------
+  for (int e = tid; e < SB * R; e += kSpThreads) {
+    const int c = e / R, r = e % R;
+    if (ts || row0 + r >= ii) A[size_t(ii + c) * nb + row0 + r] = Ps[c * LDP + r];
+  }
+  __threadfence();
+  cl.sync();
+  // ---- inv(L_uu) into the side area (columns distributed over the cluster) ---------------
+  const int sb = SB;
+  const int LL = sb + 1;
+  double* Ls = sm;
+  for (int e = tid; e < sb * sb; e += kSpThreads) {
+    const int c = e / sb, r = e % sb;
+    double v = 0.0;
+    if (r > c) v = ts ? __ldcg(inv + size_t(c) * ib + r) : __ldcg(A + size_t(ii + c) * nb + ii + r);
+    Ls[c * LL + r] = v;
+  }
+  __syncthreads();
+  cl.sync();  // every CTA has its copy of dL before anyone overwrites it
+  for (int c = q * (kSpThreads / 32) + warp; c < sb; c += kLuCl * (kSpThreads / 32)) {
+    double x[kLuMaxSb / 32];
+#pragma unroll
+    for (int m = 0; m < kLuMaxSb / 32; ++m) x[m] = (lane + 32 * m == c) ? 1.0 : 0.0;
+    for (int k = c; k < sb; ++k) {
+      double xk = 0.0;
+#pragma unroll
+      for (int m = 0; m < kLuMaxSb / 32; ++m)
+        if (m == k / 32) xk = x[m];
+      xk = __shfl_sync(0xffffffffu, xk, k % 32);
+#pragma unroll
+      for (int m = 0; m < kLuMaxSb / 32; ++m) {
+        const int i = lane + 32 * m;
+        if (i > k) x[m] = fma(-Ls[k * LL + i], xk, x[m]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kLuMaxSb / 32; ++m) inv[size_t(c) * ib + lane + 32 * m] = x[m];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_lu_apply_strip -- the same panel application without a cluster: one CTA
+// per BN-column strip owns every row of it (columns are independent), so the
+// interchanges, top' = inv(L_uu) top (DMMA) and bot -= L_a top' (DMMA) need
+// only CTA barriers.  Small shared-memory footprint (2 CTAs / SM), so it
+// co-schedules with the other tile kernels of the DAG.
+template <class G>
+__global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) {
+  constexpr int BN = G::BN;
+  constexpr int RING = GemmSmem<G, M_MAJOR, K_MAJOR>::DOUBLES;
+  static_assert(RING >= kLcMaxMoves * BN, "move staging aliases the ring");
+  extern __shared__ double sm[];
+  double* ring = sm;
+  double* mvv = sm;                       // interchange staging (ring is idle then)
+  double* Ts = sm + RING;                 // [BN][kLcLd] top rows after the moves
+  double* Wt = Ts + BN * kLcLd;           // [BN][kLcLd] top'
+  int* mv_dst = reinterpret_cast<int*>(Wt + BN * kLcLd);
+  int* mv_src = mv_dst + kLcMaxMoves;
+  int* sp = mv_src + kLcMaxMoves;         // [3 * sb]
+  __shared__ int n_moves;
+  const int nb = p.nb, ib = p.ib, sb = ib;
+  const int n0 = p.col0 + blockIdx.x * BN;
+  const bool ts = p.mode == LU_TSTRF;
+  const int tid = threadIdx.x;
+  const int* ipiv = reinterpret_cast<const int*>(p.side + size_t(ib) * nb);
+  double* top = p.top;
+  double* bot = ts ? p.bot : p.top;
+  for (int P = p.p0; P < p.p1; ++P) {
+    const int ii = P * ib;
+    const int nm = lu_moves(ipiv + ii, ii, sb, ts, sp, mv_dst, mv_src, &n_moves);
+    auto at = [&](int code, int c) -> double* {
+      return code >= 0 ? bot + size_t(c) * nb + code : top + size_t(c) * nb + ii + (-1 - code);
+    };
+    for (int e = tid; e < nm * BN; e += G::THREADS) mvv[e] = *at(mv_src[e / BN], n0 + e % BN);
+    __syncthreads();
+    for (int e = tid; e < nm * BN; e += G::THREADS) *at(mv_dst[e / BN], n0 + e % BN) = mvv[e];
+    __syncthreads();
+    for (int e = tid; e < sb * BN; e += G::THREADS) {
+      const int c = e / sb, r = e % sb;
+      Ts[c * kLcLd + r] = top[size_t(n0 + c) * nb + ii + r];
+    }
+    __syncthreads();
+    {  // top' = inv(L_uu) top
+      double acc[G::FM][G::FN][2];
+      zero_acc<G>(acc);
+      TileLoader<G, M_MAJOR, 128> la{p.side + size_t(ii) * ib, ib, 0};
+      gemm_mainloop_bsmem<G>(acc, ring, la, Ts, kLcLd, 0, sb);
+      for_each_acc<G>(acc, [&](int r, int c, double v) {
+        Wt[c * kLcLd + r] = v;
+        top[size_t(n0 + c) * nb + ii + r] = v;
+      });
+    }
+    __syncthreads();
+    if (!p.swap_only) {
+      const int m_lo = ts ? 0 : ii + sb;
+      for (int m0 = m_lo; m0 < nb; m0 += 128) {
+        double acc[G::FM][G::FN][2];
+        zero_acc<G>(acc);
+        TileLoader<G, M_MAJOR, 128> la{p.L + size_t(ii) * nb, nb, m0};
+        gemm_mainloop_bsmem<G>(acc, ring, la, Wt, kLcLd, 0, sb);
+        sub_store<G>(acc, bot, nb, m0, n0);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+using CfgLS16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
+using CfgLS32 = GemmCfg<128, 32, 16, 32, 32, 3>;  // 4 warps
+
+template <class G>
+static unsigned lu_apply_strip_smem() {
+  size_t d = GemmSmem<G, M_MAJOR, K_MAJOR>::DOUBLES + 2 * G::BN * kLcLd;
+  size_t ints = 2 * kLcMaxMoves + 3 * kLuMaxSb;
+  return unsigned(d * sizeof(double) + ints * sizeof(int));
+}
+
+static unsigned lu_apply_cl_smem() {
+  size_t d = GemmSmem<CfgLC, M_MAJOR, K_MAJOR>::DOUBLES + 3 * kLcBN * kLcLd + kLcMaxMoves * 8;
+  size_t ints = 2 * kLcMaxMoves + 3 * kLuMaxSb;
+  return unsigned(d * sizeof(double) + ints * sizeof(int));
+}
+
+// ---------------------------------------------------------------------------
+static unsigned sp_smem(int nb) {
+  size_t b = nb == 1024 ? SpSmem<128>::BYTES : SpSmem<64>::BYTES;
+  size_t ls = size_t(kSpSB) * (kSpSB + 1) * 8;  // end-of-panel inverse scratch
+  return unsigned(b > ls ? b : ls);
+}
+
 static unsigned panel_smem(int nb, int sb) {
   const int R = nb / kLuCl;
   size_t bufs = 7 * size_t(sb) + R + 4;
@@ -425,8 +1054,19 @@ static unsigned panel_smem(int nb, int sb) {
   return unsigned((bufs > inv ? bufs : inv) * sizeof(double));
 }
 
+// HG_LU_PANEL=reg selects the register-resident full-width panel kernel (experiments)
+static bool use_sp_panel(int nb, int ib) {
+  static const bool reg = [] {
+    const char* e = getenv("HG_LU_PANEL");
+    return e && e[0] == 'r';
+  }();
+  return !reg && ib == kSpSB && (nb == 1024 || nb == 512);
+}
+
 static const void* panel_kernel(int nb, int ib) {
+  if (use_sp_panel(nb, ib)) return nb == 1024 ? (const void*)k_lu_panel_sp<128> : (const void*)k_lu_panel_sp<64>;
   if (nb == 1024 && ib == 128) return (const void*)k_lu_panel<128, 128>;
+  if (nb == 512 && ib == 128) return (const void*)k_lu_panel<64, 128>;
   if (nb == 1024 && ib == 64) return (const void*)k_lu_panel<128, 64>;
   if (nb == 512 && ib == 128) return (const void*)k_lu_panel<64, 128>;
   if (nb == 512 && ib == 64) return (const void*)k_lu_panel<64, 64>;
@@ -458,6 +1098,11 @@ bool init_lu_attributes() {
   HG_ATTR(k_lu_apply<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem<128>(1024));
   HG_ATTR(k_lu_apply<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem<64>(1024));
   HG_ATTR(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, nn_smem());
+  HG_ATTR(k_lu_apply_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_cl_smem());
+  HG_ATTR(k_lu_apply_strip<CfgLS16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS16>());
+  HG_ATTR(k_lu_apply_strip<CfgLS32>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS32>());
+  HG_ATTR(k_lu_panel_sp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpSmem<128>::BYTES);
+  HG_ATTR(k_lu_panel_sp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(512));
   return true;
 }
 
@@ -475,8 +1120,43 @@ static void push_apply(std::vector<LaunchDesc>& out, int ib, const LuApplyParams
 
 // One panel applied to columns [col0, nb): narrow swap + inv(L_uu) kernel,
 // then the wide bot -= L_a * top GEMM.
+static bool use_cluster_apply(int nb, int ib) { return ib == kLuMaxSb && nb % (kLcCl * 128) == 0; }
+
+// HG_LU_APPLY env: "cl" = 4-CTA cluster kernel, 16 / 32 = strip width (experiments)
+static int lu_apply_env() {
+  static const int v = [] {
+    const char* e = getenv("HG_LU_APPLY");
+    if (!e) return 0;
+    if (e[0] == 'c') return -1;
+    return atoi(e);
+  }();
+  return v;
+}
+
+// Panels [P0, P1) applied to columns [col0, nb): strip kernel (default) or cluster kernel.
+static void push_apply_cl(std::vector<LaunchDesc>& out, const double* L, const double* side, double* top,
+                          double* bot, int nb, int ib, int P0, int P1, int col0, int mode, int bn_default = 32) {
+  LuApplyParams ap{L, side, top, bot, nb, ib, P0, P1, col0, mode, 0};
+  LaunchDesc d;
+  const int bn = lu_apply_env() ? lu_apply_env() : bn_default;
+  const int ncols = nb - col0;
+  if (bn < 0)
+    d.set((const void*)k_lu_apply_cl, dim3(ncols / kLcBN * kLcCl), dim3(CfgLC::THREADS), lu_apply_cl_smem(), ap);
+  else if (bn == 16)
+    d.set((const void*)k_lu_apply_strip<CfgLS16>, dim3(ncols / 16), dim3(CfgLS16::THREADS),
+          lu_apply_strip_smem<CfgLS16>(), ap);
+  else
+    d.set((const void*)k_lu_apply_strip<CfgLS32>, dim3(ncols / 32), dim3(CfgLS32::THREADS),
+          lu_apply_strip_smem<CfgLS32>(), ap);
+  out.push_back(d);
+}
+
 static void push_panel_apply(std::vector<LaunchDesc>& out, int ib, const double* L, const double* side,
                              double* top, double* bot, int nb, int P, int col0, int mode) {
+  if (use_cluster_apply(nb, ib)) {
+    push_apply_cl(out, L, side, top, bot, nb, ib, P, P + 1, col0, mode, 16);
+    return;
+  }
   LuApplyParams ap{L, side, top, bot, nb, ib, P, P + 1, col0, mode, 1};
   push_apply(out, ib, ap);
   const int ii = P * ib;
@@ -508,7 +1188,10 @@ bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
         LuPanelParams pp{A, ts ? o.t[0] : nullptr, ts ? side(1) : side(0), nb, ib, P * ib, ib,
                          ts ? LU_TSTRF : LU_GETRF, o.status};
         LaunchDesc d;
-        d.set(panel_kernel(nb, ib), dim3(kLuCl), dim3(kLuThreads), panel_smem(nb, ib), pp);
+        if (use_sp_panel(nb, ib))
+          d.set(panel_kernel(nb, ib), dim3(kLuCl), dim3(kSpThreads), sp_smem(nb), pp);
+        else
+          d.set(panel_kernel(nb, ib), dim3(kLuCl), dim3(kLuThreads), panel_smem(nb, ib), pp);
         out.push_back(d);
         if (P + 1 < np)
           push_panel_apply(out, ib, A, ts ? side(1) : side(0), ts ? o.t[0] : A, A, nb, P, (P + 1) * ib,
@@ -517,9 +1200,17 @@ bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
       return true;
     }
     case K_GESSM:
+      if (use_cluster_apply(nb, ib)) {
+        push_apply_cl(out, o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF);
+        return true;
+      }
       for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[1], nb, P, 0, LU_GETRF);
       return true;
     case K_SSSSM:
+      if (use_cluster_apply(nb, ib)) {
+        push_apply_cl(out, o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF);
+        return true;
+      }
       for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[2], nb, P, 0, LU_TSTRF);
       return true;
     default:

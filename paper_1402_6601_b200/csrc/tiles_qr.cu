@@ -18,6 +18,7 @@
 //                with W resident in shared memory and the masked unit-lower
 //                V blocks loaded element-wise on the diagonal slabs.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "dgemm_dmma.cuh"
 #include "tiles.h"
@@ -274,8 +275,9 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
 }
 
 // ---------------------------------------------------------------------------
-using CfgQ = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps; requires sb == 128
-constexpr int kQrBN = 64;
+using CfgQ64 = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps; requires sb == 128
+using CfgQ32 = GemmCfg<128, 32, 16, 32, 32, 3>;  // 4 warps
+using CfgQ16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
 constexpr int kWld = kQrMaxSb + 4;  // W stored [n][k]
 
 // Unit-lower reflector block V of panel ii, element (tile row tr, panel col pc):
@@ -318,7 +320,12 @@ struct QrApplyParams {
   int nb, ib, p0, p1, col0, mode;
 };
 
+// Column-strip variant: one CTA per BN-column strip (no cluster, all rows),
+// BN in {16, 32, 64}: narrower strips = more SMs per task (latency), wider =
+// more reuse of V per SM (throughput inside the DAG).
+template <class CfgQ>
 __global__ void __launch_bounds__(CfgQ::THREADS) k_qr_apply(QrApplyParams p) {
+  constexpr int kQrBN = CfgQ::BN;
   extern __shared__ double sm[];
   double* ring = sm;
   double* W = sm + GemmSmem<CfgQ, K_MAJOR, K_MAJOR>::DOUBLES;  // [n][k], ld kWld
@@ -377,6 +384,136 @@ __global__ void __launch_bounds__(CfgQ::THREADS) k_qr_apply(QrApplyParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// k_qr_apply_cl -- the same block-reflector application with the tile ROWS
+// split over a 4-CTA cluster, so one TSMQR / UNMQR (or a GEQRT / TSQRT
+// trailing update) spreads over (N/32) x 4 SMs instead of N/64:
+//   CTA q owns rows [q*nb/4, (q+1)*nb/4) of C (UNMQR) / bot (TSMQR) and a
+//   32-column strip.  Per panel:
+//     1. W_q = V[rows_q]^T C[rows_q]            (DMMA, split-K partial)
+//     2. cluster barrier; CTA q reduces W rows [32q, 32q+32) over DSMEM
+//        (+ top rows for TSMQR)
+//     3. cluster barrier; every CTA gathers W rows 0..32q+31, forms its
+//        slice of W' = T^T W (T upper triangular)
+//     4. cluster barrier; every CTA gathers W' (TSMQR: CTA q also applies
+//        top -= W' to its slice of the top rows)
+//     5. C[rows_q] -= V[rows_q] W'             (DMMA, W' resident in smem)
+// Partial / slice buffers alternate by panel parity, so a fast CTA writing
+// panel P+1's partials never overwrites a slice a slow CTA still gathers.
+constexpr int kQcCl = 4;
+constexpr int kQcBN = 32;
+using CfgQC = GemmCfg<128, kQcBN, 16, 32, 16, 3>;  // 8 warps, 32x16 warp tiles
+constexpr int kQcSlice = kQrMaxSb / kQcCl;          // W rows reduced per CTA
+
+__global__ void __cluster_dims__(kQcCl, 1, 1) __launch_bounds__(CfgQC::THREADS) k_qr_apply_cl(QrApplyParams p) {
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  constexpr int RING = GemmSmem<CfgQC, K_MAJOR, K_MAJOR>::DOUBLES;
+  constexpr int WBUF = kQcBN * kWld;
+  double* ring = sm;
+  double* Wp = sm + RING;             // [2][WBUF]: partials, then W' slices (by panel parity)
+  double* Ws = Wp + 2 * WBUF;         // reduced W slice + gathered W, then gathered W'
+  const int nb = p.nb, ib = p.ib;
+  const int n0 = p.col0 + (blockIdx.x / kQcCl) * kQcBN;
+  const int rows = nb / kQcCl;
+  const int r_begin = q * rows, r_end = r_begin + rows;
+  const bool ts = p.mode == QR_TSQRT;
+  const int tid = threadIdx.x;
+  for (int P = p.p0; P < p.p1; ++P) {
+    const int ii = P * ib;
+    const double* Vp = p.V + size_t(ii) * nb;
+    double* C = ts ? p.bot : p.top;
+    double* wp = Wp + (P & 1) * WBUF;
+    // rows of C this CTA touches in this panel (UNMQR: only tile rows >= ii)
+    const int k0 = ts ? r_begin : max(r_begin, ii);
+    // ---- 1. partial W_q --------------------------------------------------------
+    {
+      double acc[CfgQC::FM][CfgQC::FN][2];
+      zero_acc<CfgQC>(acc);
+      if (k0 < r_end) {
+        VLoader<CfgQC, K_MAJOR, 128> la{Vp, nb, 0, ii, ts ? 0 : 1};
+        TileLoader<CfgQC, K_MAJOR, kQcBN> lb{C, nb, n0};
+        gemm_mainloop<CfgQC>(acc, ring, la, lb, k0, r_end);
+      }
+      for_each_acc<CfgQC>(acc, [&](int r, int c, double v) { wp[c * kWld + r] = v; });
+    }
+    cl.sync();
+    // ---- 2. reduce my slice of W ------------------------------------------------
+    const int s0 = q * kQcSlice;
+    {
+      const double* parts[kQcCl];
+#pragma unroll
+      for (int c2 = 0; c2 < kQcCl; ++c2) parts[c2] = cl.map_shared_rank(wp, c2);
+      for (int e = tid; e < kQcSlice * kQcBN; e += CfgQC::THREADS) {
+        const int c = e / kQcSlice, r = s0 + e % kQcSlice;
+        double v[kQcCl];
+#pragma unroll
+        for (int c2 = 0; c2 < kQcCl; ++c2) v[c2] = parts[c2][c * kWld + r];
+        double t = ts ? p.top[size_t(n0 + c) * nb + ii + r] : 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 < kQcCl; ++c2) t += v[c2];
+        Ws[c * kWld + r] = t;
+      }
+    }
+    cl.sync();
+    // ---- 3. gather W rows [0, s0) and form my slice of W' = T^T W -------------------
+    for (int c2 = 0; c2 < q; ++c2) {
+      const double* src = cl.map_shared_rank(Ws, c2);
+      for (int e = tid; e < kQcSlice * kQcBN; e += CfgQC::THREADS) {
+        const int c = e / kQcSlice, r = c2 * kQcSlice + e % kQcSlice;
+        Ws[c * kWld + r] = src[c * kWld + r];
+      }
+    }
+    __syncthreads();
+    {
+      const double* T = p.side + size_t(ii) * ib;  // T(k, r) at T[r*ib + k], upper triangular
+      for (int e = tid; e < kQcSlice * kQcBN; e += CfgQC::THREADS) {
+        const int c = e / kQcSlice, r = s0 + e % kQcSlice;
+        const double* tc = T + size_t(r) * ib;
+        const double* wc = Ws + c * kWld;
+        double a0 = 0.0, a1 = 0.0;
+        int k = 0;
+        for (; k + 1 <= r; k += 2) {
+          a0 = fma(__ldg(tc + k), wc[k], a0);
+          a1 = fma(__ldg(tc + k + 1), wc[k + 1], a1);
+        }
+        if (k <= r) a0 = fma(__ldg(tc + k), wc[k], a0);
+        wp[c * kWld + r] = a0 + a1;
+      }
+    }
+    cl.sync();
+    // ---- 4. gather W' ----------------------------------------------------------------
+    for (int c2 = 0; c2 < kQcCl; ++c2) {
+      const double* src = cl.map_shared_rank(wp, c2);
+      for (int e = tid; e < kQcSlice * kQcBN; e += CfgQC::THREADS) {
+        const int c = e / kQcSlice, r = c2 * kQcSlice + e % kQcSlice;
+        Ws[c * kWld + r] = src[c * kWld + r];
+      }
+    }
+    __syncthreads();
+    if (ts)
+      for (int e = tid; e < kQcSlice * kQcBN; e += CfgQC::THREADS) {
+        const int c = e / kQcSlice, r = s0 + e % kQcSlice;
+        p.top[size_t(n0 + c) * nb + ii + r] -= Ws[c * kWld + r];
+      }
+    // ---- 5. C[rows] -= V[rows] W' ------------------------------------------------------
+    for (int m0 = k0; m0 < r_end; m0 += 128) {
+      double acc[CfgQC::FM][CfgQC::FN][2];
+      zero_acc<CfgQC>(acc);
+      VLoader<CfgQC, M_MAJOR, 128> la{Vp, nb, m0, ii, ts ? 0 : 1};
+      gemm_mainloop_bsmem<CfgQC>(acc, ring, la, Ws, kWld, 0, 128);
+      sub_store<CfgQC>(acc, C, nb, m0, n0);
+    }
+    __syncthreads();
+  }
+  cl.sync();  // no CTA leaves while a peer may still read its W' slice
+}
+
+static unsigned qr_apply_cl_smem() {
+  return unsigned((GemmSmem<CfgQC, K_MAJOR, K_MAJOR>::DOUBLES + 3 * kQcBN * kWld) * sizeof(double));
+}
+
+// ---------------------------------------------------------------------------
 static unsigned qr_panel_smem(int nb, int sb) {
   const int R = nb / kQrCl;
   size_t d = size_t(sb) * (R + 1);
@@ -386,8 +523,9 @@ static unsigned qr_panel_smem(int nb, int sb) {
   return unsigned(d * sizeof(double));
 }
 
+template <class CfgQ>
 static unsigned qr_apply_smem() {
-  return unsigned((GemmSmem<CfgQ, K_MAJOR, K_MAJOR>::DOUBLES + kQrBN * kWld) * sizeof(double));
+  return unsigned((GemmSmem<CfgQ, K_MAJOR, K_MAJOR>::DOUBLES + CfgQ::BN * kWld) * sizeof(double));
 }
 
 #define HG_QATTR(fn, attr, val)                                                                  \
@@ -401,7 +539,10 @@ static unsigned qr_apply_smem() {
 
 bool init_qr_attributes() {
   HG_QATTR(k_qr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_panel_smem(1024, 128));
-  HG_QATTR(k_qr_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem());
+  HG_QATTR(k_qr_apply<CfgQ64>, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ64>());
+  HG_QATTR(k_qr_apply<CfgQ32>, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ32>());
+  HG_QATTR(k_qr_apply<CfgQ16>, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ16>());
+  HG_QATTR(k_qr_apply_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_cl_smem());
   return true;
 }
 
@@ -414,9 +555,25 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
   const size_t tile = size_t(nb) * nb;
   const int np = nb / ib;
   auto side = [&](int i) { return o.t[i] + tile; };
-  auto push_apply = [&](const QrApplyParams& ap) {
+  // strip width: HG_QR_APPLY env ("cl" = 4-CTA cluster kernel, or 16 / 32 / 64)
+  static const int mode_env = [] {
+    const char* e = getenv("HG_QR_APPLY");
+    if (!e) return 0;
+    if (e[0] == 'c') return -1;
+    return atoi(e);
+  }();
+  auto push_apply = [&](const QrApplyParams& ap, int bn_default) {
     LaunchDesc d;
-    d.set((const void*)k_qr_apply, dim3((nb - ap.col0) / kQrBN), dim3(CfgQ::THREADS), qr_apply_smem(), ap);
+    const int bn = mode_env ? mode_env : bn_default;
+    const int ncols = nb - ap.col0;
+    if (bn < 0 && nb % (kQcCl * 128) == 0)
+      d.set((const void*)k_qr_apply_cl, dim3(ncols / kQcBN * kQcCl), dim3(CfgQC::THREADS), qr_apply_cl_smem(), ap);
+    else if (bn == 16)
+      d.set((const void*)k_qr_apply<CfgQ16>, dim3(ncols / 16), dim3(CfgQ16::THREADS), qr_apply_smem<CfgQ16>(), ap);
+    else if (bn == 32)
+      d.set((const void*)k_qr_apply<CfgQ32>, dim3(ncols / 32), dim3(CfgQ32::THREADS), qr_apply_smem<CfgQ32>(), ap);
+    else
+      d.set((const void*)k_qr_apply<CfgQ64>, dim3(ncols / 64), dim3(CfgQ64::THREADS), qr_apply_smem<CfgQ64>(), ap);
     out.push_back(d);
   };
   switch (kind) {
@@ -432,15 +589,15 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
         out.push_back(d);
         if (P + 1 < np)
           push_apply(QrApplyParams{A, ts ? side(1) : side(0), ts ? o.t[0] : A, ts ? A : nullptr, nb, ib, P, P + 1,
-                                   (P + 1) * ib, ts ? QR_TSQRT : QR_GEQRT});
+                                   (P + 1) * ib, ts ? QR_TSQRT : QR_GEQRT}, 16);
       }
       return true;
     }
     case K_UNMQR:
-      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], nullptr, nb, ib, 0, np, 0, QR_GEQRT});
+      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], nullptr, nb, ib, 0, np, 0, QR_GEQRT}, 32);
       return true;
     case K_TSMQR:
-      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, QR_TSQRT});
+      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, QR_TSQRT}, 32);
       return true;
     default:
       set_error("kind %d is not a QR kind", kind);

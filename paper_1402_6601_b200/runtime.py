@@ -14,6 +14,7 @@ column-major (PLASMA layout), T-factor blocks ``ib x b``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -97,7 +98,7 @@ class Executor:
 
     def __init__(self, graph, platform, plan, host_in: np.ndarray, host_out: np.ndarray | None = None,
                  devices=None, device_input: bool = False, host_side_out: np.ndarray | None = None,
-                 rank_node: int = 0):
+                 rank_node: int = 0, priority_levels: int = 6):
         L = _native.lib()
         lay = graph.layout
         if lay is None:
@@ -133,6 +134,10 @@ class Executor:
         self.host_side_out = host_side_out
         self.plan = plan
         self.devices = devices
+        # node priorities from the plan's own predicted durations (end - start):
+        # changes only which ready kernel gets SMs first, never the plan
+        priority_levels = int(os.environ.get("HG_PRIORITY_LEVELS", priority_levels))
+        self.task_weight = np.ascontiguousarray(np.asarray(plan.end, np.float64) - np.asarray(plan.start, np.float64))
         self._keep = [fl, kind_map]
         ep = ExecPlan_from(plan, n, len(graph.data), k, lay, self, fl)
         opts = _native.ExecOpts(
@@ -140,7 +145,8 @@ class Executor:
             _native.ptr(self.host_in, C.c_double),
             _native.ptr(host_out, C.c_double) if host_out is not None else None,
             _native.ptr(host_side_out, C.c_double) if host_side_out is not None else None,
-            int(bool(device_input)), int(rank_node))
+            int(bool(device_input)), int(rank_node),
+            _native.ptr(self.task_weight, C.c_double), int(priority_levels))
         h = C.c_void_p()
         _native.check(L.hg_exec_create(C.byref(ep), C.byref(opts), C.byref(h)), "hg_exec_create")
         self._h = h
@@ -197,7 +203,7 @@ class DistributedExecutor(Executor):
     """
 
     def __init__(self, graph, platform, plan, host_in, host_out=None, rank=None, world=None, device=None,
-                 device_input=False, host_side_out=None, group=None):
+                 device_input=False, host_side_out=None, group=None, priority_levels: int = 6):
         import torch.distributed as dist
 
         rank = dist.get_rank(group) if rank is None else rank
@@ -207,7 +213,8 @@ class DistributedExecutor(Executor):
         check_same_plan(plan, world, group)
         dev = int(device if device is not None else rank % max(1, _native.lib().hg_device_count()))
         super().__init__(graph, platform, plan, host_in, host_out, devices=[dev] * platform.k,
-                         device_input=device_input, host_side_out=host_side_out, rank_node=rank + 1)
+                         device_input=device_input, host_side_out=host_side_out, rank_node=rank + 1,
+                         priority_levels=priority_levels)
         L = _native.lib()
         mine = (C.c_char * 64)()
         _native.check(L.hg_exec_ipc_handle(self._h, mine), "hg_exec_ipc_handle")
