@@ -161,6 +161,7 @@ typedef struct hg_exec_plan {
   const int32_t* job_requester;
   const int64_t* block_bytes; /* host image bytes per block (tile or T factor) */
   const int32_t* final_writer;/* last writer task per block, -1 = never written */
+  const int8_t* acc_mode;     /* HG_ACCESS_* per access (CSR like acc_block) */
 } hg_exec_plan;
 
 typedef struct hg_exec_opts {

@@ -66,7 +66,7 @@ class ExecPlan(C.Structure):
                 ("pred_ptr", _i64p), ("pred", _i32p), ("dispatch", _i32p), ("wait_ptr", _i64p),
                 ("wait_job", _i32p), ("job_block", _i32p), ("job_src", _i32p), ("job_dst", _i32p),
                 ("job_version", _i32p), ("job_src_job", _i32p), ("job_requester", _i32p),
-                ("block_bytes", _i64p), ("final_writer", _i32p)]
+                ("block_bytes", _i64p), ("final_writer", _i32p), ("acc_mode", _i8p)]
 
 
 class ExecOpts(C.Structure):

@@ -256,3 +256,66 @@ HG_DEVICE void sub_store(double (&acc)[Cfg::FM][Cfg::FN][2], double* __restrict_
 }
 
 }  // namespace hg
+
+namespace hg {
+
+// C[m, n0 + c] -= sum_k A(m, k) B(c, k) for every BM-row chunk of [m_begin,
+// m_end), with B resident in shared memory (sB[c*ldsb + k], k in [0, K)) and
+// ONE continuous cp.async ring over all (chunk, k-slab) pairs: the A stream
+// never drains between chunks, only the per-chunk epilogue interrupts the
+// DMMAs (the trailing updates of GESSM / SSSSM / UNMQR / TSMQR, K = ib).
+// LdA exposes a mutable row origin r0.
+template <class Cfg, class LdA>
+HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int ldsb, int K, int m_begin,
+                                     int m_end, double* __restrict__ C, int ldc, int n0) {
+  constexpr int LA = LdA::layout;
+  constexpr int A_SLAB = LA == M_MAJOR ? Cfg::slab_mmaj(Cfg::BM) : Cfg::slab_kmaj(Cfg::BM);
+  constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
+  const int nk = K / BK;
+  const int total = nk * ((m_end - m_begin) / Cfg::BM);
+  if (total <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+  auto load = [&](int s) {
+    LdA l = la;
+    l.r0 = m_begin + (s / nk) * Cfg::BM;
+    l.load(ring + (s % STAGES) * A_SLAB, (s % nk) * BK);
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < total) load(s);
+    cp_async_commit();
+  }
+  double acc[Cfg::FM][Cfg::FN][2];
+  zero_acc<Cfg>(acc);
+  for (int it = 0; it < total; ++it) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (it + STAGES - 1 < total) load(it + STAGES - 1);
+    cp_async_commit();
+    const double* a_s = ring + (it % STAGES) * A_SLAB;
+    const int kb = (it % nk) * BK;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) af[i] = frag_at<Cfg, LA, Cfg::BM>(a_s, wm + i * 8 + g, kk + t);
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) bf[j] = sB[(wn + j * 8 + g) * ldsb + kb + kk + t];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    if (it % nk == nk - 1) {
+      sub_store<Cfg>(acc, C, ldc, m_begin + (it / nk) * Cfg::BM, n0);
+      zero_acc<Cfg>(acc);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+}  // namespace hg

@@ -20,6 +20,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <algorithm>
+#include <unordered_map>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -217,6 +218,7 @@ struct hg_exec {
   // plan (owned copy)
   int k = 0, nb = 0, ib = 0, side = 0, n_blocks = 0, n_tasks = 0, n_jobs = 0;
   std::vector<int32_t> task_kind, task_node, acc_block, pred, dispatch, wait_job;
+  std::vector<int8_t> acc_mode;
   std::vector<int64_t> acc_ptr, pred_ptr, wait_ptr, block_bytes;
   std::vector<int32_t> job_block, job_src, job_dst, job_version, job_src_job, job_requester, final_writer;
   // options
@@ -438,6 +440,32 @@ static int build_graph(hg_exec* ex) {
   const std::vector<int> prio = task_priorities(ex, 0);
   const bool use_prio = ex->priority_levels > 0 && !ex->task_weight.empty();
 
+  // Delivery of a block version to a node: a task must wait for the copy job
+  // that brought the version it reads to its node, even when that job was
+  // requested by ANOTHER task (sim.py:242-253 dedups (data, node) in flight
+  // and skips blocks already valid on the node, so the plan's wait list of
+  // this task does not name it, and the DAG does not order it either).
+  // Version read by access a = last writer of the block before the task in
+  // program order (the DAG's sequential consistency, graph.py:58-84).
+  std::vector<int32_t> acc_version(ex->acc_block.size(), -1);
+  {
+    std::vector<int32_t> cur(ex->n_blocks, -1);
+    for (int t = 0; t < n; ++t) {
+      for (int64_t a = ex->acc_ptr[t]; a < ex->acc_ptr[t + 1]; ++a) acc_version[a] = cur[ex->acc_block[a]];
+      for (int64_t a = ex->acc_ptr[t]; a < ex->acc_ptr[t + 1]; ++a)
+        if (ex->acc_mode.empty() || (ex->acc_mode[a] & HG_ACCESS_W)) cur[ex->acc_block[a]] = t;
+    }
+  }
+  auto dkey = [&](int b, int v, int node) {
+    return (uint64_t(uint32_t(b)) << 40) ^ (uint64_t(uint32_t(v + 1)) << 8) ^ uint64_t(node);
+  };
+  std::unordered_map<uint64_t, int> delivery;  // (block, version, dst node) -> job
+  for (int j = 0; j < ex->n_jobs; ++j) {
+    // the version a job moves: the writer task, or (H2D of an untouched block) -1
+    const int v = ex->job_version[j];
+    if (ex->job_dst[j] >= 1) delivery.emplace(dkey(ex->job_block[j], v, ex->job_dst[j]), j);
+  }
+
   // dependency on the producer of a task output / job delivery for a consumer on cons_node
   auto dep_task = [&](int u, int cons_node) -> int {
     const int pn = ex->task_node[u];
@@ -542,10 +570,23 @@ static int build_graph(hg_exec* ex) {
     if (!build_task_launches(ex->task_kind[t], ops, launches)) return HG_EINVAL;
     deps.clear();
     for (int64_t w = ex->wait_ptr[t]; w < ex->wait_ptr[t + 1]; ++w) deps.push_back(job_node[ex->wait_job[w]]);
+    for (int64_t a = a0; a < a1; ++a) {
+      if (!ex->acc_mode.empty() && !(ex->acc_mode[a] & HG_ACCESS_R)) continue;
+      auto it = delivery.find(dkey(ex->acc_block[a], acc_version[a], node));
+      if (it == delivery.end()) continue;
+      const int j = it->second;
+      if (!job_node[j]) {
+        set_error("task %d reads block %d on node %d before its delivery job %d exists", t, ex->acc_block[a], node, j);
+        return HG_EINVAL;
+      }
+      deps.push_back(job_node[j]);
+    }
     for (int64_t q = ex->pred_ptr[t]; q < ex->pred_ptr[t + 1]; ++q) {
       int rc = dep_task(ex->pred[q], node);
       if (rc) return rc;
     }
+    std::sort(deps.begin(), deps.end());  // a delivery job may also be in the wait list
+    deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
     HG_CUDA(cudaSetDevice(ex->dev[node - 1]));
     cudaGraphNode_t prev = nullptr;
     for (size_t li = 0; li < launches.size(); ++li) {
@@ -637,6 +678,7 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
   ex->task_node = vcopy(P->task_node, n);
   ex->acc_ptr = vcopy(P->acc_ptr, n + 1);
   ex->acc_block = vcopy(P->acc_block, P->acc_ptr[n]);
+  ex->acc_mode = vcopy(P->acc_mode, P->acc_ptr[n]);
   ex->pred_ptr = vcopy(P->pred_ptr, n + 1);
   ex->pred = vcopy(P->pred, P->pred_ptr[n]);
   ex->dispatch = vcopy(P->dispatch, n);

@@ -966,14 +966,14 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
 template <class G>
 __global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) {
   constexpr int BN = G::BN;
-  constexpr int RING = GemmSmem<G, M_MAJOR, K_MAJOR>::DOUBLES;
-  static_assert(RING >= kLcMaxMoves * BN, "move staging aliases the ring");
+  constexpr int RING = G::STAGES * G::slab_mmaj(G::BM);  // only A streams (B is resident)
+  constexpr int AREA = (RING + BN * kLcLd > kLcMaxMoves * BN) ? RING + BN * kLcLd : kLcMaxMoves * BN;
   extern __shared__ double sm[];
   double* ring = sm;
-  double* mvv = sm;                       // interchange staging (ring is idle then)
-  double* Ts = sm + RING;                 // [BN][kLcLd] top rows after the moves
-  double* Wt = Ts + BN * kLcLd;           // [BN][kLcLd] top'
-  int* mv_dst = reinterpret_cast<int*>(Wt + BN * kLcLd);
+  double* mvv = sm;                       // interchange staging (ring and Ts are idle then)
+  double* Ts = sm + RING;                 // [BN][kLcLd] top rows after the moves, then top'
+  double* Wt = Ts;                        // top' overwrites Ts once the product has read it
+  int* mv_dst = reinterpret_cast<int*>(sm + AREA);
   int* mv_src = mv_dst + kLcMaxMoves;
   int* sp = mv_src + kLcMaxMoves;         // [3 * sb]
   __shared__ int n_moves;
@@ -1011,14 +1011,8 @@ __global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) 
     }
     __syncthreads();
     if (!p.swap_only) {
-      const int m_lo = ts ? 0 : ii + sb;
-      for (int m0 = m_lo; m0 < nb; m0 += 128) {
-        double acc[G::FM][G::FN][2];
-        zero_acc<G>(acc);
-        TileLoader<G, M_MAJOR, 128> la{p.L + size_t(ii) * nb, nb, m0};
-        gemm_mainloop_bsmem<G>(acc, ring, la, Wt, kLcLd, 0, sb);
-        sub_store<G>(acc, bot, nb, m0, n0);
-      }
+      TileLoader<G, M_MAJOR, 128> la{p.L + size_t(ii) * nb, nb, 0};
+      gemm_sub_chunks_bsmem<G>(ring, la, Wt, kLcLd, sb, ts ? 0 : ii + sb, nb, bot, nb, n0);
     }
     __syncthreads();
   }
@@ -1026,10 +1020,12 @@ __global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) 
 
 using CfgLS16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
 using CfgLS32 = GemmCfg<128, 32, 16, 32, 32, 3>;  // 4 warps
+using CfgLS64 = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps
 
 template <class G>
 static unsigned lu_apply_strip_smem() {
-  size_t d = GemmSmem<G, M_MAJOR, K_MAJOR>::DOUBLES + 2 * G::BN * kLcLd;
+  size_t d = size_t(G::STAGES) * G::slab_mmaj(G::BM) + G::BN * kLcLd;
+  if (d < size_t(kLcMaxMoves) * G::BN) d = size_t(kLcMaxMoves) * G::BN;
   size_t ints = 2 * kLcMaxMoves + 3 * kLuMaxSb;
   return unsigned(d * sizeof(double) + ints * sizeof(int));
 }
@@ -1101,6 +1097,7 @@ bool init_lu_attributes() {
   HG_ATTR(k_lu_apply_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_cl_smem());
   HG_ATTR(k_lu_apply_strip<CfgLS16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS16>());
   HG_ATTR(k_lu_apply_strip<CfgLS32>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS32>());
+  HG_ATTR(k_lu_apply_strip<CfgLS64>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS64>());
   HG_ATTR(k_lu_panel_sp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpSmem<128>::BYTES);
   HG_ATTR(k_lu_panel_sp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(512));
   return true;
@@ -1145,6 +1142,9 @@ static void push_apply_cl(std::vector<LaunchDesc>& out, const double* L, const d
   else if (bn == 16)
     d.set((const void*)k_lu_apply_strip<CfgLS16>, dim3(ncols / 16), dim3(CfgLS16::THREADS),
           lu_apply_strip_smem<CfgLS16>(), ap);
+  else if (bn == 64 && ncols % 64 == 0)
+    d.set((const void*)k_lu_apply_strip<CfgLS64>, dim3(ncols / 64), dim3(CfgLS64::THREADS),
+          lu_apply_strip_smem<CfgLS64>(), ap);
   else
     d.set((const void*)k_lu_apply_strip<CfgLS32>, dim3(ncols / 32), dim3(CfgLS32::THREADS),
           lu_apply_strip_smem<CfgLS32>(), ap);

@@ -370,15 +370,10 @@ __global__ void __launch_bounds__(CfgQ::THREADS) k_qr_apply(QrApplyParams p) {
         p.top[size_t(n0 + c) * nb + ii + r] -= W[c * kWld + r];
       }
     }
-    const int m_begin = ts ? 0 : ii;
-    for (int m0 = m_begin; m0 < nb; m0 += 128) {
-      double acc[CfgQ::FM][CfgQ::FN][2];
-      zero_acc<CfgQ>(acc);
-      VLoader<CfgQ, M_MAJOR, 128> la{Vp, nb, m0, ii, ts ? 0 : 1};
-      gemm_mainloop_bsmem<CfgQ>(acc, ring, la, W, kWld, 0, 128);
-      sub_store<CfgQ>(acc, ts ? p.bot : p.top, nb, m0, n0);
+    {
+      VLoader<CfgQ, M_MAJOR, 128> la{Vp, nb, 0, ii, ts ? 0 : 1};
+      gemm_sub_chunks_bsmem<CfgQ>(ring, la, W, kWld, 128, ts ? 0 : ii, nb, ts ? p.bot : p.top, nb, n0);
     }
-    __threadfence();
     __syncthreads();
   }
 }

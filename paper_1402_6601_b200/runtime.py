@@ -298,7 +298,7 @@ def ExecPlan_from(plan, n, n_blocks, k, lay, ex, fl):
         P(plan.dispatch, C.c_int32), P(plan.wait_ptr, C.c_int64), P(plan.wait_job, C.c_int32),
         P(plan.job_block, C.c_int32), P(plan.job_src, C.c_int32), P(plan.job_dst, C.c_int32),
         P(plan.job_version, C.c_int32), P(plan.job_src_job, C.c_int32), P(plan.job_requester, C.c_int32),
-        P(fl["sizes"], C.c_int64), P(ex.final_writer, C.c_int32))
+        P(fl["sizes"], C.c_int64), P(ex.final_writer, C.c_int32), P(fl["acc_mode"], C.c_int8))
 
 
 def execute(graph, platform, scheduler, model, host_in: np.ndarray, host_out: np.ndarray | None = None,
