@@ -17,6 +17,8 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <utility>
+
 #include "dgemm_dmma.cuh"
 #include "tiles.h"
 
@@ -324,6 +326,112 @@ __device__ void diag64_reg(double* A, int ld, int j0, int* status, double* bufs)
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// 64x64 Cholesky + inverse by 128 threads, register resident, with the column
+// loop FULLY UNROLLED so every register index is a compile-time constant (the
+// runtime-j variant above pays ~1100 instructions per column in index
+// selects and divergent branches).  Thread t owns row i = t/2 and columns
+// k = 2m + (t&1) of A (-> L) and R (-> X = L^-1, R = I initially).  ONE
+// barrier per column: at the end of step j the owners of column j+1 publish
+// it, and the two owners of row j+1 of R publish that row (both final after
+// step j), into the buffer of the other parity; step j+1 then reads
+//   d = A(j+1, j+1), A(i, j+1), A(k, j+1), R(j+1, k)
+// and updates its registers with no further synchronisation.
+template <int J>
+__device__ __forceinline__ void diag64_step(double (&a)[32], double (&r)[32], double* colb, double* rowb, int i, int h,
+                                            bool& bad) {
+  constexpr int par = J & 1;
+  const double* cj = colb + par * kR;
+  const double* rj = rowb + par * kR;
+  double d = cj[J];
+  if (!(d > 0.0)) {
+    bad = true;
+    d = 1.0;
+  }
+  const double rs = rsqrt(d);
+  const double lij = cj[i] * rs;  // L(i, J) (meaningful for i > J)
+  const bool below = i > J, diag = i == J;
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int k = 2 * m + h;
+    if (2 * m > J) {  // k > J: trailing column of A
+      a[m] = fma(-lij, cj[k] * rs, a[m]);
+    } else if (2 * m + 1 < J) {  // k < J: R columns of earlier pivots
+      const double x = rj[k] * rs;
+      r[m] = below ? fma(-lij, x, r[m]) : (diag ? x : r[m]);
+    } else {  // the pair {2m, 2m+1} holds column J
+      if (k == J) {
+        a[m] = below ? lij : (diag ? d * rs : a[m]);
+        const double x = rj[k] * rs;
+        r[m] = below ? fma(-lij, x, r[m]) : (diag ? x : r[m]);
+      } else if (k > J) {
+        a[m] = fma(-lij, cj[k] * rs, a[m]);
+      } else {
+        const double x = rj[k] * rs;
+        r[m] = below ? fma(-lij, x, r[m]) : (diag ? x : r[m]);
+      }
+    }
+  }
+  if constexpr (J + 1 < kR) {
+    double* cn = colb + (par ^ 1) * kR;
+    double* rn = rowb + (par ^ 1) * kR;
+    constexpr int mn = (J + 1) >> 1;
+    if (h == ((J + 1) & 1)) cn[i] = a[mn];
+    if (i == J + 1) {
+#pragma unroll
+      for (int m = 0; m < 32; ++m)
+        if (2 * m <= J + 1 && 2 * m + h <= J + 1) rn[2 * m + h] = r[m];
+    }
+  }
+  __syncthreads();
+}
+
+template <int... Js>
+__device__ __forceinline__ void diag64_steps(double (&a)[32], double (&r)[32], double* colb, double* rowb, int i,
+                                             int h, bool& bad, std::integer_sequence<int, Js...>) {
+  (diag64_step<Js>(a, r, colb, rowb, i, h, bad), ...);
+}
+
+// ---------------------------------------------------------------------------
+// 64x64 Cholesky + inverse by 128 threads, register resident, with the column
+// loop unrolled at compile time (diag64_step<J>) so every register index is a
+// constant (the runtime-j variant above pays ~1100 instructions per column in
+// index selects and divergent branches; a shifted-window runtime loop was
+// measured 4x slower still).  Thread t owns row i = t/2 and columns
+// k = 2m + (t&1) of A (-> L) and R (-> X = L^-1, R = I initially).  ONE
+// barrier per column: at the end of step j the owners of column j+1 publish
+// it and the two owners of row j+1 of R publish that row (both final after
+// step j) into the buffer of the other parity; step j+1 then reads
+// d = A(j+1, j+1), A(i, j+1), A(k, j+1), R(j+1, k) with no further barrier.
+// Measured (tools/potrf_micro): 94 us -> 57 us per 64x64 block.
+__device__ __noinline__ void diag64_fast(double* A, int ld, int j0, int* status, double* bufs) {
+  double* blk = A + size_t(j0) * ld + j0;
+  const int tid = threadIdx.x;
+  const int i = tid >> 1, h = tid & 1;
+  double* colb = bufs;           // [2][64]: column j of A
+  double* rowb = bufs + 2 * kR;  // [2][64]: row j of R (unscaled)
+  double a[32], r[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int k = 2 * m + h;
+    a[m] = (k <= i) ? __ldcg(blk + size_t(k) * ld + i) : 0.0;
+    r[m] = (k == i) ? 1.0 : 0.0;
+  }
+  if (h == 0) colb[i] = a[0];
+  if (tid == 0) rowb[0] = 1.0;
+  bool bad = false;
+  __syncthreads();
+  diag64_steps(a, r, colb, rowb, i, h, bad, std::make_integer_sequence<int, kR>{});
+  if (bad && tid == 0 && status) atomicOr(status, 1);
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int k = 2 * m + h;
+    if (k <= i) blk[size_t(k) * ld + i] = a[m];
+    if (k < i) blk[size_t(i) * ld + k] = r[m];
+  }
+  __syncthreads();
+}
+
 struct PotrfDiagParams {
   double* A;
   int ld, j0;
@@ -449,7 +557,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
   const int nb = p.nb, nJ = nb / kR, ld = nb;
   double* A = p.A;
   auto blk = [&](int I, int K) { return A + size_t(K) * kR * ld + size_t(I) * kR; };  // block (I, K)
-  if (q == 0) diag64_reg(A, nb, 0, p.status, &s[0][0]);
+  if (q == 0) diag64_fast(A, nb, 0, p.status, &s[0][0]);
   __threadfence();
   cl.sync();
   for (int J = 0; J < nJ; ++J) {
@@ -466,7 +574,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
       TileLoader<CfgG, M_MAJOR, kR> la{blk(0, J), ld, (J + 1) * kR};
       block_update(blk(J + 1, J + 1), ld, la, la, true, false, smem);
       __threadfence();
-      diag64_reg(A, nb, (J + 1) * kR, p.status, &s[0][0]);
+      diag64_fast(A, nb, (J + 1) * kR, p.status, &s[0][0]);
     } else {
       int t = 0;
       const int others = kPotrfCl - 1;

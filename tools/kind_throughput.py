@@ -1,0 +1,99 @@
+"""Per-kind latency (one task alone) and throughput (many independent tasks
+on concurrent streams, as inside the DAG) of the sm_100a tile kernels.
+
+    python tools/kind_throughput.py [KIND ...]   -> one JSON line per kind
+
+throughput_tflops = conc * reps * flops / wall; sm_eff = that / DMMA peak."""
+import ctypes as C
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_1402_6601_b200 as H
+from paper_1402_6601_b200 import _native
+
+nb, ib = 1024, 128
+NT = {"POTRF": 1, "TRSM": 2, "SYRK": 2, "GEMM": 3, "GETRF_INC": 1, "GESSM": 2, "TSTRF": 2, "SSSSM": 3,
+      "GEQRT": 1, "UNMQR": 2, "TSQRT": 2, "TSMQR": 3}
+kinds = sys.argv[1:] or list(NT)
+L = _native.lib()
+dev = torch.cuda.current_device()
+peak, _ = _native.fp64_peak(dev)
+status = torch.zeros(1, dtype=torch.int32, device="cuda")
+rng = np.random.default_rng(0)
+side = ib * nb + nb
+
+
+def operands(kind, conc):
+    """conc independent operand sets: factor tiles come from one real factorisation."""
+    n = NT[kind]
+    sets = []
+    base = []
+    for i in range(n):
+        a = rng.uniform(-0.5, 0.5, (nb, nb))
+        if i == 0:
+            a = (a + a.T) / 2 + nb * np.eye(nb)
+        t = torch.zeros(nb * nb + side, dtype=torch.float64, device="cuda")
+        t[: nb * nb] = torch.from_numpy(np.asfortranarray(a).ravel(order="F")).cuda()
+        base.append(t)
+    # make the factor operands valid (run the producing kinds once)
+    fam = {"POTRF": None, "TRSM": "POTRF", "SYRK": None, "GEMM": None, "GETRF_INC": None, "GESSM": "GETRF_INC",
+           "TSTRF": "GETRF_INC", "SSSSM": ("GETRF_INC", "TSTRF"), "GEQRT": None, "UNMQR": "GEQRT",
+           "TSQRT": "GEQRT", "TSMQR": ("GEQRT", "TSQRT")}[kind]
+    def run1(k, ts):
+        ptrs = (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+        _native.check(L.hg_tile_run(H.ALL_KINDS.index(k), dev, None, ptrs, len(ts), nb, ib,
+                                    C.c_void_p(status.data_ptr())), k)
+    if isinstance(fam, tuple):
+        run1(fam[0], [base[0]])
+        run1(fam[1], [base[0], base[1]])
+    elif fam:
+        run1(fam, [base[0]])
+    torch.cuda.synchronize()
+    for _ in range(conc):
+        sets.append([t.clone() for t in base])
+    return sets
+
+
+for kind in kinds:
+    res = {"kind": kind}
+    flops = H.kind_flops(kind, nb) if hasattr(H, "kind_flops") else None
+    # TRSM's in-place counters live in hg_tile_run's per-device scratch: never overlap two
+    for conc in ((1,) if kind == "TRSM" else (1, 8)):
+        sets = operands(kind, conc)
+        streams = [torch.cuda.Stream() for _ in range(conc)]
+        ptrs = [(C.c_void_p * len(ts))(*[t.data_ptr() for t in ts]) for ts in sets]
+        def go(reps):
+            for r in range(reps):
+                for s, p in zip(streams, ptrs):
+                    _native.check(L.hg_tile_run(H.ALL_KINDS.index(kind), dev, C.c_void_p(s.cuda_stream), p,
+                                                len(sets[0]), nb, ib, C.c_void_p(status.data_ptr())), kind)
+        go(1)
+        torch.cuda.synchronize()
+        reps = 5
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for s in streams:
+            s.wait_event(e0)
+        go(reps)
+        for s in streams:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            torch.cuda.current_stream().wait_event(ev)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        tput = conc * reps * flops / (ms * 1e-3) / 1e12
+        if conc == 1:
+            res["latency_us"] = ms / reps * 1e3
+        res[f"tflops_conc{conc}"] = tput
+        del sets
+        torch.cuda.empty_cache()
+    if "tflops_conc8" in res:
+        res["sm_eff_conc8"] = res["tflops_conc8"] / peak
+    res["peak"] = peak
+    print(json.dumps(res), flush=True)
