@@ -319,3 +319,26 @@ HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int
 }
 
 }  // namespace hg
+
+namespace hg {
+
+// Loads C(m0 + r, n0 + c) at every accumulator position (all loads issued
+// before any use, so the L2 latency is paid once, not once per element).
+template <class Cfg>
+HG_DEVICE void load_like_acc(double (&cv)[Cfg::FM][Cfg::FN][2], const double* __restrict__ C, int ldc, int m0,
+                             int n0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) {
+      const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t;
+      cv[i][j][0] = C[size_t(n0 + c) * ldc + m0 + r];
+      cv[i][j][1] = C[size_t(n0 + c + 1) * ldc + m0 + r];
+    }
+}
+
+}  // namespace hg

@@ -990,14 +990,30 @@ __global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) 
     auto at = [&](int code, int c) -> double* {
       return code >= 0 ? bot + size_t(c) * nb + code : top + size_t(c) * nb + ii + (-1 - code);
     };
-    for (int e = tid; e < nm * BN; e += G::THREADS) mvv[e] = *at(mv_src[e / BN], n0 + e % BN);
+    // gather every moved value before any is written; 8 loads in flight per thread
+    for (int e0 = tid; e0 < nm * BN; e0 += 8 * G::THREADS) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * G::THREADS;
+        v[u] = e < nm * BN ? *at(mv_src[e / BN], n0 + e % BN) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * G::THREADS;
+        if (e < nm * BN) mvv[e] = v[u];
+      }
+    }
     __syncthreads();
     for (int e = tid; e < nm * BN; e += G::THREADS) *at(mv_dst[e / BN], n0 + e % BN) = mvv[e];
     __syncthreads();
-    for (int e = tid; e < sb * BN; e += G::THREADS) {
-      const int c = e / sb, r = e % sb;
-      Ts[c * kLcLd + r] = top[size_t(n0 + c) * nb + ii + r];
+    // top rows -> smem with cp.async (16-byte chunks along the contiguous rows)
+    for (int e = tid; e < (sb / 2) * BN; e += G::THREADS) {
+      const int c = e / (sb / 2), r = (e % (sb / 2)) * 2;
+      cp_async16(Ts + c * kLcLd + r, top + size_t(n0 + c) * nb + ii + r);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     {  // top' = inv(L_uu) top
       double acc[G::FM][G::FN][2];

@@ -348,10 +348,18 @@ __global__ void __launch_bounds__(CfgQ::THREADS) k_qr_apply(QrApplyParams p) {
         TileLoader<CfgQ, K_MAJOR, kQrBN> lb{p.top, nb, n0};
         gemm_mainloop<CfgQ>(acc, ring, la, lb, ii, nb);
       }
-      for_each_acc<CfgQ>(acc, [&](int r, int c, double v) {
-        if (ts) v += p.top[size_t(n0 + c) * nb + ii + r];
-        W[c * kWld + r] = v;
-      });
+      if (ts) {  // W = top + V_B^T bot: top loads batched, not one L2 round trip per element
+        double tv[CfgQ::FM][CfgQ::FN][2];
+        load_like_acc<CfgQ>(tv, p.top + ii, nb, 0, n0);
+#pragma unroll
+        for (int i = 0; i < CfgQ::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < CfgQ::FN; ++j) {
+            acc[i][j][0] += tv[i][j][0];
+            acc[i][j][1] += tv[i][j][1];
+          }
+      }
+      for_each_acc<CfgQ>(acc, [&](int r, int c, double v) { W[c * kWld + r] = v; });
     }
     __syncthreads();
     // ---- W <- T^T W  (T^T(r, k) = T(k, r) at side[(ii + r)*ib + k])
@@ -361,15 +369,10 @@ __global__ void __launch_bounds__(CfgQ::THREADS) k_qr_apply(QrApplyParams p) {
       TileLoader<CfgQ, K_MAJOR, 128> la{p.side + size_t(ii) * ib, ib, 0};
       gemm_mainloop_bsmem<CfgQ>(acc, ring, la, W, kWld, 0, 128);
       for_each_acc<CfgQ>(acc, [&](int r, int c, double v) { W[c * kWld + r] = v; });
+      if (ts) sub_store<CfgQ>(acc, p.top + ii, nb, 0, n0);  // top -= W (all loads first)
     }
     __syncthreads();
-    // ---- C -= V W  (UNMQR rows [ii, nb))  |  top -= W; bot -= V_B W (TSMQR)
-    if (ts) {
-      for (int e = threadIdx.x; e < 128 * kQrBN; e += CfgQ::THREADS) {
-        int c = e / 128, r = e % 128;
-        p.top[size_t(n0 + c) * nb + ii + r] -= W[c * kWld + r];
-      }
-    }
+    // ---- C -= V W  (UNMQR rows [ii, nb))  |  bot -= V_B W (TSMQR)
     {
       VLoader<CfgQ, M_MAJOR, 128> la{Vp, nb, 0, ii, ts ? 0 : 1};
       gemm_sub_chunks_bsmem<CfgQ>(ring, la, W, kWld, 128, ts ? 0 : ii, nb, ts ? p.bot : p.top, nb, n0);
