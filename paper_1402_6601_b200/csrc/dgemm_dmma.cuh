@@ -167,6 +167,30 @@ HG_DEVICE void zero_acc(double (&acc)[Cfg::FM][Cfg::FN][2]) {
     for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 }
 
+// (i, j, row, col) of every accumulator fragment pair of this thread
+template <class Cfg, class F>
+HG_DEVICE void for_each_acc_ij(F&& f) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) f(i, j, wm + i * 8 + g, wn + j * 8 + 2 * t);
+}
+
+// Loads C(m0 + r, n0 + c) at every accumulator position (all loads issued
+// before any use, so the L2 latency is paid once, not once per element).
+template <class Cfg>
+HG_DEVICE void load_like_acc(double (&cv)[Cfg::FM][Cfg::FN][2], const double* __restrict__ C, int ldc, int m0,
+                             int n0) {
+  for_each_acc_ij<Cfg>([&](int i, int j, int r, int c) {
+    cv[i][j][0] = C[size_t(n0 + c) * ldc + m0 + r];
+    cv[i][j][1] = C[size_t(n0 + c + 1) * ldc + m0 + r];
+  });
+}
+
 }  // namespace hg
 
 namespace hg {
@@ -265,7 +289,7 @@ namespace hg {
 // never drains between chunks, only the per-chunk epilogue interrupts the
 // DMMAs (the trailing updates of GESSM / SSSSM / UNMQR / TSMQR, K = ib).
 // LdA exposes a mutable row origin r0.
-template <class Cfg, class LdA>
+template <class Cfg, class LdA, bool PREFETCH_C = true>
 HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int ldsb, int K, int m_begin,
                                      int m_end, double* __restrict__ C, int ldc, int n0) {
   constexpr int LA = LdA::layout;
@@ -289,8 +313,10 @@ HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int
     cp_async_commit();
   }
   double acc[Cfg::FM][Cfg::FN][2];
+  double cv[Cfg::FM][Cfg::FN][2];  // this chunk's C, loaded while its k-slabs run
   zero_acc<Cfg>(acc);
   for (int it = 0; it < total; ++it) {
+    if (PREFETCH_C && it % nk == 0) load_like_acc<Cfg>(cv, C, ldc, m_begin + (it / nk) * Cfg::BM, n0);
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     if (it + STAGES - 1 < total) load(it + STAGES - 1);
@@ -310,35 +336,17 @@ HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int
         for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     if (it % nk == nk - 1) {
-      sub_store<Cfg>(acc, C, ldc, m_begin + (it / nk) * Cfg::BM, n0);
+      const int m0 = m_begin + (it / nk) * Cfg::BM;
+      if (!PREFETCH_C) load_like_acc<Cfg>(cv, C, ldc, m0, n0);
+      for_each_acc_ij<Cfg>([&](int i, int j, int r, int c) {
+        C[size_t(n0 + c) * ldc + m0 + r] = cv[i][j][0] - acc[i][j][0];
+        C[size_t(n0 + c + 1) * ldc + m0 + r] = cv[i][j][1] - acc[i][j][1];
+      });
       zero_acc<Cfg>(acc);
     }
   }
   cp_async_wait<0>();
   __syncthreads();
-}
-
-}  // namespace hg
-
-namespace hg {
-
-// Loads C(m0 + r, n0 + c) at every accumulator position (all loads issued
-// before any use, so the L2 latency is paid once, not once per element).
-template <class Cfg>
-HG_DEVICE void load_like_acc(double (&cv)[Cfg::FM][Cfg::FN][2], const double* __restrict__ C, int ldc, int m0,
-                             int n0) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
-  const int wn = (warp / Cfg::WARPS_M) * Cfg::WN;
-  const int g = lane >> 2, t = lane & 3;
-#pragma unroll
-  for (int i = 0; i < Cfg::FM; ++i)
-#pragma unroll
-    for (int j = 0; j < Cfg::FN; ++j) {
-      const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t;
-      cv[i][j][0] = C[size_t(n0 + c) * ldc + m0 + r];
-      cv[i][j][1] = C[size_t(n0 + c + 1) * ldc + m0 + r];
-    }
 }
 
 }  // namespace hg

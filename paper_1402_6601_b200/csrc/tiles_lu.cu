@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) 
 }
 
 using CfgLS16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
-using CfgLS32 = GemmCfg<128, 32, 16, 32, 32, 3>;  // 4 warps
+using CfgLS32 = GemmCfg<128, 32, 16, 32, 16, 3>;  // 8 warps (32x16 warp tiles): 2 CTAs / SM -> 16 warps
 using CfgLS64 = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps
 
 template <class G>

@@ -276,7 +276,7 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
 
 // ---------------------------------------------------------------------------
 using CfgQ64 = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps; requires sb == 128
-using CfgQ32 = GemmCfg<128, 32, 16, 32, 32, 3>;  // 4 warps
+using CfgQ32 = GemmCfg<128, 32, 16, 32, 16, 3>;  // 8 warps (32x16 warp tiles)
 using CfgQ16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
 constexpr int kWld = kQrMaxSb + 4;  // W stored [n][k]
 
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(CfgQ::THREADS) k_qr_apply(QrApplyParams p) {
     // ---- C -= V W  (UNMQR rows [ii, nb))  |  bot -= V_B W (TSMQR)
     {
       VLoader<CfgQ, M_MAJOR, 128> la{Vp, nb, 0, ii, ts ? 0 : 1};
-      gemm_sub_chunks_bsmem<CfgQ>(ring, la, W, kWld, 128, ts ? 0 : ii, nb, ts ? p.bot : p.top, nb, n0);
+      gemm_sub_chunks_bsmem<CfgQ, decltype(la), false>(ring, la, W, kWld, 128, ts ? 0 : ii, nb, ts ? p.bot : p.top, nb, n0);
     }
     __syncthreads();
   }

@@ -63,7 +63,7 @@ for kind in kinds:
     res = {"kind": kind}
     flops = H.kind_flops(kind, nb) if hasattr(H, "kind_flops") else None
     # TRSM's in-place counters live in hg_tile_run's per-device scratch: never overlap two
-    for conc in ((1,) if kind == "TRSM" else (1, 8)):
+    for conc in ((1,) if kind == "TRSM" else tuple(int(c) for c in os.environ.get("HG_CONC", "1,8").split(","))):
         sets = operands(kind, conc)
         streams = [torch.cuda.Stream() for _ in range(conc)]
         ptrs = [(C.c_void_p * len(ts))(*[t.data_ptr() for t in ts]) for ts in sets]
@@ -93,7 +93,7 @@ for kind in kinds:
         res[f"tflops_conc{conc}"] = tput
         del sets
         torch.cuda.empty_cache()
-    if "tflops_conc8" in res:
+    if "tflops_conc8" in res and "peak" not in res:
         res["sm_eff_conc8"] = res["tflops_conc8"] / peak
     res["peak"] = peak
     print(json.dumps(res), flush=True)
