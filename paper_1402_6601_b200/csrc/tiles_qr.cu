@@ -146,14 +146,15 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
       const int c = tid % kQrMaxSb, half = tid / kQrMaxSb;
       if (c < sb) {
         const int rb = half * (R / 2), re = rb + R / 2;
-        double acc0 = 0.0, acc1 = 0.0;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains (FMA latency)
         if (c != jj) {
-          for (int r = rb; r < re; r += 2) {
-            acc0 = fma(vv[r], s[c * LD + r], acc0);
-            acc1 = fma(vv[r + 1], s[c * LD + r + 1], acc1);
+          const double* sc = s + c * LD;
+          for (int r = rb; r < re; r += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(vv[r + u], sc[r + u], acc[u]);
           }
         }
-        ph[half * kQrMaxSb + c] = acc0 + acc1;
+        ph[half * kQrMaxSb + c] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       }
     }
     __syncthreads();
@@ -191,7 +192,20 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
         else v = 0.0;
         if (v != 0.0) {
           const double tv = tau * v;
-          for (int c = jj + 1 + grp; c < sb; c += ngroup) s[c * LD + r] = fma(-tv, wv[c], s[c * LD + r]);
+          int c = jj + 1 + grp;
+          // 8 independent read-modify-writes in flight (a plain loop serialises each
+          // shared-memory store before the next load)
+          for (; c + 7 * ngroup < sb; c += 8 * ngroup) {
+            double x[8], w8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              x[u] = s[(c + u * ngroup) * LD + r];
+              w8[u] = wv[c + u * ngroup];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s[(c + u * ngroup) * LD + r] = fma(-tv, w8[u], x[u]);
+          }
+          for (; c < sb; c += ngroup) s[c * LD + r] = fma(-tv, wv[c], s[c * LD + r]);
         }
       }
     }
