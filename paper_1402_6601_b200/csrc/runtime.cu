@@ -600,9 +600,35 @@ static int build_graph(hg_exec* ex) {
       }
       deps.push_back(job_node[j]);
     }
+    // local predecessors first; a predecessor on another rank becomes a flag-wait
+    // node of THIS task that itself waits for the task's local dependencies, so it
+    // only spins once the task is otherwise ready (a root wait node per remote edge
+    // would keep thousands of 1-warp CTAs spinning from the start of the graph)
+    int n_remote = 0;
     for (int64_t q = ex->pred_ptr[t]; q < ex->pred_ptr[t + 1]; ++q) {
-      int rc = dep_task(ex->pred[q], node);
-      if (rc) return rc;
+      const int u = ex->pred[q];
+      if (ex->is_local(ex->task_node[u])) {
+        int rc = dep_task(u, node);
+        if (rc) return rc;
+      } else {
+        ++n_remote;
+      }
+    }
+    if (n_remote) {
+      std::sort(deps.begin(), deps.end());
+      deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+      std::vector<cudaGraphNode_t> local = deps;
+      HG_CUDA(cudaSetDevice(ex->dev[node - 1]));
+      for (int64_t q = ex->pred_ptr[t]; q < ex->pred_ptr[t + 1]; ++q) {
+        const int u = ex->pred[q];
+        const int pn = ex->task_node[u];
+        if (ex->is_local(pn)) continue;
+        cudaGraphNode_t w;
+        int rc = add_flag_kernel(ex->graph, &w, local.data(), local.size(), (const void*)hg::k_wait_flag,
+                                 hg::FlagParams{ex->task_flag(pn, u), ex->epoch_ptr(node)});
+        if (rc) return rc;
+        deps.push_back(w);
+      }
     }
     std::sort(deps.begin(), deps.end());  // a delivery job may also be in the wait list
     deps.erase(std::unique(deps.begin(), deps.end()), deps.end());

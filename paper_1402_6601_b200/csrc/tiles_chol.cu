@@ -432,6 +432,176 @@ __device__ __noinline__ void diag64_fast(double* A, int ld, int j0, int* status,
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// 64x64 Cholesky + inverse, BLOCKED (4 x 16-column blocks) so the serial
+// part is a 16-column warp leaf and everything else is DMMA:
+//   for J in 0..3:
+//     leaf (warp 0, registers + shuffles): L_JJ, T = L_JJ^-1      (16 serial columns)
+//     L(I,J) = A(I,J) T^T (I > J);  M(J,K) <- T M(J,K) (K < J), M(J,J) = T     (DMMA)
+//     A(I,K) -= L(I,J) L(K,J)^T (J < K <= I);  M(I,K) -= L(I,J) M(J,K) (K <= J)  (DMMA)
+// with M = L^-1 accumulated exactly as the cluster kernel does per 64-block.
+// The 64 serial columns of the unblocked variants (~1700 cycles each) become
+// 4 leaves of 16 columns plus 8 small DMMA products.
+constexpr int kBL = 68;  // smem column stride (conflict-free DMMA fragment loads)
+
+// C(8x8 tile at (r0, c0)) op= sum_k A(r0+i, k) * B(c0+j, k) over k in [0, K) (K % 4 == 0),
+// operands fetched by functors fa(row, k), fb(col, k).
+template <class FA, class FB>
+__device__ __forceinline__ void tile8_dmma(double& c0, double& c1, int K, FA&& fa, FB&& fb) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  for (int k0 = 0; k0 < K; k0 += 4) dmma_8x8x4(c0, c1, fa(g, k0 + t), fb(g, k0 + t));
+}
+
+// Warp-level 16x16 Cholesky + inverse: lanes 0..15 own the rows.  In: sA block (lower).
+// Out: L in sA (lower), T = L^-1 in sT[c*17 + r] (lower).  Returns false on a non-positive pivot.
+__device__ __forceinline__ bool leaf16(double* sA, int r0, double* sT) {
+  const int lane = threadIdx.x & 31;
+  const int i = lane & 15;
+  double a[16], r[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    a[k] = (k <= i) ? sA[(r0 + k) * kBL + r0 + i] : 0.0;
+    r[k] = (k == i) ? 1.0 : 0.0;
+  }
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    double d = __shfl_sync(0xffffffffu, a[j], j);
+    if (!(d > 0.0)) {
+      ok = false;
+      d = 1.0;
+    }
+    const double rs = rsqrt(d);
+    const double lij = a[j] * rs;  // L(i, j) for i > j
+    if (i > j) a[j] = lij;
+    else if (i == j) a[j] = d * rs;
+#pragma unroll
+    for (int k = j + 1; k < 16; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, a[j], k);  // L(k, j) (lane k, already scaled)
+      if (i >= k) a[k] = fma(-lij, lkj, a[k]);
+    }
+#pragma unroll
+    for (int k = 0; k <= j; ++k) {
+      const double xjk = __shfl_sync(0xffffffffu, r[k], j) * rs;  // X(j, k) = R(j, k) / L(j, j)
+      if (i > j) r[k] = fma(-lij, xjk, r[k]);
+      else if (i == j) r[k] = xjk;
+    }
+  }
+  if (lane < 16) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (k <= i) sA[(r0 + k) * kBL + r0 + i] = a[k];
+      sT[k * 17 + i] = (k <= i) ? r[k] : 0.0;
+    }
+  }
+  return ok;
+}
+
+__device__ __noinline__ void diag64_blocked(double* A, int ld, int j0, int* status, double* work) {
+  double* blk = A + size_t(j0) * ld + j0;
+  double* sA = work;               // [64][kBL]: A -> L, sA[c*kBL + r]
+  double* sM = work + kR * kBL;    // [64][kBL]: M = L^-1
+  double* sT = sM + kR * kBL;      // [16][17]: leaf inverse
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  constexpr int NW = CfgG::THREADS / 32;
+  for (int e = tid; e < kR * kR; e += CfgG::THREADS) {
+    const int c = e / kR, r = e % kR;
+    sA[c * kBL + r] = r >= c ? __ldcg(blk + size_t(c) * ld + r) : 0.0;
+    sM[c * kBL + r] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  bool ok = true;
+  for (int J = 0; J < 4; ++J) {
+    const int b0 = 16 * J;
+    if (warp == 0) ok = leaf16(sA, b0, sT) && ok;
+    __syncthreads();
+    // ---- L(I,J) = A(I,J) T^T for rows [b0+16, 64); M(J,K) <- T M(J,K), M(J,J) = T ----------
+    {
+      const int nr = (kR - b0 - 16) / 8;  // 8-row tiles below the block
+      const int n_panel = nr * 2;           // x 2 column tiles
+      const int n_mrow = 2 * (b0 / 8);      // M(J, K<J): 2 row tiles x b0/8 column tiles
+      double acc[4][2];
+      int tiles[4];
+      int nt = 0;
+      for (int w = warp; w < n_panel + n_mrow; w += NW) {
+        double c0 = 0.0, c1 = 0.0;
+        if (w < n_panel) {
+          const int r0 = b0 + 16 + (w >> 1) * 8, cc = (w & 1) * 8;
+          tile8_dmma(c0, c1, 16, [&](int gg, int k) { return sA[(b0 + k) * kBL + r0 + gg]; },
+                     [&](int gg, int k) { return sT[k * 17 + cc + gg]; });  // T^T(k, c) = T(c, k)
+        } else {
+          const int w2 = w - n_panel;
+          const int rr = (w2 & 1) * 8, c0m = (w2 >> 1) * 8;
+          tile8_dmma(c0, c1, 16, [&](int gg, int k) { return sT[k * 17 + rr + gg]; },           // T(r, k)
+                     [&](int gg, int k) { return sM[(c0m + gg) * kBL + b0 + k]; });         // M(b0+k, c)
+        }
+        acc[nt][0] = c0;
+        acc[nt][1] = c1;
+        tiles[nt++] = w;
+      }
+      __syncthreads();
+      for (int q2 = 0; q2 < nt; ++q2) {
+        const int w = tiles[q2];
+        if (w < n_panel) {
+          const int r0 = b0 + 16 + (w >> 1) * 8, cc = b0 + (w & 1) * 8;
+          sA[(cc + 2 * t) * kBL + r0 + g] = acc[q2][0];
+          sA[(cc + 2 * t + 1) * kBL + r0 + g] = acc[q2][1];
+        } else {
+          const int w2 = w - n_panel;
+          const int rr = b0 + (w2 & 1) * 8, c0m = (w2 >> 1) * 8;
+          sM[(c0m + 2 * t) * kBL + rr + g] = acc[q2][0];
+          sM[(c0m + 2 * t + 1) * kBL + rr + g] = acc[q2][1];
+        }
+      }
+      // M(J,J) = T
+      for (int e = tid; e < 256; e += CfgG::THREADS) {
+        const int c = e >> 4, r = e & 15;
+        sM[(b0 + c) * kBL + b0 + r] = sT[c * 17 + r];
+      }
+    }
+    __syncthreads();
+    if (J == 3) break;
+    // ---- trailing: A(r,c) -= L(r,J) L(c,J)^T (c <= r, both >= b0+16); M(r,K) -= L(r,J) M(J,K) --------
+    {
+      const int m0 = b0 + 16;
+      const int nt8 = (kR - m0) / 8;
+      const int n_tr = nt8 * (nt8 + 1) / 2;  // lower tiles incl. diagonal tiles
+      const int n_mu = nt8 * ((b0 + 16) / 8);
+      // outputs (columns / rows >= m0) are disjoint from the inputs (block column / row J): write in place
+      for (int w = warp; w < n_tr + n_mu; w += NW) {
+        double c0 = 0.0, c1 = 0.0;
+        if (w < n_tr) {
+          int ti = 0, rem = w;
+          while (rem > ti) { rem -= ti + 1; ++ti; }  // (ti, tj = rem), tj <= ti
+          const int r0 = m0 + ti * 8, cl0 = m0 + rem * 8;
+          tile8_dmma(c0, c1, 16, [&](int gg, int k) { return sA[(b0 + k) * kBL + r0 + gg]; },
+                     [&](int gg, int k) { return sA[(b0 + k) * kBL + cl0 + gg]; });
+          sA[(cl0 + 2 * t) * kBL + r0 + g] -= c0;
+          sA[(cl0 + 2 * t + 1) * kBL + r0 + g] -= c1;
+        } else {
+          const int w2 = w - n_tr;
+          const int ti = w2 % nt8, tj = w2 / nt8;
+          const int r0 = m0 + ti * 8, cm = tj * 8;
+          tile8_dmma(c0, c1, 16, [&](int gg, int k) { return sA[(b0 + k) * kBL + r0 + gg]; },  // L(r, b0+k)
+                     [&](int gg, int k) { return sM[(cm + gg) * kBL + b0 + k]; });           // M(b0+k, c)
+          sM[(cm + 2 * t) * kBL + r0 + g] -= c0;
+          sM[(cm + 2 * t + 1) * kBL + r0 + g] -= c1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!ok && tid == 0 && status) atomicOr(status, 1);
+  // L (lower) and M^T into the strict upper triangle: (row c, col i) <- M(i, c), c < i
+  for (int e = tid; e < kR * kR; e += CfgG::THREADS) {
+    const int c = e / kR, r = e % kR;
+    if (r >= c) blk[size_t(c) * ld + r] = sA[c * kBL + r];
+    else blk[size_t(c) * ld + r] = sM[r * kBL + c];
+  }
+  __syncthreads();
+}
+
 struct PotrfDiagParams {
   double* A;
   int ld, j0;
@@ -557,7 +727,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
   const int nb = p.nb, nJ = nb / kR, ld = nb;
   double* A = p.A;
   auto blk = [&](int I, int K) { return A + size_t(K) * kR * ld + size_t(I) * kR; };  // block (I, K)
-  if (q == 0) diag64_fast(A, nb, 0, p.status, &s[0][0]);
+  if (q == 0) diag64_blocked(A, nb, 0, p.status, &s[0][0]);
   __threadfence();
   cl.sync();
   for (int J = 0; J < nJ; ++J) {
@@ -574,7 +744,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
       TileLoader<CfgG, M_MAJOR, kR> la{blk(0, J), ld, (J + 1) * kR};
       block_update(blk(J + 1, J + 1), ld, la, la, true, false, smem);
       __threadfence();
-      diag64_fast(A, nb, (J + 1) * kR, p.status, &s[0][0]);
+      diag64_blocked(A, nb, (J + 1) * kR, p.status, &s[0][0]);
     } else {
       int t = 0;
       const int others = kPotrfCl - 1;

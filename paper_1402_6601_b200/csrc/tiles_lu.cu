@@ -840,22 +840,33 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
     //   TSTRF: dst A rows in my range (src: U rows, global); CTA 0 also the dst U rows
     const int ncol_out = SB - W;
     auto out_col = [&](int k) { return k < c0 ? k : k + W; };
-    for (int m = 0; m < nm; ++m) {
-      const int d = mvd[m], sidx = mvs[m];
-      const bool d_top = d < 0;
-      const bool writer = d_top ? (q == 0) : (d >= row0 && d < row0 + R);
-      if (!writer) continue;
-      if (!ts) {
-        const double* src = cl.map_shared_rank(Ps, sidx / R) + (sidx % R);
-        for (int k = tid; k < ncol_out; k += kSpThreads) stg[m * SB + k] = src[out_col(k) * LDP];
-      } else {
-        for (int c = cR + tid; c < SB; c += kSpThreads) {
-          double v;
-          if (sidx < 0) v = __ldcg(p.U + size_t(ii + c) * nb + ii + c0 + (-1 - sidx));
-          else v = cl.map_shared_rank(Ps, sidx / R)[c * LDP + (sidx % R)];
-          stg[m * SB + c] = v;
+    // (every thread handles one column k < 128 of every move: all remote loads of
+    // the 2W possible moves are issued before any store, so the DSMEM / L2
+    // latency is paid once per sub-panel, not once per move)
+    {
+      double v[2 * W];
+#pragma unroll
+      for (int m = 0; m < 2 * W; ++m) {
+        v[m] = 0.0;
+        if (m < nm) {
+          const int d = mvd[m], sidx = mvs[m];
+          const bool writer = d < 0 ? (q == 0) : (d >= row0 && d < row0 + R);
+          if (writer) {
+            if (!ts) {
+              if (tid < ncol_out) v[m] = cl.map_shared_rank(Ps, sidx / R)[out_col(tid) * LDP + (sidx % R)];
+            } else {
+              const int c = cR + tid;
+              if (c < SB)
+                v[m] = sidx < 0 ? __ldcg(p.U + size_t(ii + c) * nb + ii + c0 + (-1 - sidx))
+                                : cl.map_shared_rank(Ps, sidx / R)[c * LDP + (sidx % R)];
+            }
+          }
         }
       }
+      const int col = ts ? cR + tid : tid;
+#pragma unroll
+      for (int m = 0; m < 2 * W; ++m)
+        if (m < nm && col < SB) stg[m * SB + col] = v[m];
     }
     cl.sync();
     for (int m = 0; m < nm; ++m) {
@@ -864,20 +875,22 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
       const bool writer = d_top ? (q == 0) : (d >= row0 && d < row0 + R);
       if (!writer) continue;
       if (!ts) {
-        for (int k = tid; k < ncol_out; k += kSpThreads) Ps[out_col(k) * LDP + (d - row0)] = stg[m * SB + k];
+        if (tid < ncol_out) Ps[out_col(tid) * LDP + (d - row0)] = stg[m * SB + tid];
       } else if (d_top) {
-        for (int c = cR + tid; c < SB; c += kSpThreads) p.U[size_t(ii + c) * nb + ii + c0 + (-1 - d)] = stg[m * SB + c];
+        const int c = cR + tid;
+        if (c < SB) p.U[size_t(ii + c) * nb + ii + c0 + (-1 - d)] = stg[m * SB + c];
       } else {
-        for (int c = cR + tid; c < SB; c += kSpThreads) Ps[c * LDP + (d - row0)] = stg[m * SB + c];
+        const int c = cR + tid;
+        if (c < SB) Ps[c * LDP + (d - row0)] = stg[m * SB + c];
       }
     }
-    __threadfence();
     __syncthreads();
     if (cR >= SB) break;
     // ---- U: right-hand columns: U12 = L11^-1 A12, A22 -= L21 U12 --------------------------
     const int nR = SB - cR;
+    // (no cluster barrier needed here: the owner reads only rows it wrote itself
+    // and dL entries published before the phase-S barrier)
     const int owner = ts ? 0 : (ii + c0) / R;
-    cl.sync();  // moved rows / U rows visible everywhere
     if (q == owner) {
       // forward substitution, one thread per right-hand column
       for (int c = tid; c < nR; c += kSpThreads) {
@@ -899,12 +912,13 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
       }
     }
     cl.sync();
-    if (q != owner) {
+    if (q != owner && tid < nR) {  // thread c copies column c of U12 (16 loads in flight)
       const double* src = cl.map_shared_rank(U12, owner);
-      for (int e = tid; e < W * nR; e += kSpThreads) {
-        const int v = e / nR, c = e % nR;
-        U12[v * SB + c] = src[v * SB + c];
-      }
+      double v[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[w] = src[w * SB + tid];
+#pragma unroll
+      for (int w = 0; w < W; ++w) U12[w * SB + tid] = v[w];
     }
     __syncthreads();
     if (live && (ts || gr >= ii + cR)) {

@@ -15,7 +15,7 @@ __global__ void __launch_bounds__(128) k_time_diag(double* A, int ld, long long*
   auto iv = reinterpret_cast<double(*)[kR + 1]>(sm + kR * (kR + 1));
   auto tm = reinterpret_cast<double(*)[33]>(sm + 2 * kR * (kR + 1));
   long long t0 = clock64();
-  for (int r = 0; r < reps; ++r) diag64_fast(A, ld, 0, st, &s[0][0]);
+  for (int r = 0; r < reps; ++r) diag64_blocked(A, ld, 0, st, &s[0][0]);
   long long t1 = clock64();
   if (threadIdx.x == 0) out[0] = (t1 - t0) / reps;
 }
@@ -75,7 +75,7 @@ int main() {
   cudaMalloc(&out, 8 * 8);
   cudaMalloc(&st, 4);
   cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
-  const int smem = (2 * kR * (kR + 1) + 32 * 33) * 8;
+  const int smem = (2 * kR * kBL + 16 * 17) * 8;
   cudaFuncSetAttribute(k_time_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_time_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_time_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
