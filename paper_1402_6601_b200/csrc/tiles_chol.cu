@@ -452,8 +452,40 @@ __device__ __forceinline__ void tile8_dmma(double& c0, double& c1, int K, FA&& f
   for (int k0 = 0; k0 < K; k0 += 4) dmma_8x8x4(c0, c1, fa(g, k0 + t), fb(g, k0 + t));
 }
 
-// Warp-level 16x16 Cholesky + inverse: lanes 0..15 own the rows.  In: sA block (lower).
-// Out: L in sA (lower), T = L^-1 in sT[c*17 + r] (lower).  Returns false on a non-positive pivot.
+// One column step of the warp leaf (J compile-time, so a[] / r[] stay in registers).
+template <int J>
+__device__ __forceinline__ void leaf16_step(double (&a)[16], double (&r)[16], int i, bool& ok) {
+  double d = __shfl_sync(0xffffffffu, a[J], J);
+  if (!(d > 0.0)) {
+    ok = false;
+    d = 1.0;
+  }
+  const double rs = rsqrt(d);
+  const double lij = a[J] * rs;  // L(i, J) for i > J
+  if (i > J) a[J] = lij;
+  else if (i == J) a[J] = d * rs;
+#pragma unroll
+  for (int k = J + 1; k < 16; ++k) {
+    const double lkj = __shfl_sync(0xffffffffu, a[J], k);  // L(k, J) (lane k, already scaled)
+    if (i >= k) a[k] = fma(-lij, lkj, a[k]);
+  }
+#pragma unroll
+  for (int k = 0; k <= J; ++k) {
+    const double xjk = __shfl_sync(0xffffffffu, r[k], J) * rs;  // X(J, k) = R(J, k) / L(J, J)
+    if (i > J) r[k] = fma(-lij, xjk, r[k]);
+    else if (i == J) r[k] = xjk;
+  }
+}
+
+template <int... Js>
+__device__ __forceinline__ void leaf16_steps(double (&a)[16], double (&r)[16], int i, bool& ok,
+                                             std::integer_sequence<int, Js...>) {
+  (leaf16_step<Js>(a, r, i, ok), ...);
+}
+
+// Warp-level 16x16 Cholesky + inverse: lanes 0..15 own the rows (16..31 mirror them).
+// In: sA block (lower).  Out: L in sA (lower), T = L^-1 in sT[c*17 + r] (lower).
+// Returns false on a non-positive pivot.
 __device__ __forceinline__ bool leaf16(double* sA, int r0, double* sT) {
   const int lane = threadIdx.x & 31;
   const int i = lane & 15;
@@ -464,29 +496,7 @@ __device__ __forceinline__ bool leaf16(double* sA, int r0, double* sT) {
     r[k] = (k == i) ? 1.0 : 0.0;
   }
   bool ok = true;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    double d = __shfl_sync(0xffffffffu, a[j], j);
-    if (!(d > 0.0)) {
-      ok = false;
-      d = 1.0;
-    }
-    const double rs = rsqrt(d);
-    const double lij = a[j] * rs;  // L(i, j) for i > j
-    if (i > j) a[j] = lij;
-    else if (i == j) a[j] = d * rs;
-#pragma unroll
-    for (int k = j + 1; k < 16; ++k) {
-      const double lkj = __shfl_sync(0xffffffffu, a[j], k);  // L(k, j) (lane k, already scaled)
-      if (i >= k) a[k] = fma(-lij, lkj, a[k]);
-    }
-#pragma unroll
-    for (int k = 0; k <= j; ++k) {
-      const double xjk = __shfl_sync(0xffffffffu, r[k], j) * rs;  // X(j, k) = R(j, k) / L(j, j)
-      if (i > j) r[k] = fma(-lij, xjk, r[k]);
-      else if (i == j) r[k] = xjk;
-    }
-  }
+  leaf16_steps(a, r, i, ok, std::make_integer_sequence<int, 16>{});
   if (lane < 16) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
@@ -505,11 +515,18 @@ __device__ __noinline__ void diag64_blocked(double* A, int ld, int j0, int* stat
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   constexpr int NW = CfgG::THREADS / 32;
+  // the whole 64x64 block with cp.async (16-byte chunks of a column), so all the
+  // L2 round trips overlap; the strict upper part is never read as L
+  for (int e = tid; e < kR * (kR / 2); e += CfgG::THREADS) {
+    const int c = e / (kR / 2), r = (e % (kR / 2)) * 2;
+    cp_async16(sA + c * kBL + r, blk + size_t(c) * ld + r);
+  }
+  cp_async_commit();
   for (int e = tid; e < kR * kR; e += CfgG::THREADS) {
     const int c = e / kR, r = e % kR;
-    sA[c * kBL + r] = r >= c ? __ldcg(blk + size_t(c) * ld + r) : 0.0;
     sM[c * kBL + r] = (r == c) ? 1.0 : 0.0;
   }
+  cp_async_wait<0>();
   __syncthreads();
   bool ok = true;
   for (int J = 0; J < 4; ++J) {

@@ -35,6 +35,19 @@ __global__ void __launch_bounds__(128) k_time_leaf(double* A, int ld, long long*
   if (threadIdx.x == 0) out[1] = (t1 - t0) / reps;
 }
 
+__global__ void __launch_bounds__(128) k_time_leaf16(double* A, int ld, long long* out, int reps, int* st) {
+  extern __shared__ double sm[];
+  for (int e = threadIdx.x; e < kR * kBL; e += 128) sm[e] = (e % kBL == e / kBL) ? 64.0 : 0.001;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    if (threadIdx.x < 32) leaf16(sm, 0, sm + 2 * kR * kBL);
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[5] = (t1 - t0) / reps;
+}
+
 __global__ void __launch_bounds__(128) k_time_update(double* A, int ld, long long* out, int reps) {
   extern __shared__ double sm[];
   TileLoader<CfgG, M_MAJOR, kR> la{A, ld, 64};
@@ -83,6 +96,8 @@ int main() {
   cudaFuncSetAttribute(k_time_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   k_time_diag<<<1, 128, smem>>>(A, nb, out, 20, st);
   k_time_leaf<<<1, 128, smem>>>(A, nb, out, 20, st);
+  cudaFuncSetAttribute(k_time_leaf16, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_time_leaf16<<<1, 128, smem>>>(A, nb, out, 20, st);
   k_time_update<<<1, 128, 100000>>>(A, nb, out, 50);
   k_time_apply<<<1, 128, 100000>>>(A, nb, out, 50);
   k_time_cluster<<<16, 128>>>(out, 200);
@@ -93,8 +108,8 @@ int main() {
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   double mhz = clk / 1000.0;
   printf("{\"err\":\"%s\",\"mhz\":%.0f,\"diag64_cycles\":%lld,\"leaf32_cycles\":%lld,\"block_update_cycles\":%lld,"
-         "\"apply_inv_cycles\":%lld,\"cluster_sync_cycles\":%lld}\n",
-         cudaGetErrorString(e), mhz, r[0], r[1], r[2], r[3], r[4]);
+         "\"apply_inv_cycles\":%lld,\"cluster_sync_cycles\":%lld,\"leaf16_cycles\":%lld}\n",
+         cudaGetErrorString(e), mhz, r[0], r[1], r[2], r[3], r[4], r[5]);
   printf("{\"diag64_us\":%.2f,\"leaf32_us\":%.2f,\"block_update_us\":%.2f,\"apply_inv_us\":%.2f,\"cluster_sync_us\":%.3f}\n",
          r[0] / mhz, r[1] / mhz, r[2] / mhz, r[3] / mhz, r[4] / mhz);
   return 0;
