@@ -18,8 +18,10 @@ namespace hg {
 //   A (8x4, row):  a = A[g][t]
 //   B (4x8, col):  b = B[t][g]
 //   C (8x8):       c0 = C[g][2t], c1 = C[g][2t+1]
+// (not volatile: a pure function of its operands, so the compiler may hoist the
+// next k-step's fragment loads above it)
 HG_DEVICE void dmma_8x8x4(double& c0, double& c1, double a, double b) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
       "{%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c0), "+d"(c1)
