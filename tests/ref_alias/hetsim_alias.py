@@ -10,8 +10,8 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 import paper_1402_6601_b200 as _pkg  # noqa: E402
-from paper_1402_6601_b200 import graph, kernels, perfmodel, platform, sched, sim  # noqa: E402,F401
+from paper_1402_6601_b200 import cli, graph, kernels, perfmodel, platform, sched, sim  # noqa: E402,F401
 
 sys.modules["hetsim"] = _pkg
-for _name in ("graph", "kernels", "perfmodel", "platform", "sched", "sim"):
+for _name in ("cli", "graph", "kernels", "perfmodel", "platform", "sched", "sim"):
     sys.modules["hetsim." + _name] = getattr(_pkg, _name)
