@@ -915,6 +915,19 @@ bool init_qr_attributes() {
   return true;
 }
 
+// materialize_t (kernels.py:188-211): the T factor the panel left in the tile's side
+// area is also written to the task's separate T block, so the DAG's T data block
+// holds what the reference models it to hold
+struct CopyParams {
+  double* dst;
+  const double* src;
+  long long n;
+};
+__global__ void k_copy_doubles(CopyParams p) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.n; i += (long long)gridDim.x * blockDim.x)
+    p.dst[i] = p.src[i];
+}
+
 bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out) {
   const int nb = o.nb, ib = o.ib;
   if (nb % 128 != 0 || nb > 1024 || ib != 128) {
@@ -971,6 +984,13 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
         if (P + 1 < np)
           push_apply(QrApplyParams{A, ts ? side(1) : side(0), ts ? o.t[0] : A, ts ? A : nullptr, nb, ib, P, P + 1,
                                    (P + 1) * ib, ts ? QR_TSQRT : QR_GEQRT}, 16);
+      }
+      const int t_idx = ts ? 2 : 1;  // materialized T block (GEQRT: kk, T; TSQRT: kk, ik, T)
+      if (o.n_t > t_idx) {
+        LaunchDesc d;
+        d.set((const void*)k_copy_doubles, dim3(64), dim3(256), 0,
+              CopyParams{o.t[t_idx], ts ? side(1) : side(0), (long long)ib * nb});
+        out.push_back(d);
       }
       return true;
     }

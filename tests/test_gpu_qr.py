@@ -112,3 +112,39 @@ def test_qr_planned_factorization(k, devices):
     assert _rel(R, LQ.qr_r(T, lay)) < TOL
     QtA = LQ.qr_apply_qt(gt, gs, lay, A)
     assert np.linalg.norm(QtA - R) / np.linalg.norm(A) < 1e-13
+
+
+def test_qr_materialize_t_planned():
+    """gen_qr(materialize_t=True) (kernels.py:171-212): the T blocks are DAG data of
+    their own (transferred and accounted like tiles); after the run each holds its
+    panel's T factor, and the factor matches the run without materialized T."""
+    import math
+
+    n, b, ib = 2048, 512, 128
+    outs = {}
+    for mt in (False, True):
+        g = H.gen_qr(n // b, b, ib, materialize_t=mt)
+        plat = H.build_platform(2, 2, 2, link_bandwidth=7.7e11, link_latency=3e-6, switch_cap=math.inf, p2p=True)
+        plan = H.make_plan(g, plat, H.make_scheduler("dada", alpha=0.5, cp=True), H.PerfModel(H.default_timing_table(b, ib)))
+        A = O.general_matrix(n, 6)
+        img = runtime.to_tile_major(A, g)
+        out = np.zeros_like(img)
+        sd = g.layout.side_doubles
+        side_out = np.zeros(len(g.data) * sd)
+        ex = runtime.Executor(g, plat, plan, img, out, devices=[0, 0], host_side_out=side_out)
+        st = ex.run()
+        ex.close()
+        assert st.bytes_h2d == plan.bytes_h2d and st.bytes_d2d == plan.bytes_d2d
+        outs[mt] = (g, out, side_out)
+    g1, out1, _ = outs[True]
+    g0, out0, _ = outs[False]
+    f1, f0 = runtime.from_tile_major(out1, g1), runtime.from_tile_major(out0, g0)
+    assert np.abs(f1 - f0).max() / np.abs(f0).max() < 1e-12
+    offs = np.cumsum([0] + [s // 8 for s in g1.sizes])
+    sd = g1.layout.side_doubles
+    lay = g1.layout
+    tile_of = {ij: d for d, ij in lay.tiles.items()}
+    for d, (i, j) in lay.tfactors.items():
+        tblk = out1[offs[d]:offs[d + 1]]
+        side = outs[True][2][tile_of[(i, j)] * sd: tile_of[(i, j)] * sd + ib * b]
+        assert np.array_equal(tblk, side), (i, j)
