@@ -224,6 +224,12 @@ int hg_exec_destroy(hg_exec* ex);
  * ---------------------------------------------------------------------- */
 int hg_tile_run(int32_t kind, int32_t device, void* stream, double* const* t, int32_t n_t,
                 int32_t nb, int32_t ib, int32_t* status_dev);
+/* the same with caller-owned scratch (hg_task_scratch_ints(kind, nb, ib) ints on the device,
+ * zeroed once): independent tasks may then run concurrently on different streams
+ * (the online executor, paper_1402_6601_b200/online.py) */
+int hg_tile_run_scratch(int32_t kind, int32_t device, void* stream, double* const* t, int32_t n_t,
+                        int32_t nb, int32_t ib, int32_t* status_dev, int32_t* scratch_dev);
+int hg_task_scratch_ints(int32_t kind, int32_t nb, int32_t ib);
 
 /* FP64 roofline denominator: DMMA (mma.sync m8n8k4 f64) throughput of a
  * register-only kernel filling every SM, in TFLOP/s (MEASURED_PEAKS.json has

@@ -84,7 +84,8 @@ class ExecStats(C.Structure):
 EXPORTS = ("hg_last_error", "hg_abi_version", "hg_device_count", "hg_plan_build", "hg_plan_free",
            "hg_pysum", "hg_exec_create", "hg_exec_run", "hg_exec_read_block", "hg_exec_destroy",
            "hg_tile_run", "hg_exec_launch", "hg_exec_wait", "hg_exec_info", "hg_fp64_peak",
-           "hg_exec_ipc_handle", "hg_exec_ipc_open", "hg_exec_build", "hg_exec_partition")
+           "hg_exec_ipc_handle", "hg_exec_ipc_open", "hg_exec_build", "hg_exec_partition",
+           "hg_tile_run_scratch", "hg_task_scratch_ints")
 
 _lib = None
 
@@ -116,6 +117,9 @@ def lib():
     L.hg_exec_destroy.argtypes = [C.c_void_p]
     L.hg_tile_run.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p), C.c_int32,
                               C.c_int32, C.c_int32, C.c_void_p]
+    L.hg_tile_run_scratch.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p), C.c_int32,
+                                      C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+    L.hg_task_scratch_ints.argtypes = [C.c_int32, C.c_int32, C.c_int32]
     L.hg_exec_launch.argtypes = [C.c_void_p, C.c_void_p]
     L.hg_exec_wait.argtypes = [C.c_void_p]
     L.hg_exec_info.argtypes = [C.c_void_p, C.POINTER(ExecStats)]

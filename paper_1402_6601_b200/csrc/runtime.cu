@@ -163,6 +163,43 @@ int hg_tile_run(int32_t kind, int32_t device, void* stream, double* const* t, in
   return HG_OK;
 }
 
+// Same as hg_tile_run with caller-owned per-task scratch (hg_task_scratch_ints
+// ints, zeroed once, self-consistent across runs), so independent tasks may run
+// concurrently on different streams (the online executor).
+int hg_tile_run_scratch(int32_t kind, int32_t device, void* stream, double* const* t, int32_t n_t, int32_t nb,
+                        int32_t ib, int32_t* status_dev, int32_t* scratch_dev) {
+  if (n_t < 1 || n_t > 4 || t == nullptr) {
+    set_error("hg_tile_run_scratch: need 1..4 tile pointers");
+    return HG_EINVAL;
+  }
+  HG_CUDA(cudaSetDevice(device));
+  int rc = ensure_attributes(device);
+  if (rc) return rc;
+  TaskOperands ops;
+  for (int i = 0; i < n_t; ++i) ops.t[i] = t[i];
+  ops.n_t = n_t;
+  ops.nb = nb;
+  ops.ib = ib;
+  ops.status = status_dev;
+  if (task_scratch_ints(kind, nb, ib) > 0) {
+    if (!scratch_dev) {
+      set_error("hg_tile_run_scratch: kind %d needs %d scratch ints", kind, task_scratch_ints(kind, nb, ib));
+      return HG_EINVAL;
+    }
+    ops.scratch = scratch_dev;
+  }
+  std::vector<LaunchDesc> launches;
+  if (!build_task_launches(kind, ops, launches)) return HG_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (auto& d : launches) {
+    void* args[1] = {d.params};
+    HG_CUDA(cudaLaunchKernel(d.func, d.grid, d.block, args, d.smem, s));
+  }
+  return HG_OK;
+}
+
+int hg_task_scratch_ints(int32_t kind, int32_t nb, int32_t ib) { return task_scratch_ints(kind, nb, ib); }
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
