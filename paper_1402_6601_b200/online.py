@@ -34,6 +34,7 @@ version, completed).
 from __future__ import annotations
 
 import ctypes as C
+import random
 import time
 from collections import deque
 from dataclasses import dataclass
@@ -58,12 +59,15 @@ class OnlineReport:
     sched_seconds: float       # host time spent inside scheduler.activate
     worker: np.ndarray         # task -> worker
     kernel_seconds: dict       # kind -> list of measured durations
+    steals_ok: int = 0
+    steals_failed: int = 0
 
 
 class OnlineExecutor:
     """Runs ``graph`` on the GPUs of ``platform`` (GPU-only, p2p) with online decisions."""
 
-    def __init__(self, graph, platform, scheduler, model, host_in: np.ndarray, devices=None, depth: int = 8):
+    def __init__(self, graph, platform, scheduler, model, host_in: np.ndarray, devices=None, depth: int = 8,
+                 seed: int = 0):
         import torch
 
         if platform.n_cpu_workers:
@@ -79,6 +83,7 @@ class OnlineExecutor:
         ndev = torch.cuda.device_count()
         self.devices = list(devices) if devices is not None else [g % max(1, ndev) for g in range(self.k)]
         self.depth = depth
+        self.seed = seed
         self.L = _native.lib()
         self.sizes = [s // 8 for s in graph.sizes]
         self.offs = np.cumsum([0] + self.sizes)
@@ -190,6 +195,22 @@ class OnlineExecutor:
             running[tid] = (w, si, e0, e1)
             placed[tid] = w
 
+        rng = random.Random(self.seed)
+        steals = [0, 0]  # ok, failed
+
+        def steal(thief):
+            # a worker with free streams and an empty queue takes the newest task of a
+            # random victim's queue (sim.py:219-233; the ws baseline, sched.py:434-452)
+            pool = [v for v in range(nw) if v != thief]
+            while pool:
+                victim = pool.pop(rng.randrange(len(pool)))
+                if queues[victim]:
+                    steals[0] += 1
+                    dispatch(thief, queues[victim].pop())
+                    return True
+                steals[1] += 1
+            return False
+
         def dispatch_round():
             moved = True
             while moved:
@@ -198,6 +219,10 @@ class OnlineExecutor:
                     if free_streams[w] and queues[w]:
                         dispatch(w, queues[w].popleft())
                         moved = True
+                if self.sched.steals:
+                    for w in range(nw):
+                        if free_streams[w] and not queues[w] and steal(w):
+                            moved = True
 
         activate([t for t in range(n) if preds_left[t] == 0], None)
         dispatch_round()
@@ -240,7 +265,8 @@ class OnlineExecutor:
         from .sim import flops_of
 
         fl = flops_of(g.layout.family, g.layout.n)
-        return OnlineReport(span, fl / span / 1e9, bytes_h2d, bytes_d2d, n_act, sched_time, placed, measured)
+        return OnlineReport(span, fl / span / 1e9, bytes_h2d, bytes_d2d, n_act, sched_time, placed, measured,
+                            steals[0], steals[1])
 
     def result_image(self) -> np.ndarray:
         """Final version of every block (from the GPU that holds it), tile-major like host_in."""
