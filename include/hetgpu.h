@@ -162,6 +162,8 @@ typedef struct hg_exec_plan {
   const int64_t* block_bytes; /* host image bytes per block (tile or T factor) */
   const int32_t* final_writer;/* last writer task per block, -1 = never written */
   const int8_t* acc_mode;     /* HG_ACCESS_* per access (CSR like acc_block) */
+  const int32_t* job_stage_job; /* host-staged route: the job whose first leg stages the block, or -1 */
+  int32_t p2p;                /* 0: every GPU->GPU job is host-staged (GPU->host->GPU, platform.py:117) */
 } hg_exec_plan;
 
 typedef struct hg_exec_opts {
@@ -177,6 +179,8 @@ typedef struct hg_exec_opts {
                                  hg_exec_ipc_open, then hg_exec_build */
   const double* task_weight;  /* optional [n_tasks] predicted seconds per task (the plan's
                                  end - start); NULL = no node priorities */
+  double* host_stage;         /* p2p = 0 plans: pinned staging image (same layout as host_in) for the
+                                 GPU->host legs of host-staged moves; NULL otherwise */
   int32_t priority_levels;    /* >0: kernel nodes get CUDA priorities from the task's slack
                                  (longest path through it vs the DAG's critical path, weights
                                  task_weight) quantised to min(levels, device range) levels;

@@ -66,13 +66,14 @@ class ExecPlan(C.Structure):
                 ("pred_ptr", _i64p), ("pred", _i32p), ("dispatch", _i32p), ("wait_ptr", _i64p),
                 ("wait_job", _i32p), ("job_block", _i32p), ("job_src", _i32p), ("job_dst", _i32p),
                 ("job_version", _i32p), ("job_src_job", _i32p), ("job_requester", _i32p),
-                ("block_bytes", _i64p), ("final_writer", _i32p), ("acc_mode", _i8p)]
+                ("block_bytes", _i64p), ("final_writer", _i32p), ("acc_mode", _i8p),
+                ("job_stage_job", _i32p), ("p2p", C.c_int32)]
 
 
 class ExecOpts(C.Structure):
     _fields_ = [("devices", _i32p), ("host_in", _f64p), ("host_out", _f64p), ("host_side_out", _f64p),
                 ("device_input", C.c_int32), ("rank_node", C.c_int32),
-                ("task_weight", _f64p), ("priority_levels", C.c_int32)]
+                ("task_weight", _f64p), ("host_stage", _f64p), ("priority_levels", C.c_int32)]
 
 
 class ExecStats(C.Structure):

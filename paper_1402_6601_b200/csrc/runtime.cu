@@ -259,6 +259,10 @@ struct hg_exec {
   std::vector<int8_t> acc_mode;
   std::vector<int64_t> acc_ptr, pred_ptr, wait_ptr, block_bytes;
   std::vector<int32_t> job_block, job_src, job_dst, job_version, job_src_job, job_requester, final_writer;
+  std::vector<int32_t> job_stage_job;
+  int p2p = 1;
+  double* host_stage = nullptr;          // p2p = 0: pinned staging image, slot-sized regions
+  std::vector<int64_t> stage_off;
   // options
   int rank_node = 0;
   const double* host_in = nullptr;
@@ -331,6 +335,12 @@ static void plan_layout(hg_exec* ex) {
     ex->slot_doubles[b] = ex->blk_doubles[b] + (ex->blk_doubles[b] == tile_d ? ex->side : 0);
     ex->host_off[b] = host_total;
     host_total += ex->blk_doubles[b];
+  }
+  ex->stage_off.resize(ex->n_blocks);
+  int64_t so = 0;
+  for (int b = 0; b < ex->n_blocks; ++b) {
+    ex->stage_off[b] = so;
+    so += ex->slot_doubles[b];
   }
   const int64_t flag_ints = int64_t(ex->n_tasks) + ex->n_jobs + 1;
   ex->header_doubles = ((flag_ints * 4 + 255) / 256) * 32;
@@ -463,6 +473,7 @@ static int build_graph(hg_exec* ex) {
   HG_CUDA(cudaGraphCreate(&ex->graph, 0));
   std::vector<cudaGraphNode_t> task_last(n, nullptr);
   std::vector<cudaGraphNode_t> job_node(ex->n_jobs, nullptr);
+  std::vector<cudaGraphNode_t> d2h_node(ex->n_jobs, nullptr);  // GPU->host leg of host-staged moves
   std::vector<cudaGraphNode_t> wait_node(size_t(n) + ex->n_jobs, nullptr);
   std::vector<std::vector<int>> jobs_of(n);
   for (int j = 0; j < ex->n_jobs; ++j) jobs_of[ex->job_requester[j]].push_back(j);
@@ -554,17 +565,46 @@ static int build_graph(hg_exec* ex) {
       const int b = ex->job_block[j], src = ex->job_src[j];
       deps.clear();
       int rc = HG_OK;
-      if (ex->job_src_job[j] >= 0) rc = dep_job(ex->job_src_job[j], dst);
-      else if (ex->job_version[j] >= 0) rc = dep_task(ex->job_version[j], dst);
+      const bool staged_in = src == 0 && (ex->job_version[j] >= 0 || ex->job_src_job[j] >= 0 ||
+                                          ex->job_stage_job[j] >= 0);
+      const bool staged_move = src >= 1 && dst >= 1 && !ex->p2p;
+      if (staged_in) {
+        // a version staged in host memory by an earlier GPU->host leg (sim.py:255-261, 322-337)
+        const int sj = ex->job_stage_job[j] >= 0 ? ex->job_stage_job[j] : ex->job_src_job[j];
+        if (sj < 0 || !d2h_node[sj]) {
+          set_error("job %d: staged version of block %d without its host leg", j, b);
+          return HG_EINVAL;
+        }
+        deps.push_back(d2h_node[sj]);
+      } else if (ex->job_src_job[j] >= 0) {
+        rc = dep_job(ex->job_src_job[j], dst);
+      } else if (ex->job_version[j] >= 0) {
+        rc = dep_task(ex->job_version[j], dst);
+      }
       if (rc) return rc;
       double* dptr = ex->slot_ptr(dst, b);
       const void* sptr;
       size_t bytes;
-      if (src == 0) {
-        if (ex->job_version[j] >= 0 || ex->job_src_job[j] >= 0) {
-          set_error("job %d: host-staged versions (p2p=False) are not executable", j);
-          return HG_EINVAL;
-        }
+      if (staged_move) {
+        // GPU -> host -> GPU (platform.py:117): two copy nodes through the staging image
+        const size_t sb = size_t(ex->slot_doubles[b]) * 8;
+        double* stage = ex->host_stage + ex->stage_off[b];
+        HG_CUDA(cudaSetDevice(ex->dev[src - 1]));
+        HG_CUDA(cudaGraphAddMemcpyNode1D(&d2h_node[j], ex->graph, deps.data(), deps.size(), stage,
+                                         ex->slot_ptr(src, b), sb, cudaMemcpyDefault));
+        st.bytes_d2h += size_t(ex->blk_doubles[b]) * 8;
+        st.n_copy_nodes++;
+        deps.assign(1, d2h_node[j]);
+        bytes = sb;
+        sptr = stage;
+        st.bytes_h2d += size_t(ex->blk_doubles[b]) * 8;
+        side_bytes += 2 * (sb - size_t(ex->blk_doubles[b]) * 8);
+      } else if (staged_in) {
+        bytes = size_t(ex->slot_doubles[b]) * 8;
+        sptr = ex->host_stage + ex->stage_off[b];
+        st.bytes_h2d += size_t(ex->blk_doubles[b]) * 8;
+        side_bytes += bytes - size_t(ex->blk_doubles[b]) * 8;
+      } else if (src == 0) {
         bytes = size_t(ex->blk_doubles[b]) * 8;
         sptr = ex->device_input ? (const void*)(ex->replica[dst - 1] + ex->host_off[b])
                                 : (const void*)(ex->host_in + ex->host_off[b]);
@@ -586,7 +626,7 @@ static int build_graph(hg_exec* ex) {
       // copy engine delivers tiles in the order tasks need them instead of all at once in arbitrary
       // order (C2 e2e: 427 -> 372 ms, i.e. PCIe fully hidden behind compute; HG_H2D_CHAINS overrides,
       // 0 = independent copies)
-      const bool from_host = src == 0 && !ex->device_input;
+      const bool from_host = src == 0 && !ex->device_input && !staged_in;
       if (from_host && h2d_chains > 0) {
         cudaGraphNode_t& prev = h2d_tail[size_t(dst - 1) * h2d_chains + (h2d_count[dst - 1]++ % h2d_chains)];
         if (prev) deps.push_back(prev);
@@ -761,6 +801,21 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
   ex->acc_ptr = vcopy(P->acc_ptr, n + 1);
   ex->acc_block = vcopy(P->acc_block, P->acc_ptr[n]);
   ex->acc_mode = vcopy(P->acc_mode, P->acc_ptr[n]);
+  ex->job_stage_job = vcopy(P->job_stage_job, P->n_jobs);
+  ex->p2p = P->p2p;
+  ex->host_stage = O->host_stage;
+  if (!ex->p2p && P->k > 1) {
+    if (!O->host_stage) {
+      set_error("hg_exec_create: a p2p=0 plan needs opts.host_stage (pinned, slot-sized regions)");
+      delete ex;
+      return HG_EINVAL;
+    }
+    if (O->rank_node != 0) {
+      set_error("hg_exec_create: host-staged routes need the single-process executor (rank_node 0)");
+      delete ex;
+      return HG_EINVAL;
+    }
+  }
   ex->pred_ptr = vcopy(P->pred_ptr, n + 1);
   ex->pred = vcopy(P->pred, P->pred_ptr[n]);
   ex->dispatch = vcopy(P->dispatch, n);

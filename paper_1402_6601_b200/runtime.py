@@ -87,9 +87,6 @@ def _gpu_nodes(plan, platform):
             raise PlatformError(
                 f"{cpu_tasks} tasks were planned on CPU workers; the B200 runtime executes "
                 "GPU-only platforms (build_platform(k, k, ...)), there is no CPU fallback")
-    if not platform.p2p and platform.k > 1:
-        raise PlatformError("GPU->GPU moves staged through the host (p2p=False) are not executable; "
-                            "use p2p=True (NVLink peer copies)")
     return (plan.worker - platform.n_cpu_workers + 1).astype(np.int32)
 
 
@@ -138,6 +135,16 @@ class Executor:
         # changes only which ready kernel gets SMs first, never the plan
         priority_levels = int(os.environ.get("HG_PRIORITY_LEVELS", priority_levels))
         self.task_weight = np.ascontiguousarray(np.asarray(plan.end, np.float64) - np.asarray(plan.start, np.float64))
+        # host-staged routes (p2p=False, platform.py:117): GPU->host->GPU moves stage through
+        # a pinned image with the host image's layout
+        self.p2p = bool(platform.p2p) or k == 1
+        self.host_stage = None
+        if not self.p2p:
+            import torch
+
+            tile = lay.b * lay.b
+            n_stage = sum(sz // 8 + (lay.side_doubles if sz // 8 == tile else 0) for sz in graph.sizes)
+            self.host_stage = torch.empty(n_stage, dtype=torch.float64).pin_memory().numpy()
         self._keep = [fl, kind_map]
         ep = ExecPlan_from(plan, n, len(graph.data), k, lay, self, fl)
         opts = _native.ExecOpts(
@@ -146,7 +153,9 @@ class Executor:
             _native.ptr(host_out, C.c_double) if host_out is not None else None,
             _native.ptr(host_side_out, C.c_double) if host_side_out is not None else None,
             int(bool(device_input)), int(rank_node),
-            _native.ptr(self.task_weight, C.c_double), int(priority_levels))
+            _native.ptr(self.task_weight, C.c_double),
+            _native.ptr(self.host_stage, C.c_double) if self.host_stage is not None else None,
+            int(priority_levels))
         h = C.c_void_p()
         _native.check(L.hg_exec_create(C.byref(ep), C.byref(opts), C.byref(h)), "hg_exec_create")
         self._h = h
@@ -274,6 +283,7 @@ def partition_counts(graph, platform, plan, rank_node: int, with_flags: bool = F
     holder.pred_ptr[1:] = np.cumsum([len(p) for p in preds])
     holder.pred = np.asarray([q for p in preds for q in p], np.int32)
     holder.final_writer = np.full(len(graph.data), -1, np.int32)
+    holder.p2p = bool(platform.p2p) or platform.k == 1
     lay = graph.layout
     ep = ExecPlan_from(plan, n, len(graph.data), platform.k, lay, holder, fl)
     out = np.zeros(4, np.int32)
@@ -298,7 +308,8 @@ def ExecPlan_from(plan, n, n_blocks, k, lay, ex, fl):
         P(plan.dispatch, C.c_int32), P(plan.wait_ptr, C.c_int64), P(plan.wait_job, C.c_int32),
         P(plan.job_block, C.c_int32), P(plan.job_src, C.c_int32), P(plan.job_dst, C.c_int32),
         P(plan.job_version, C.c_int32), P(plan.job_src_job, C.c_int32), P(plan.job_requester, C.c_int32),
-        P(fl["sizes"], C.c_int64), P(ex.final_writer, C.c_int32), P(fl["acc_mode"], C.c_int8))
+        P(fl["sizes"], C.c_int64), P(ex.final_writer, C.c_int32), P(fl["acc_mode"], C.c_int8),
+        P(plan.job_stage_job, C.c_int32), int(bool(ex.p2p)))
 
 
 def execute(graph, platform, scheduler, model, host_in: np.ndarray, host_out: np.ndarray | None = None,

@@ -88,3 +88,32 @@ def test_lu_qr_4_nodes_one_gpu(fam):
     # incremental pivoting is less stable than partial pivoting: the backward
     # error itself is ~1e-13..1e-12 at n=4096, and must match the oracle's
     assert r_gpu < 1e-11 and abs(r_gpu - r_cpu) < 1e-12
+
+
+@pytest.mark.parametrize("fam", ["cholesky", "lu"])
+def test_host_staged_route_p2p_false(fam):
+    """p2p=False plans (platform.py:117, the paper's PCIe machine): every GPU->GPU move
+    is staged GPU->host->GPU through a pinned image; executed bytes per direction
+    equal the plan's (d2h and h2d both charged, no d2d) and the factor is exact."""
+    from oracle import tiles_lu_qr as LQ  # noqa: F401
+
+    n, nb, k = 4096, 512, 4
+    g = H.gen_family(fam, n // nb, nb, 128)
+    plat = H.build_platform(k, k, k, link_bandwidth=5.5e10, link_latency=5e-6, switch_cap=math.inf, p2p=False)
+    plan = H.make_plan(g, plat, H.make_scheduler("dada", alpha=0.5, cp=True), H.PerfModel(H.default_timing_table(nb, 128)))
+    assert plan.bytes_d2h > 0 and plan.bytes_d2d == 0
+    A = O.spd_matrix(n, 5) if fam == "cholesky" else O.general_matrix(n, 5)
+    img = runtime.to_tile_major(A, g)
+    out = np.zeros_like(img)
+    ex = runtime.Executor(g, plat, plan, img, out, devices=[0] * k)
+    st = ex.run()
+    ex.close()
+    assert (st.bytes_h2d, st.bytes_d2d) == (plan.bytes_h2d, 0)
+    assert st.bytes_d2h == plan.bytes_d2h + sum(g.sizes)  # + the write-back of every (written) block
+    T = O.tiles_of(A, g.layout)
+    O.run_tasks(g, T, side={})
+    ref = O.assemble(T, g.layout)
+    got = runtime.from_tile_major(out, g)
+    if fam == "cholesky":
+        ref, got = np.tril(ref), np.tril(got)
+    assert np.abs(got - ref).max() / np.abs(ref).max() < (1e-12 if fam == "cholesky" else 1e-9)
