@@ -246,6 +246,28 @@ __global__ void k_signal_flag(FlagParams p) {
   }
 }
 
+// Step fence between launches (one process per GPU): before run e starts, every
+// peer must have finished run e-1 -- a peer's last pulls from THIS rank's slots
+// (consumer-pull copies) may still be pending when this rank's own graph is done,
+// and run e's first touches would overwrite those slots.
+struct StepFence {
+  const int* peer_done[16];
+  int n;
+  int need;
+};
+__global__ void k_wait_peers_done(StepFence f) {
+  if (threadIdx.x < f.n) {
+    while (ld_acquire_sys(f.peer_done[threadIdx.x]) < f.need) __nanosleep(256);
+  }
+}
+
+__global__ void k_mark_done(int* done, int v) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(done, v);
+  }
+}
+
 __global__ void k_set_epoch(int* epoch, int v) {
   if (threadIdx.x == 0) *epoch = v;
 }
@@ -296,6 +318,7 @@ struct hg_exec {
   int* task_flag(int node, int t) const { return flags(node) + t; }
   int* job_flag(int node, int j) const { return flags(node) + n_tasks + j; }
   int* epoch_ptr(int node) const { return flags(node) + n_tasks + n_jobs; }
+  int* done_ptr(int node) const { return flags(node) + n_tasks + n_jobs + 1; }  // last finished epoch
   double* slot_ptr(int node, int b) const {
     int64_t off = slot[node - 1][b];
     return off < 0 ? nullptr : base[node - 1] + off;
@@ -342,7 +365,7 @@ static void plan_layout(hg_exec* ex) {
     ex->stage_off[b] = so;
     so += ex->slot_doubles[b];
   }
-  const int64_t flag_ints = int64_t(ex->n_tasks) + ex->n_jobs + 1;
+  const int64_t flag_ints = int64_t(ex->n_tasks) + ex->n_jobs + 2;
   ex->header_doubles = ((flag_ints * 4 + 255) / 256) * 32;
   ex->slot.assign(ex->k, std::vector<int64_t>(ex->n_blocks, -1));
   ex->pool_doubles.assign(ex->k, ex->header_doubles);
@@ -1037,7 +1060,23 @@ extern "C" int hg_exec_launch(hg_exec* ex, void* stream) {
   }
   const int first = ex->rank_node ? ex->rank_node : 1;
   HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
+  if (ex->rank_node) {
+    hg::StepFence f{};
+    for (int g = 0; g < ex->k && f.n < 16; ++g)
+      if (g + 1 != ex->rank_node) f.peer_done[f.n++] = ex->done_ptr(g + 1);
+    f.need = ex->epoch - 1;
+    if (ex->k > 17) {
+      set_error("hg_exec_launch: step fence supports up to 17 ranks");
+      return HG_EINVAL;
+    }
+    hg::k_wait_peers_done<<<1, 32, 0, s>>>(f);
+    HG_CUDA(cudaGetLastError());
+  }
   HG_CUDA(cudaGraphLaunch(ex->exec, s));
+  if (ex->rank_node) {
+    hg::k_mark_done<<<1, 32, 0, s>>>(ex->done_ptr(ex->rank_node), ex->epoch);
+    HG_CUDA(cudaGetLastError());
+  }
   ex->last_stream = s;
   ex->launched = true;
   return HG_OK;

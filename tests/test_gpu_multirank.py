@@ -42,6 +42,9 @@ def _rank_main(rank, world, port, family, q):
         for _ in range(2):  # two runs: flags must advance with the epoch
             ex.launch(0)
             ex.wait()
+        for _ in range(3):  # back-to-back runs (as bench.py times them): the step fence keeps a
+            ex.launch(0)    # rank from overwriting slots a slower peer still pulls from
+        ex.wait()
         st = ex.info()
         ex.close()
         q.put((rank, out, st.bytes_h2d, st.bytes_d2d))
