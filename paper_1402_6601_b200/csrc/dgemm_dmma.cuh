@@ -45,16 +45,38 @@ HG_DEVICE void load_slab(double* s, const double* __restrict__ g, int ld, int r0
   if constexpr (L == M_MAJOR) {
     constexpr int CH_PER_K = ROWS / 2;  // 16-byte chunks per k-row
     constexpr int CHUNKS = BK * CH_PER_K;
-    for (int c = threadIdx.x; c < CHUNKS; c += Cfg::THREADS) {
-      int kk = c / CH_PER_K, rr = (c % CH_PER_K) * 2;
-      cp_async16(s + kk * (ROWS + PAD) + rr, g + size_t(k0 + kk) * ld + r0 + rr);
+    if constexpr (CHUNKS % Cfg::THREADS == 0) {
+      // compile-time trip count: the per-chunk offsets strength-reduce to one base
+      // pointer per thread plus immediates
+      const double* gb = g + size_t(k0) * ld + r0;
+#pragma unroll
+      for (int i = 0; i < CHUNKS / Cfg::THREADS; ++i) {
+        const int c = threadIdx.x + i * Cfg::THREADS;
+        const int kk = c / CH_PER_K, rr = (c % CH_PER_K) * 2;
+        cp_async16(s + kk * (ROWS + PAD) + rr, gb + size_t(kk) * ld + rr);
+      }
+    } else {
+      for (int c = threadIdx.x; c < CHUNKS; c += Cfg::THREADS) {
+        int kk = c / CH_PER_K, rr = (c % CH_PER_K) * 2;
+        cp_async16(s + kk * (ROWS + PAD) + rr, g + size_t(k0 + kk) * ld + r0 + rr);
+      }
     }
   } else {
     constexpr int CH_PER_R = BK / 2;
     constexpr int CHUNKS = ROWS * CH_PER_R;
-    for (int c = threadIdx.x; c < CHUNKS; c += Cfg::THREADS) {
-      int rr = c / CH_PER_R, kk = (c % CH_PER_R) * 2;
-      cp_async16(s + rr * (BK + PAD) + kk, g + size_t(r0 + rr) * ld + k0 + kk);
+    if constexpr (CHUNKS % Cfg::THREADS == 0) {
+      const double* gb = g + size_t(r0) * ld + k0;
+#pragma unroll
+      for (int i = 0; i < CHUNKS / Cfg::THREADS; ++i) {
+        const int c = threadIdx.x + i * Cfg::THREADS;
+        const int rr = c / CH_PER_R, kk = (c % CH_PER_R) * 2;
+        cp_async16(s + rr * (BK + PAD) + kk, gb + size_t(rr) * ld + kk);
+      }
+    } else {
+      for (int c = threadIdx.x; c < CHUNKS; c += Cfg::THREADS) {
+        int rr = c / CH_PER_R, kk = (c % CH_PER_R) * 2;
+        cp_async16(s + rr * (BK + PAD) + kk, g + size_t(r0 + rr) * ld + k0 + kk);
+      }
     }
   }
 }

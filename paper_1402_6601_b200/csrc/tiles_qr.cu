@@ -347,7 +347,7 @@ struct QrApplyParams {
 // BN in {16, 32, 64}: narrower strips = more SMs per task (latency), wider =
 // more reuse of V per SM (throughput inside the DAG).
 template <class CfgQ>
-__global__ void __launch_bounds__(CfgQ::THREADS) k_qr_apply(QrApplyParams p) {
+__global__ void __launch_bounds__(CfgQ::THREADS, 2) k_qr_apply(QrApplyParams p) {  // 2 CTAs / SM: <= 128 regs (32-wide)
   constexpr int kQrBN = CfgQ::BN;
   extern __shared__ double sm[];
   double* ring = sm;

@@ -62,16 +62,19 @@ def operands(kind, conc):
 for kind in kinds:
     res = {"kind": kind}
     flops = H.kind_flops(kind, nb) if hasattr(H, "kind_flops") else None
-    # TRSM's in-place counters live in hg_tile_run's per-device scratch: never overlap two
-    for conc in ((1,) if kind == "TRSM" else tuple(int(c) for c in os.environ.get("HG_CONC", "1,8").split(","))):
+    for conc in tuple(int(c) for c in os.environ.get("HG_CONC", "1,8").split(",")):
         sets = operands(kind, conc)
         streams = [torch.cuda.Stream() for _ in range(conc)]
         ptrs = [(C.c_void_p * len(ts))(*[t.data_ptr() for t in ts]) for ts in sets]
+        # per-stream scratch (TRSM's in-place counters): independent tasks may overlap
+        nsc = max(1, L.hg_task_scratch_ints(H.ALL_KINDS.index(kind), nb, ib))
+        scr = [torch.zeros(nsc, dtype=torch.int32, device="cuda") for _ in range(conc)]
         def go(reps):
             for r in range(reps):
-                for s, p in zip(streams, ptrs):
-                    _native.check(L.hg_tile_run(H.ALL_KINDS.index(kind), dev, C.c_void_p(s.cuda_stream), p,
-                                                len(sets[0]), nb, ib, C.c_void_p(status.data_ptr())), kind)
+                for s, p, sc in zip(streams, ptrs, scr):
+                    _native.check(L.hg_tile_run_scratch(H.ALL_KINDS.index(kind), dev, C.c_void_p(s.cuda_stream), p,
+                                                        len(sets[0]), nb, ib, C.c_void_p(status.data_ptr()),
+                                                        C.c_void_p(sc.data_ptr())), kind)
         go(1)
         torch.cuda.synchronize()
         reps = 5
