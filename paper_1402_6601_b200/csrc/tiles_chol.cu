@@ -41,7 +41,7 @@ struct GemmNTParams {
   int lower;  // 1: update only C(i, j) with i >= j (SYRK)
 };
 
-__global__ void __launch_bounds__(CfgG::THREADS) k_gemm_nt(GemmNTParams p) {
+__global__ void __launch_bounds__(CfgG::THREADS, 4) k_gemm_nt(GemmNTParams p) {  // 4 CTAs / SM (smem allows 4)
   extern __shared__ double smem[];
   const int m0 = blockIdx.x * CfgG::BM, n0 = blockIdx.y * CfgG::BN;
   if (p.lower && m0 + CfgG::BM - 1 < n0) return;  // tile strictly above the diagonal
@@ -836,7 +836,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
-__global__ void __launch_bounds__(CfgG::THREADS) k_trsm_inv(TrsmInvParams p) {
+__global__ void __launch_bounds__(CfgG::THREADS, 3) k_trsm_inv(TrsmInvParams p) {
   extern __shared__ double smem[];
   const int ld = p.ld, nI = ld / kR, nJ = ld / kR, P = nJ / 2;
   // strip-major ids: the P CTAs that meet on a strip counter are dispatched
