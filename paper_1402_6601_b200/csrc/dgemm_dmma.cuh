@@ -311,14 +311,17 @@ namespace hg {
 // never drains between chunks, only the per-chunk epilogue interrupts the
 // DMMAs (the trailing updates of GESSM / SSSSM / UNMQR / TSMQR, K = ib).
 // LdA exposes a mutable row origin r0.
-template <class Cfg, class LdA, bool PREFETCH_C = true>
+template <class Cfg, class LdA, bool PREFETCH_C = true, int KC = 128>
 HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int ldsb, int K, int m_begin,
                                      int m_end, double* __restrict__ C, int ldc, int n0) {
+  // K == KC (the panel width ib = 128 in every caller): the slab / chunk indices are
+  // compile-time divisions, and the A fragments are double-buffered in registers
   constexpr int LA = LdA::layout;
   constexpr int A_SLAB = LA == M_MAJOR ? Cfg::slab_mmaj(Cfg::BM) : Cfg::slab_kmaj(Cfg::BM);
   constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
-  const int nk = K / BK;
-  const int total = nk * ((m_end - m_begin) / Cfg::BM);
+  constexpr int NK = KC / BK;
+  (void)K;
+  const int total = NK * ((m_end - m_begin) / Cfg::BM);
   if (total <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
@@ -326,8 +329,8 @@ HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int
   const int g = lane >> 2, t = lane & 3;
   auto load = [&](int s) {
     LdA l = la;
-    l.r0 = m_begin + (s / nk) * Cfg::BM;
-    l.load(ring + (s % STAGES) * A_SLAB, (s % nk) * BK);
+    l.r0 = m_begin + (s / NK) * Cfg::BM;
+    l.load(ring + (s % STAGES) * A_SLAB, (s % NK) * BK);
   };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -338,27 +341,35 @@ HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int
   double cv[Cfg::FM][Cfg::FN][2];  // this chunk's C, loaded while its k-slabs run
   zero_acc<Cfg>(acc);
   for (int it = 0; it < total; ++it) {
-    if (PREFETCH_C && it % nk == 0) load_like_acc<Cfg>(cv, C, ldc, m_begin + (it / nk) * Cfg::BM, n0);
+    const int kslab = it % NK;
+    if (PREFETCH_C && kslab == 0) load_like_acc<Cfg>(cv, C, ldc, m_begin + (it / NK) * Cfg::BM, n0);
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     if (it + STAGES - 1 < total) load(it + STAGES - 1);
     cp_async_commit();
     const double* a_s = ring + (it % STAGES) * A_SLAB;
-    const int kb = (it % nk) * BK;
+    const int kb = kslab * BK;
+    double af[2][Cfg::FM], bf[2][Cfg::FN];
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i) af[0][i] = frag_at<Cfg, LA, Cfg::BM>(a_s, wm + i * 8 + g, t);
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) bf[0][j] = sB[(wn + j * 8 + g) * ldsb + kb + t];
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[Cfg::FM], bf[Cfg::FN];
+      const int cur = (kk >> 2) & 1, nxt = cur ^ 1;
+      if (kk + 4 < BK) {
 #pragma unroll
-      for (int i = 0; i < Cfg::FM; ++i) af[i] = frag_at<Cfg, LA, Cfg::BM>(a_s, wm + i * 8 + g, kk + t);
+        for (int i = 0; i < Cfg::FM; ++i) af[nxt][i] = frag_at<Cfg, LA, Cfg::BM>(a_s, wm + i * 8 + g, kk + 4 + t);
 #pragma unroll
-      for (int j = 0; j < Cfg::FN; ++j) bf[j] = sB[(wn + j * 8 + g) * ldsb + kb + kk + t];
+        for (int j = 0; j < Cfg::FN; ++j) bf[nxt][j] = sB[(wn + j * 8 + g) * ldsb + kb + kk + 4 + t];
+      }
 #pragma unroll
       for (int i = 0; i < Cfg::FM; ++i)
 #pragma unroll
-        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
     }
-    if (it % nk == nk - 1) {
-      const int m0 = m_begin + (it / nk) * Cfg::BM;
+    if (kslab == NK - 1) {
+      const int m0 = m_begin + (it / NK) * Cfg::BM;
       if (!PREFETCH_C) load_like_acc<Cfg>(cv, C, ldc, m0, n0);
       for_each_acc_ij<Cfg>([&](int i, int j, int r, int c) {
         C[size_t(n0 + c) * ldc + m0 + r] = cv[i][j][0] - acc[i][j][0];

@@ -1051,6 +1051,7 @@ __global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) 
 using CfgLS16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
 using CfgLS32 = GemmCfg<128, 32, 16, 32, 16, 3>;  // 8 warps (32x16 warp tiles): 2 CTAs / SM -> 16 warps
 using CfgLS64 = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps
+using CfgLS32w4 = GemmCfg<128, 32, 16, 32, 32, 3>;  // 4 warps, 32x32 warp tiles (HG_LU_APPLY=33)
 
 template <class G>
 static unsigned lu_apply_strip_smem() {
@@ -1128,6 +1129,7 @@ bool init_lu_attributes() {
   HG_ATTR(k_lu_apply_strip<CfgLS16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS16>());
   HG_ATTR(k_lu_apply_strip<CfgLS32>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS32>());
   HG_ATTR(k_lu_apply_strip<CfgLS64>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS64>());
+  HG_ATTR(k_lu_apply_strip<CfgLS32w4>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS32w4>());
   HG_ATTR(k_lu_panel_sp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpSmem<128>::BYTES);
   HG_ATTR(k_lu_panel_sp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(512));
   return true;
@@ -1172,6 +1174,9 @@ static void push_apply_cl(std::vector<LaunchDesc>& out, const double* L, const d
   else if (bn == 16)
     d.set((const void*)k_lu_apply_strip<CfgLS16>, dim3(ncols / 16), dim3(CfgLS16::THREADS),
           lu_apply_strip_smem<CfgLS16>(), ap);
+  else if (bn == 33)
+    d.set((const void*)k_lu_apply_strip<CfgLS32w4>, dim3(ncols / 32), dim3(CfgLS32w4::THREADS),
+          lu_apply_strip_smem<CfgLS32w4>(), ap);
   else if (bn == 64 && ncols % 64 == 0)
     d.set((const void*)k_lu_apply_strip<CfgLS64>, dim3(ncols / 64), dim3(CfgLS64::THREADS),
           lu_apply_strip_smem<CfgLS64>(), ap);
