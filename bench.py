@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--family", default="cholesky")
-    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=32768)
     ap.add_argument("--nb", type=int, default=1024)
     ap.add_argument("--ib", type=int, default=128)
     ap.add_argument("--alpha", type=float, default=0.5)
@@ -315,11 +315,19 @@ def run_ours(args, rank, world, local):
     import paper_1402_6601_b200 as H
     from paper_1402_6601_b200 import _native, runtime
 
+    # test hooks (never set by the driver): HG_BENCH_DEVICE pins every rank to one GPU and
+    # HG_DIST_BACKEND=gloo lets several ranks share it, to exercise the N > 1 path on one B200
+    local = int(os.environ.get("HG_BENCH_DEVICE", local))
+    backend = os.environ.get("HG_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
     k = world
     n, nb, fam = args.n, args.nb, args.family
     g = H.gen_family(fam, n // nb, nb, args.ib)
@@ -344,14 +352,14 @@ def run_ours(args, rank, world, local):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         torch.distributed.all_reduce(t)
         return float(t.item())
 
