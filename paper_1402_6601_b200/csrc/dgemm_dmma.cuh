@@ -311,9 +311,15 @@ namespace hg {
 // never drains between chunks, only the per-chunk epilogue interrupts the
 // DMMAs (the trailing updates of GESSM / SSSSM / UNMQR / TSMQR, K = ib).
 // LdA exposes a mutable row origin r0.
-template <class Cfg, class LdA, bool PREFETCH_C = true, int KC = 128>
+// RED: the epilogue is red.global.add(-acc) instead of load / subtract / store
+// (no C load latency, no C registers, half the C traffic); the caller's later
+// reads of C must bypass L1 (cp.async.cg / ld.cg): a __threadfence() here makes
+// the reductions visible before the caller's next barrier.
+// m_mask: rows < m_mask are computed but not written (lets a BM that does not
+// divide m_end - m_mask start its first chunk early; RED epilogue only).
+template <class Cfg, class LdA, bool PREFETCH_C = true, int KC = 128, bool RED = false>
 HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int ldsb, int K, int m_begin,
-                                     int m_end, double* __restrict__ C, int ldc, int n0) {
+                                     int m_end, double* __restrict__ C, int ldc, int n0, int m_mask = 0) {
   // K == KC (the panel width ib = 128 in every caller): the slab / chunk indices are
   // compile-time divisions, and the A fragments are double-buffered in registers
   constexpr int LA = LdA::layout;
@@ -342,7 +348,7 @@ HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int
   zero_acc<Cfg>(acc);
   for (int it = 0; it < total; ++it) {
     const int kslab = it % NK;
-    if (PREFETCH_C && kslab == 0) load_like_acc<Cfg>(cv, C, ldc, m_begin + (it / NK) * Cfg::BM, n0);
+    if (!RED && PREFETCH_C && kslab == 0) load_like_acc<Cfg>(cv, C, ldc, m_begin + (it / NK) * Cfg::BM, n0);
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     if (it + STAGES - 1 < total) load(it + STAGES - 1);
@@ -370,14 +376,24 @@ HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int
     }
     if (kslab == NK - 1) {
       const int m0 = m_begin + (it / NK) * Cfg::BM;
-      if (!PREFETCH_C) load_like_acc<Cfg>(cv, C, ldc, m0, n0);
-      for_each_acc_ij<Cfg>([&](int i, int j, int r, int c) {
-        C[size_t(n0 + c) * ldc + m0 + r] = cv[i][j][0] - acc[i][j][0];
-        C[size_t(n0 + c + 1) * ldc + m0 + r] = cv[i][j][1] - acc[i][j][1];
-      });
+      if constexpr (RED) {
+        for_each_acc_ij<Cfg>([&](int i, int j, int r, int c) {
+          if (m0 + r >= m_mask) {
+            red_add_f64(C + size_t(n0 + c) * ldc + m0 + r, -acc[i][j][0]);
+            red_add_f64(C + size_t(n0 + c + 1) * ldc + m0 + r, -acc[i][j][1]);
+          }
+        });
+      } else {
+        if (!PREFETCH_C) load_like_acc<Cfg>(cv, C, ldc, m0, n0);
+        for_each_acc_ij<Cfg>([&](int i, int j, int r, int c) {
+          C[size_t(n0 + c) * ldc + m0 + r] = cv[i][j][0] - acc[i][j][0];
+          C[size_t(n0 + c + 1) * ldc + m0 + r] = cv[i][j][1] - acc[i][j][1];
+        });
+      }
       zero_acc<Cfg>(acc);
     }
   }
+  if constexpr (RED) __threadfence();
   cp_async_wait<0>();
   __syncthreads();
 }

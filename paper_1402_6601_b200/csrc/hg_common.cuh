@@ -36,6 +36,13 @@ HG_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); 
 template <int N>
 HG_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// C += v as a fire-and-forget reduction performed at L2 (no load round trip to
+// the SM).  fl(c + (-a)) == fl(c - a), so "red(-acc)" is bit-identical to the
+// read-modify-write "c = c - acc" when one thread owns the element.
+HG_DEVICE void red_add_f64(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+}
+
 HG_DEVICE double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

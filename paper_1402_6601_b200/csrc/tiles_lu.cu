@@ -977,10 +977,18 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
 // interchanges, top' = inv(L_uu) top (DMMA) and bot -= L_a top' (DMMA) need
 // only CTA barriers.  Small shared-memory footprint (2 CTAs / SM), so it
 // co-schedules with the other tile kernels of the DAG.
-template <class G>
-__global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) {
+// RED: bot -= L_a top' as L2 reductions (red.global.add.f64 of -acc); every
+// later read of bot inside the kernel goes through L2 (ld.cg / cp.async.cg).
+// GU: the configuration of the bot -= L_a top' stream (default G); a GU with
+// BM = 256 starts its first row chunk early and masks the rows above it.
+template <class G, bool RED = false, class GU = G>
+__global__ void __launch_bounds__(G::THREADS, G::THREADS == 128 ? 3 : (GU::BM == 256 ? 2 : 1))
+k_lu_apply_strip(LuApplyParams p) {
+  static_assert(GU::THREADS == G::THREADS && GU::BN == G::BN, "update config");
   constexpr int BN = G::BN;
-  constexpr int RING = G::STAGES * G::slab_mmaj(G::BM);  // only A streams (B is resident)
+  constexpr int RING_T = G::STAGES * G::slab_mmaj(G::BM);  // only A streams (B is resident)
+  constexpr int RING_U = GU::STAGES * GU::slab_mmaj(GU::BM);
+  constexpr int RING = RING_T > RING_U ? RING_T : RING_U;
   constexpr int AREA = (RING + BN * kLcLd > kLcMaxMoves * BN) ? RING + BN * kLcLd : kLcMaxMoves * BN;
   extern __shared__ double sm[];
   double* ring = sm;
@@ -1010,7 +1018,7 @@ __global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) 
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int e = e0 + u * G::THREADS;
-        v[u] = e < nm * BN ? *at(mv_src[e / BN], n0 + e % BN) : 0.0;
+        v[u] = e < nm * BN ? __ldcg(at(mv_src[e / BN], n0 + e % BN)) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -1019,7 +1027,7 @@ __global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) 
       }
     }
     __syncthreads();
-    for (int e = tid; e < nm * BN; e += G::THREADS) *at(mv_dst[e / BN], n0 + e % BN) = mvv[e];
+    for (int e = tid; e < nm * BN; e += G::THREADS) __stcg(at(mv_dst[e / BN], n0 + e % BN), mvv[e]);
     __syncthreads();
     // top rows -> smem with cp.async (16-byte chunks along the contiguous rows)
     for (int e = tid; e < (sb / 2) * BN; e += G::THREADS) {
@@ -1041,8 +1049,11 @@ __global__ void __launch_bounds__(G::THREADS) k_lu_apply_strip(LuApplyParams p) 
     }
     __syncthreads();
     if (!p.swap_only) {
-      TileLoader<G, M_MAJOR, 128> la{p.L + size_t(ii) * nb, nb, 0};
-      gemm_sub_chunks_bsmem<G>(ring, la, Wt, kLcLd, sb, ts ? 0 : ii + sb, nb, bot, nb, n0);
+      TileLoader<GU, M_MAJOR, GU::BM> la{p.L + size_t(ii) * nb, nb, 0};
+      const int m_mask = ts ? 0 : ii + sb;
+      const int m_lo = nb - (nb - m_mask + GU::BM - 1) / GU::BM * GU::BM;
+      gemm_sub_chunks_bsmem<GU, decltype(la), true, 128, RED>(ring, la, Wt, kLcLd, sb, m_lo, nb, bot, nb, n0,
+                                                              m_mask);
     }
     __syncthreads();
   }
@@ -1052,10 +1063,15 @@ using CfgLS16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
 using CfgLS32 = GemmCfg<128, 32, 16, 32, 16, 3>;  // 8 warps (32x16 warp tiles): 2 CTAs / SM -> 16 warps
 using CfgLS64 = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps
 using CfgLS32w4 = GemmCfg<128, 32, 16, 32, 32, 3>;  // 4 warps, 32x32 warp tiles (HG_LU_APPLY=33)
+using CfgLU256 = GemmCfg<256, 32, 8, 32, 32, 4>;    // update stream: 8 warps of 32x32, 4 x 8-wide k-slabs
+using CfgLS4w = GemmCfg<128, 32, 8, 32, 32, 4>;     // 4 warps of 32x32, 8-wide k-slabs: 3 CTAs / SM
 
-template <class G>
+template <class G, class GU = G>
 static unsigned lu_apply_strip_smem() {
-  size_t d = size_t(G::STAGES) * G::slab_mmaj(G::BM) + G::BN * kLcLd;
+  size_t ring = size_t(G::STAGES) * G::slab_mmaj(G::BM);
+  const size_t ru = size_t(GU::STAGES) * GU::slab_mmaj(GU::BM);
+  if (ru > ring) ring = ru;
+  size_t d = ring + G::BN * kLcLd;
   if (d < size_t(kLcMaxMoves) * G::BN) d = size_t(kLcMaxMoves) * G::BN;
   size_t ints = 2 * kLcMaxMoves + 3 * kLuMaxSb;
   return unsigned(d * sizeof(double) + ints * sizeof(int));
@@ -1130,6 +1146,12 @@ bool init_lu_attributes() {
   HG_ATTR(k_lu_apply_strip<CfgLS32>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS32>());
   HG_ATTR(k_lu_apply_strip<CfgLS64>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS64>());
   HG_ATTR(k_lu_apply_strip<CfgLS32w4>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS32w4>());
+  HG_ATTR((k_lu_apply_strip<CfgLS16, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS16>());
+  HG_ATTR((k_lu_apply_strip<CfgLS32, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS32>());
+  HG_ATTR((k_lu_apply_strip<CfgLS4w, true>), cudaFuncAttributeMaxDynamicSharedMemorySize,
+          lu_apply_strip_smem<CfgLS4w>());
+  HG_ATTR((k_lu_apply_strip<CfgLS32, true, CfgLU256>), cudaFuncAttributeMaxDynamicSharedMemorySize,
+          (lu_apply_strip_smem<CfgLS32, CfgLU256>()));
   HG_ATTR(k_lu_panel_sp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpSmem<128>::BYTES);
   HG_ATTR(k_lu_panel_sp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(512));
   return true;
@@ -1162,6 +1184,24 @@ static int lu_apply_env() {
   return v;
 }
 
+// HG_RED=0: trailing updates as load / subtract / store instead of L2 reductions (A/B)
+static bool use_red() {
+  static const bool v = [] {
+    const char* e = getenv("HG_RED");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// 32-column strip variants (A/B)
+static int strip_mode() {  // HG_WIDE: 0 = 4-warp strips (default), 1 = 256-row 8-warp update, 2 = 8 warps 32x16
+  static const int v = [] {
+    const char* e = getenv("HG_WIDE");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 // Panels [P0, P1) applied to columns [col0, nb): strip kernel (default) or cluster kernel.
 static void push_apply_cl(std::vector<LaunchDesc>& out, const double* L, const double* side, double* top,
                           double* bot, int nb, int ib, int P0, int P1, int col0, int mode, int bn_default = 32) {
@@ -1172,17 +1212,23 @@ static void push_apply_cl(std::vector<LaunchDesc>& out, const double* L, const d
   if (bn < 0)
     d.set((const void*)k_lu_apply_cl, dim3(ncols / kLcBN * kLcCl), dim3(CfgLC::THREADS), lu_apply_cl_smem(), ap);
   else if (bn == 16)
-    d.set((const void*)k_lu_apply_strip<CfgLS16>, dim3(ncols / 16), dim3(CfgLS16::THREADS),
-          lu_apply_strip_smem<CfgLS16>(), ap);
+    d.set(use_red() ? (const void*)k_lu_apply_strip<CfgLS16, true> : (const void*)k_lu_apply_strip<CfgLS16>,
+          dim3(ncols / 16), dim3(CfgLS16::THREADS), lu_apply_strip_smem<CfgLS16>(), ap);
   else if (bn == 33)
     d.set((const void*)k_lu_apply_strip<CfgLS32w4>, dim3(ncols / 32), dim3(CfgLS32w4::THREADS),
           lu_apply_strip_smem<CfgLS32w4>(), ap);
   else if (bn == 64 && ncols % 64 == 0)
     d.set((const void*)k_lu_apply_strip<CfgLS64>, dim3(ncols / 64), dim3(CfgLS64::THREADS),
           lu_apply_strip_smem<CfgLS64>(), ap);
+  else if (bn == 34 || (bn == 32 && use_red() && strip_mode() == 0))
+    d.set((const void*)k_lu_apply_strip<CfgLS4w, true>, dim3(ncols / 32), dim3(CfgLS4w::THREADS),
+          lu_apply_strip_smem<CfgLS4w>(), ap);
+  else if (bn == 32 && use_red() && strip_mode() == 1)
+    d.set((const void*)k_lu_apply_strip<CfgLS32, true, CfgLU256>, dim3(ncols / 32), dim3(CfgLS32::THREADS),
+          lu_apply_strip_smem<CfgLS32, CfgLU256>(), ap);
   else
-    d.set((const void*)k_lu_apply_strip<CfgLS32>, dim3(ncols / 32), dim3(CfgLS32::THREADS),
-          lu_apply_strip_smem<CfgLS32>(), ap);
+    d.set(use_red() ? (const void*)k_lu_apply_strip<CfgLS32, true> : (const void*)k_lu_apply_strip<CfgLS32>,
+          dim3(ncols / 32), dim3(CfgLS32::THREADS), lu_apply_strip_smem<CfgLS32>(), ap);
   out.push_back(d);
 }
 

@@ -301,6 +301,8 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
 using CfgQ64 = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps; requires sb == 128
 using CfgQ32 = GemmCfg<128, 32, 16, 32, 16, 3>;  // 8 warps (32x16 warp tiles)
 using CfgQ16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
+using CfgQ4w = GemmCfg<128, 32, 8, 32, 32, 4>;    // 4 warps of 32x32: C -= V W stream (3 CTAs / SM)
+using CfgQ4w1 = GemmCfg<128, 32, 8, 32, 32, 2>;   //   and its W = V^T C / T^T W phases
 constexpr int kWld = kQrMaxSb + 4;  // W stored [n][k]
 
 // Unit-lower reflector block V of panel ii, element (tile row tr, panel col pc):
@@ -346,12 +348,24 @@ struct QrApplyParams {
 // Column-strip variant: one CTA per BN-column strip (no cluster, all rows),
 // BN in {16, 32, 64}: narrower strips = more SMs per task (latency), wider =
 // more reuse of V per SM (throughput inside the DAG).
-template <class CfgQ>
-__global__ void __launch_bounds__(CfgQ::THREADS, 2) k_qr_apply(QrApplyParams p) {  // 2 CTAs / SM: <= 128 regs (32-wide)
+// RED: C -= V W as L2 reductions (red.global.add.f64 of -acc); the next panel
+// reads C only through cp.async.cg (L2), after the fence in the update loop.
+// C1: the configuration of the two K_MAJOR x K_MAJOR phases (W = V^T C, W = T^T W);
+// a shallower ring there lets the 4-warp variant fit 3 CTAs per SM.
+template <class CfgQ, class C1>
+__host__ __device__ constexpr int qr_ring_doubles() {
+  constexpr int a = GemmSmem<C1, K_MAJOR, K_MAJOR>::DOUBLES;
+  constexpr int b = CfgQ::STAGES * CfgQ::slab_mmaj(CfgQ::BM);
+  return a > b ? a : b;
+}
+
+template <class CfgQ, bool RED = false, class C1 = CfgQ>
+__global__ void __launch_bounds__(CfgQ::THREADS, CfgQ::THREADS == 128 ? 3 : 2) k_qr_apply(QrApplyParams p) {
+  static_assert(C1::THREADS == CfgQ::THREADS && C1::BN == CfgQ::BN && C1::BM == CfgQ::BM, "phase config");
   constexpr int kQrBN = CfgQ::BN;
   extern __shared__ double sm[];
   double* ring = sm;
-  double* W = sm + GemmSmem<CfgQ, K_MAJOR, K_MAJOR>::DOUBLES;  // [n][k], ld kWld
+  double* W = sm + qr_ring_doubles<CfgQ, C1>();  // [n][k], ld kWld
   const int nb = p.nb, ib = p.ib;
   const int n0 = p.col0 + blockIdx.x * kQrBN;
   const bool ts = p.mode == QR_TSQRT;
@@ -360,45 +374,46 @@ __global__ void __launch_bounds__(CfgQ::THREADS, 2) k_qr_apply(QrApplyParams p) 
     const double* Vp = p.V + size_t(ii) * nb;  // V(tr, pc) at Vp[pc*nb + tr]
     // ---- W = V^T C   (UNMQR, K over tile rows [ii, nb))  |  top + V_B^T bot (TSMQR)
     {
-      double acc[CfgQ::FM][CfgQ::FN][2];
-      zero_acc<CfgQ>(acc);
+      double acc[C1::FM][C1::FN][2];
+      zero_acc<C1>(acc);
       if (ts) {
-        VLoader<CfgQ, K_MAJOR, 128> la{Vp, nb, 0, ii, 0};
-        TileLoader<CfgQ, K_MAJOR, kQrBN> lb{p.bot, nb, n0};
-        gemm_mainloop<CfgQ>(acc, ring, la, lb, 0, nb);
+        VLoader<C1, K_MAJOR, 128> la{Vp, nb, 0, ii, 0};
+        TileLoader<C1, K_MAJOR, kQrBN> lb{p.bot, nb, n0};
+        gemm_mainloop<C1>(acc, ring, la, lb, 0, nb);
       } else {
-        VLoader<CfgQ, K_MAJOR, 128> la{Vp, nb, 0, ii, 1};
-        TileLoader<CfgQ, K_MAJOR, kQrBN> lb{p.top, nb, n0};
-        gemm_mainloop<CfgQ>(acc, ring, la, lb, ii, nb);
+        VLoader<C1, K_MAJOR, 128> la{Vp, nb, 0, ii, 1};
+        TileLoader<C1, K_MAJOR, kQrBN> lb{p.top, nb, n0};
+        gemm_mainloop<C1>(acc, ring, la, lb, ii, nb);
       }
       if (ts) {  // W = top + V_B^T bot: top loads batched, not one L2 round trip per element
-        double tv[CfgQ::FM][CfgQ::FN][2];
-        load_like_acc<CfgQ>(tv, p.top + ii, nb, 0, n0);
+        double tv[C1::FM][C1::FN][2];
+        load_like_acc<C1>(tv, p.top + ii, nb, 0, n0);
 #pragma unroll
-        for (int i = 0; i < CfgQ::FM; ++i)
+        for (int i = 0; i < C1::FM; ++i)
 #pragma unroll
-          for (int j = 0; j < CfgQ::FN; ++j) {
+          for (int j = 0; j < C1::FN; ++j) {
             acc[i][j][0] += tv[i][j][0];
             acc[i][j][1] += tv[i][j][1];
           }
       }
-      for_each_acc<CfgQ>(acc, [&](int r, int c, double v) { W[c * kWld + r] = v; });
+      for_each_acc<C1>(acc, [&](int r, int c, double v) { W[c * kWld + r] = v; });
     }
     __syncthreads();
     // ---- W <- T^T W  (T^T(r, k) = T(k, r) at side[(ii + r)*ib + k])
     {
-      double acc[CfgQ::FM][CfgQ::FN][2];
-      zero_acc<CfgQ>(acc);
-      TileLoader<CfgQ, K_MAJOR, 128> la{p.side + size_t(ii) * ib, ib, 0};
-      gemm_mainloop_bsmem<CfgQ>(acc, ring, la, W, kWld, 0, 128);
-      for_each_acc<CfgQ>(acc, [&](int r, int c, double v) { W[c * kWld + r] = v; });
-      if (ts) sub_store<CfgQ>(acc, p.top + ii, nb, 0, n0);  // top -= W (all loads first)
+      double acc[C1::FM][C1::FN][2];
+      zero_acc<C1>(acc);
+      TileLoader<C1, K_MAJOR, 128> la{p.side + size_t(ii) * ib, ib, 0};
+      gemm_mainloop_bsmem<C1>(acc, ring, la, W, kWld, 0, 128);
+      for_each_acc<C1>(acc, [&](int r, int c, double v) { W[c * kWld + r] = v; });
+      if (ts) sub_store<C1>(acc, p.top + ii, nb, 0, n0);  // top -= W (all loads first)
     }
     __syncthreads();
     // ---- C -= V W  (UNMQR rows [ii, nb))  |  bot -= V_B W (TSMQR)
     {
       VLoader<CfgQ, M_MAJOR, 128> la{Vp, nb, 0, ii, ts ? 0 : 1};
-      gemm_sub_chunks_bsmem<CfgQ, decltype(la), false>(ring, la, W, kWld, 128, ts ? 0 : ii, nb, ts ? p.bot : p.top, nb, n0);
+      gemm_sub_chunks_bsmem<CfgQ, decltype(la), false, 128, RED>(ring, la, W, kWld, 128, ts ? 0 : ii, nb,
+                                                                  ts ? p.bot : p.top, nb, n0);
     }
     __syncthreads();
   }
@@ -890,9 +905,9 @@ static unsigned qr_panel_smem(int nb, int sb) {
   return unsigned(d * sizeof(double));
 }
 
-template <class CfgQ>
+template <class CfgQ, class C1 = CfgQ>
 static unsigned qr_apply_smem() {
-  return unsigned((GemmSmem<CfgQ, K_MAJOR, K_MAJOR>::DOUBLES + CfgQ::BN * kWld) * sizeof(double));
+  return unsigned((qr_ring_doubles<CfgQ, C1>() + CfgQ::BN * kWld) * sizeof(double));
 }
 
 #define HG_QATTR(fn, attr, val)                                                                  \
@@ -911,6 +926,10 @@ bool init_qr_attributes() {
   HG_QATTR(k_qr_apply<CfgQ64>, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ64>());
   HG_QATTR(k_qr_apply<CfgQ32>, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ32>());
   HG_QATTR(k_qr_apply<CfgQ16>, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ16>());
+  HG_QATTR((k_qr_apply<CfgQ32, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ32>());
+  HG_QATTR((k_qr_apply<CfgQ4w, true, CfgQ4w1>), cudaFuncAttributeMaxDynamicSharedMemorySize,
+           (qr_apply_smem<CfgQ4w, CfgQ4w1>()));
+  HG_QATTR((k_qr_apply<CfgQ16, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ16>());
   HG_QATTR(k_qr_apply_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_cl_smem());
   return true;
 }
@@ -944,6 +963,11 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
     if (e[0] == 'c') return -1;
     return atoi(e);
   }();
+  // HG_RED=0: C -= V W as load / subtract / store instead of L2 reductions (A/B)
+  static const bool red = [] {
+    const char* e = getenv("HG_RED");
+    return !(e && e[0] == '0');
+  }();
   auto push_apply = [&](const QrApplyParams& ap, int bn_default) {
     LaunchDesc d;
     const int bn = mode_env ? mode_env : bn_default;
@@ -951,9 +975,14 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
     if (bn < 0 && nb % (kQcCl * 128) == 0)
       d.set((const void*)k_qr_apply_cl, dim3(ncols / kQcBN * kQcCl), dim3(CfgQC::THREADS), qr_apply_cl_smem(), ap);
     else if (bn == 16)
-      d.set((const void*)k_qr_apply<CfgQ16>, dim3(ncols / 16), dim3(CfgQ16::THREADS), qr_apply_smem<CfgQ16>(), ap);
+      d.set(red ? (const void*)k_qr_apply<CfgQ16, true> : (const void*)k_qr_apply<CfgQ16>, dim3(ncols / 16),
+            dim3(CfgQ16::THREADS), qr_apply_smem<CfgQ16>(), ap);
+    else if (bn == 34 || (bn == 32 && red && mode_env == 0))
+      d.set((const void*)k_qr_apply<CfgQ4w, true, CfgQ4w1>, dim3(ncols / 32), dim3(CfgQ4w::THREADS),
+            qr_apply_smem<CfgQ4w, CfgQ4w1>(), ap);
     else if (bn == 32)
-      d.set((const void*)k_qr_apply<CfgQ32>, dim3(ncols / 32), dim3(CfgQ32::THREADS), qr_apply_smem<CfgQ32>(), ap);
+      d.set(red ? (const void*)k_qr_apply<CfgQ32, true> : (const void*)k_qr_apply<CfgQ32>, dim3(ncols / 32),
+            dim3(CfgQ32::THREADS), qr_apply_smem<CfgQ32>(), ap);
     else
       d.set((const void*)k_qr_apply<CfgQ64>, dim3(ncols / 64), dim3(CfgQ64::THREADS), qr_apply_smem<CfgQ64>(), ap);
     out.push_back(d);
