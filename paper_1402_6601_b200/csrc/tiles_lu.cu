@@ -295,6 +295,8 @@ struct LuApplyParams {
   double* bot;          // GETRF-type: == top; TSTRF-type: the other tile
   int nb, ib, p0, p1, col0, mode;
   int swap_only;        // 1: row interchanges + inv(L_uu)*top only (the bot update is a separate wide GEMM)
+  long long batch_stride;  // profiling only (HG_PROF_BATCH): CTA b works on operand set b / strips,
+                           // the sets batch_stride doubles apart; 0 = one set
 };
 
 template <int SB>
@@ -1000,7 +1002,15 @@ k_lu_apply_strip(LuApplyParams p) {
   int* sp = mv_src + kLcMaxMoves;         // [3 * sb]
   __shared__ int n_moves;
   const int nb = p.nb, ib = p.ib, sb = ib;
-  const int n0 = p.col0 + blockIdx.x * BN;
+  const int strips = (nb - p.col0) / BN;
+  const size_t set_off = p.batch_stride ? size_t(blockIdx.x / strips) * size_t(p.batch_stride) : 0;
+  if (set_off) {
+    p.L += set_off;
+    p.side += set_off;
+    p.top += set_off;
+    p.bot += set_off;
+  }
+  const int n0 = p.col0 + (blockIdx.x % strips) * BN;
   const bool ts = p.mode == LU_TSTRF;
   const int tid = threadIdx.x;
   const int* ipiv = reinterpret_cast<const int*>(p.side + size_t(ib) * nb);
@@ -1013,15 +1023,16 @@ k_lu_apply_strip(LuApplyParams p) {
       return code >= 0 ? bot + size_t(c) * nb + code : top + size_t(c) * nb + ii + (-1 - code);
     };
     // gather every moved value before any is written; 8 loads in flight per thread
-    for (int e0 = tid; e0 < nm * BN; e0 += 8 * G::THREADS) {
-      double v[8];
+    constexpr int GU_ = 2048 / G::THREADS;  // loads in flight per thread
+    for (int e0 = tid; e0 < nm * BN; e0 += GU_ * G::THREADS) {
+      double v[GU_];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < GU_; ++u) {
         const int e = e0 + u * G::THREADS;
         v[u] = e < nm * BN ? __ldcg(at(mv_src[e / BN], n0 + e % BN)) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < GU_; ++u) {
         const int e = e0 + u * G::THREADS;
         if (e < nm * BN) mvv[e] = v[u];
       }
@@ -1041,7 +1052,7 @@ k_lu_apply_strip(LuApplyParams p) {
       double acc[G::FM][G::FN][2];
       zero_acc<G>(acc);
       TileLoader<G, M_MAJOR, 128> la{p.side + size_t(ii) * ib, ib, 0};
-      gemm_mainloop_bsmem<G>(acc, ring, la, Ts, kLcLd, 0, sb);
+      gemm_mainloop_bsmem<G, decltype(la), true>(acc, ring, la, Ts, kLcLd, 0, sb);  // inv(L_uu) lower
       for_each_acc<G>(acc, [&](int r, int c, double v) {
         Wt[c * kLcLd + r] = v;
         top[size_t(n0 + c) * nb + ii + r] = v;
@@ -1205,8 +1216,19 @@ static int strip_mode() {  // HG_WIDE: 0 = 4-warp strips (default), 1 = 256-row 
 // Panels [P0, P1) applied to columns [col0, nb): strip kernel (default) or cluster kernel.
 static void push_apply_cl(std::vector<LaunchDesc>& out, const double* L, const double* side, double* top,
                           double* bot, int nb, int ib, int P0, int P1, int col0, int mode, int bn_default = 32) {
-  LuApplyParams ap{L, side, top, bot, nb, ib, P0, P1, col0, mode, 0};
+  LuApplyParams ap{L, side, top, bot, nb, ib, P0, P1, col0, mode, 0, 0};
   LaunchDesc d;
+  // profiling hook: HG_PROF_BATCH=B HG_PROF_STRIDE=S launch B operand sets S doubles apart in
+  // one grid (a saturated single launch that ncu can capture); never set in production
+  static const int prof_batch = [] {
+    const char* e = getenv("HG_PROF_BATCH");
+    return e ? atoi(e) : 0;
+  }();
+  if (prof_batch > 1 && mode == LU_TSTRF && col0 == 0) {
+    const char* e = getenv("HG_PROF_STRIDE");
+    ap.batch_stride = e ? atoll(e) : 0;
+  }
+  const int batch = ap.batch_stride ? prof_batch : 1;
   const int bn = lu_apply_env() ? lu_apply_env() : bn_default;
   const int ncols = nb - col0;
   if (bn < 0)
@@ -1221,7 +1243,7 @@ static void push_apply_cl(std::vector<LaunchDesc>& out, const double* L, const d
     d.set((const void*)k_lu_apply_strip<CfgLS64>, dim3(ncols / 64), dim3(CfgLS64::THREADS),
           lu_apply_strip_smem<CfgLS64>(), ap);
   else if (bn == 34 || (bn == 32 && use_red() && strip_mode() == 0))
-    d.set((const void*)k_lu_apply_strip<CfgLS4w, true>, dim3(ncols / 32), dim3(CfgLS4w::THREADS),
+    d.set((const void*)k_lu_apply_strip<CfgLS4w, true>, dim3(ncols / 32 * batch), dim3(CfgLS4w::THREADS),
           lu_apply_strip_smem<CfgLS4w>(), ap);
   else if (bn == 32 && use_red() && strip_mode() == 1)
     d.set((const void*)k_lu_apply_strip<CfgLS32, true, CfgLU256>, dim3(ncols / 32), dim3(CfgLS32::THREADS),

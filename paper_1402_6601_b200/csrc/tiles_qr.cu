@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(CfgQ::THREADS, CfgQ::THREADS == 128 ? 3 : 2) k
       double acc[C1::FM][C1::FN][2];
       zero_acc<C1>(acc);
       TileLoader<C1, K_MAJOR, 128> la{p.side + size_t(ii) * ib, ib, 0};
-      gemm_mainloop_bsmem<C1>(acc, ring, la, W, kWld, 0, 128);
+      gemm_mainloop_bsmem<C1, decltype(la), true>(acc, ring, la, W, kWld, 0, 128);  // T^T lower
       for_each_acc<C1>(acc, [&](int r, int c, double v) { W[c * kWld + r] = v; });
       if (ts) sub_store<C1>(acc, p.top + ii, nb, 0, n0);  // top -= W (all loads first)
     }

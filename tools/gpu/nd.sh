@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_lu.py tests/test_gpu_qr.py -x -q > gpurun_out/nd_tests.log 2>&1; echo tests=$? >> gpurun_out/nd_tests.log
+for b in 1 14 28; do HG_PROF_BATCH=$b python tools/prof_batch.py; done > gpurun_out/prof_batch_nd.txt 2>&1
+HG_CONC=1,32 python tools/kind_throughput.py TSMQR UNMQR SSSSM GESSM > gpurun_out/kt_nd.jsonl 2>&1
+python bench.py --family lu --steps 3 --warmup 3 > gpurun_out/bench_lu_nd.json 2> gpurun_out/bench_lu_nd.err
+python bench.py --family qr --steps 3 --warmup 3 > gpurun_out/bench_qr_nd.json 2> gpurun_out/bench_qr_nd.err

@@ -36,6 +36,20 @@ __global__ void dfma_peak(double* out, int iters) {
 }
 
 template <class Cfg, int MINB = 1>
+__global__ void __launch_bounds__(Cfg::THREADS, MINB) gemm_nt_bench_nd(const double* A, const double* B, double* C, int nb) {
+  extern __shared__ double smem[];
+  size_t off = size_t(blockIdx.z) * nb * nb;
+  const double* a = A + off; const double* b = B + off; double* c = C + off;
+  int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
+  double acc[Cfg::FM][Cfg::FN][2];
+  hg::zero_acc<Cfg>(acc);
+  hg::TileLoader<Cfg, hg::M_MAJOR, Cfg::BM> la{a, nb, m0};
+  hg::TileLoader<Cfg, hg::M_MAJOR, Cfg::BN> lb{b, nb, n0};
+  hg::gemm_mainloop_nd<Cfg>(acc, smem, la, lb, 0, nb);
+  hg::sub_store<Cfg>(acc, c, nb, m0, n0);
+}
+
+template <class Cfg, int MINB = 1>
 __global__ void __launch_bounds__(Cfg::THREADS, MINB) gemm_nt_bench(const double* A, const double* B, double* C, int nb) {
   extern __shared__ double smem[];
   size_t off = size_t(blockIdx.z) * nb * nb;
@@ -66,17 +80,18 @@ __global__ void fill(double* p, size_t n, unsigned seed) {
   }
 }
 
-template <class Cfg, int MINB = 1>
+template <class Cfg, int MINB = 1, bool ND = false>
 void bench_cfg(const char* name, int nb, int batch) {
+  auto kern = ND ? gemm_nt_bench_nd<Cfg, MINB> : gemm_nt_bench<Cfg, MINB>;
   size_t n = size_t(nb) * nb * batch;
   double *A, *B, *C, *R;
   CK(cudaMalloc(&A, n * 8)); CK(cudaMalloc(&B, n * 8)); CK(cudaMalloc(&C, n * 8)); CK(cudaMalloc(&R, n * 8));
   fill<<<(n + 255) / 256, 256>>>(A, n, 1); fill<<<(n + 255) / 256, 256>>>(B, n, 2);
   fill<<<(n + 255) / 256, 256>>>(C, n, 3); CK(cudaMemcpy(R, C, n * 8, cudaMemcpyDeviceToDevice));
   size_t smem = hg::GemmSmem<Cfg, hg::M_MAJOR, hg::M_MAJOR>::BYTES;
-  CK(cudaFuncSetAttribute(gemm_nt_bench<Cfg, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid(nb / Cfg::BM, nb / Cfg::BN, batch);
-  gemm_nt_bench<Cfg, MINB><<<grid, Cfg::THREADS, smem>>>(A, B, C, nb);
+  kern<<<grid, Cfg::THREADS, smem>>>(A, B, C, nb);
   CK(cudaGetLastError());
   // correctness on batch 0 only
   gemm_nt_ref<<<dim3((nb + 127) / 128, nb), 128>>>(A, B, R, nb);
@@ -87,10 +102,10 @@ void bench_cfg(const char* name, int nb, int batch) {
   double md = 0, mx = 0;
   for (size_t i = 0; i < hc.size(); ++i) { md = fmax(md, fabs(hc[i] - hr[i])); mx = fmax(mx, fabs(hr[i])); }
   cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
-  for (int w = 0; w < 3; ++w) gemm_nt_bench<Cfg, MINB><<<grid, Cfg::THREADS, smem>>>(A, B, C, nb);
+  for (int w = 0; w < 3; ++w) kern<<<grid, Cfg::THREADS, smem>>>(A, B, C, nb);
   int reps = 10;
   CK(cudaEventRecord(e0));
-  for (int r = 0; r < reps; ++r) gemm_nt_bench<Cfg, MINB><<<grid, Cfg::THREADS, smem>>>(A, B, C, nb);
+  for (int r = 0; r < reps; ++r) kern<<<grid, Cfg::THREADS, smem>>>(A, B, C, nb);
   CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
   float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
   double flops = 2.0 * nb * double(nb) * nb * batch * reps;
@@ -119,16 +134,18 @@ int main() {
   }
   using C64 = hg::GemmCfg<64, 64, 16, 32, 32, 3>;
   using C64s4 = hg::GemmCfg<64, 64, 16, 32, 32, 4>;
-  using C128x64w64 = hg::GemmCfg<128, 64, 16, 64, 32, 3>;
-  using C64x128w64 = hg::GemmCfg<64, 128, 16, 32, 64, 3>;
-  using C128x128w64 = hg::GemmCfg<128, 128, 16, 64, 64, 3>;
+  using C64k8s4 = hg::GemmCfg<64, 64, 8, 32, 32, 4>;
+  using C64k8s3 = hg::GemmCfg<64, 64, 8, 32, 32, 3>;
+  using C64k32s3 = hg::GemmCfg<64, 64, 32, 32, 32, 3>;
   for (int batch : {32}) {
-    bench_cfg<C64, 1>("64x64x16_w32x32_s3_minb1", 1024, batch);
     bench_cfg<C64, 4>("64x64x16_w32x32_s3_minb4", 1024, batch);
-    bench_cfg<C64s4, 3>("64x64x16_w32x32_s4_minb3", 1024, batch);
-    bench_cfg<C128x64w64, 2>("128x64x16_w64x32_s3_minb2", 1024, batch);
-    bench_cfg<C64x128w64, 2>("64x128x16_w32x64_s3_minb2", 1024, batch);
-    bench_cfg<C128x128w64, 1>("128x128x16_w64x64_s3_minb1", 1024, batch);
+    bench_cfg<C64, 4, true>("ND_64x64x16_w32x32_s3_minb4", 1024, batch);
+    bench_cfg<C64s4, 3, true>("ND_64x64x16_w32x32_s4_minb3", 1024, batch);
+    bench_cfg<C64k8s4, 5, true>("ND_64x64x8_w32x32_s4_minb5", 1024, batch);
+    bench_cfg<C64k8s4, 4, true>("ND_64x64x8_w32x32_s4_minb4", 1024, batch);
+    bench_cfg<C64k8s3, 5, true>("ND_64x64x8_w32x32_s3_minb5", 1024, batch);
+    bench_cfg<C64k8s4, 5>("64x64x8_w32x32_s4_minb5", 1024, batch);
+    bench_cfg<C64k32s3, 2, true>("ND_64x64x32_w32x32_s3_minb2", 1024, batch);
   }
   return 0;
 }
