@@ -41,16 +41,20 @@ struct GemmNTParams {
   int lower;  // 1: update only C(i, j) with i >= j (SYRK)
 };
 
-__global__ void __launch_bounds__(CfgG::THREADS, 4) k_gemm_nt(GemmNTParams p) {  // 4 CTAs / SM (smem allows 4)
+using CfgG4 = GemmCfg<64, 64, 16, 32, 32, 4>;  // 4-stage ring, 3 CTAs / SM (default GEMM / SYRK tile)
+
+// CfgG: 3-stage ring, 4 CTAs / SM (smem allows 4)
+template <class G = CfgG, int MINB = 4>
+__global__ void __launch_bounds__(G::THREADS, MINB) k_gemm_nt(GemmNTParams p) {
   extern __shared__ double smem[];
-  const int m0 = blockIdx.x * CfgG::BM, n0 = blockIdx.y * CfgG::BN;
-  if (p.lower && m0 + CfgG::BM - 1 < n0) return;  // tile strictly above the diagonal
-  double acc[CfgG::FM][CfgG::FN][2];
-  zero_acc<CfgG>(acc);
-  TileLoader<CfgG, M_MAJOR, CfgG::BM> la{p.A, p.ld, m0};
-  TileLoader<CfgG, M_MAJOR, CfgG::BN> lb{p.B, p.ld, n0};
-  gemm_mainloop<CfgG>(acc, smem, la, lb, 0, p.K);
-  sub_store<CfgG>(acc, p.C, p.ld, m0, n0, p.lower != 0, false);
+  const int m0 = blockIdx.x * G::BM, n0 = blockIdx.y * G::BN;
+  if (p.lower && m0 + G::BM - 1 < n0) return;  // tile strictly above the diagonal
+  double acc[G::FM][G::FN][2];
+  zero_acc<G>(acc);
+  TileLoader<G, M_MAJOR, G::BM> la{p.A, p.ld, m0};
+  TileLoader<G, M_MAJOR, G::BN> lb{p.B, p.ld, n0};
+  gemm_mainloop<G>(acc, smem, la, lb, 0, p.K);
+  sub_store<G>(acc, p.C, p.ld, m0, n0, p.lower != 0, false);
 }
 
 // ---------------------------------------------------------------------------
@@ -890,7 +894,9 @@ static unsigned trsm_smem() { return (unsigned)GemmSmem<CfgG, M_MAJOR, K_MAJOR>:
   } while (0)
 
 bool init_chol_attributes() {
-  HG_ATTR(k_gemm_nt, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem());
+  HG_ATTR((k_gemm_nt<CfgG, 4>), cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem());
+  HG_ATTR((k_gemm_nt<CfgG4, 3>), cudaFuncAttributeMaxDynamicSharedMemorySize,
+          (int)(GemmSmem<CfgG4, M_MAJOR, M_MAJOR>::BYTES));
   HG_ATTR(k_trsm_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
   HG_ATTR(k_potrf_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPotrfDynDoubles * sizeof(double)));
   HG_ATTR(k_potrf_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -901,7 +907,15 @@ static void push_gemm(std::vector<LaunchDesc>& out, const double* A, const doubl
                       int ld, int M, int N, int K, int lower) {
   LaunchDesc d;
   GemmNTParams p{A, B, C, ld, M, N, K, lower};
-  d.set((const void*)k_gemm_nt, dim3(M / CfgG::BM, N / CfgG::BN), dim3(CfgG::THREADS), gemm_smem(), p);
+  static const bool four = [] {  // HG_GEMM_STAGES=3: the 3-stage, 4 CTAs / SM variant
+    const char* e = getenv("HG_GEMM_STAGES");
+    return !(e && e[0] == '3');
+  }();
+  if (four)
+    d.set((const void*)k_gemm_nt<CfgG4, 3>, dim3(M / CfgG::BM, N / CfgG::BN), dim3(CfgG::THREADS),
+          (unsigned)GemmSmem<CfgG4, M_MAJOR, M_MAJOR>::BYTES, p);
+  else
+    d.set((const void*)k_gemm_nt<CfgG, 4>, dim3(M / CfgG::BM, N / CfgG::BN), dim3(CfgG::THREADS), gemm_smem(), p);
   out.push_back(d);
 }
 
