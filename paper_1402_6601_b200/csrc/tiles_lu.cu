@@ -461,10 +461,22 @@ __device__ int lu_moves(const int* steps, int ii, int sb, bool ts, int* sp, int*
     for (int j = tid; j < sb; j += blockDim.x) {
       const int r = sp[j];
       if (r < 0) continue;
+      // one pass over the pivot list, 4 entries per LDS.128 (sp is 16-byte aligned, sb % 4 == 0)
       int jp = -1;
-      for (int k = 0; k < j; ++k) jp = (sp[k] == r) ? k : jp;
       bool last = true;
-      for (int k = j + 1; k < sb; ++k) last = last && (sp[k] != r);
+      if ((reinterpret_cast<uintptr_t>(sp) & 15) || (sb & 3)) {
+        for (int k = 0; k < j; ++k) jp = (sp[k] == r) ? k : jp;
+        for (int k = j + 1; k < sb; ++k) last = last && (sp[k] != r);
+      } else
+      for (int k = 0; k < sb; k += 4) {
+        const int4 q4 = *reinterpret_cast<const int4*>(sp + k);
+        const int qv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          jp = (k + u < j && qv[u] == r) ? k + u : jp;
+          last = last && !(k + u > j && qv[u] == r);
+        }
+      }
       int n = atomicAdd(cnt, last ? 2 : 1);
       mv_dst[n] = -1 - j;
       mv_src[n] = jp >= 0 ? -1 - jp : r;
@@ -1023,7 +1035,7 @@ k_lu_apply_strip(LuApplyParams p) {
       return code >= 0 ? bot + size_t(c) * nb + code : top + size_t(c) * nb + ii + (-1 - code);
     };
     // gather every moved value before any is written; 8 loads in flight per thread
-    constexpr int GU_ = 2048 / G::THREADS;  // loads in flight per thread
+    constexpr int GU_ = 4096 / G::THREADS;  // loads in flight per thread
     for (int e0 = tid; e0 < nm * BN; e0 += GU_ * G::THREADS) {
       double v[GU_];
 #pragma unroll
