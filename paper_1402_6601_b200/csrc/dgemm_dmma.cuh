@@ -249,6 +249,106 @@ HG_DEVICE void gemm_mainloop_nd(double (&acc)[Cfg::FM][Cfg::FN][2], double* smem
   __syncthreads();
 }
 
+// Producer/consumer variant of the M_MAJOR x M_MAJOR main loop: one thread
+// streams each k-slab with bulk copies (one per k-column: ROWS contiguous
+// doubles) that complete on the slot's `full` mbarrier; each warp releases a
+// slot by arriving on its `empty` mbarrier.  No CTA-wide barrier in the loop:
+// a warp only waits for the bytes it reads.  bars: 2 * STAGES uint64 in smem.
+// Measured SLOWER than gemm_mainloop_nd (30.4 vs 34.4 TF/s on 32 tiles,
+// profiles/r01_gemm_nd_variants.jsonl): 32 small (512 B) bulk copies per stage
+// from one thread; a 2D tensor map per operand would need tile-pool tensor maps
+// in the runtime.  Kept for tools/microbench.cu only.
+template <class Cfg>
+HG_DEVICE void gemm_mainloop_mb(double (&acc)[Cfg::FM][Cfg::FN][2], double* smem, uint64_t* bars,
+                                const double* __restrict__ A, int lda, int m0, const double* __restrict__ B, int ldb,
+                                int n0, int k_begin, int k_end) {
+  constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES, PAD = Cfg::PAD;
+  constexpr int WARPS = Cfg::THREADS / 32;
+  constexpr int A_SLAB = Cfg::slab_mmaj(Cfg::BM), B_SLAB = Cfg::slab_mmaj(Cfg::BN);
+  constexpr unsigned STAGE_BYTES = unsigned(BK * (Cfg::BM + Cfg::BN) * sizeof(double));
+  static_assert(BK % 8 == 0 && STAGES >= 2, "pipeline");
+  double* sA = smem;
+  double* sB = smem + STAGES * A_SLAB;
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
+  const int wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+  const int nk = (k_end - k_begin) / BK;
+  const bool producer = threadIdx.x == 0;
+  auto issue = [&](int s) {  // slab s into slot s % STAGES
+    const int slot = s % STAGES;
+    mbar_arrive_tx(&full[slot], STAGE_BYTES);
+    const int k0 = k_begin + s * BK;
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      bulk_g2s(sA + slot * A_SLAB + kk * (Cfg::BM + PAD), A + size_t(k0 + kk) * lda + m0,
+               Cfg::BM * sizeof(double), &full[slot]);
+      bulk_g2s(sB + slot * B_SLAB + kk * (Cfg::BN + PAD), B + size_t(k0 + kk) * ldb + n0,
+               Cfg::BN * sizeof(double), &full[slot]);
+    }
+  };
+  __syncthreads();  // previous users of this smem / barrier area are done
+  if (producer) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (producer)
+    for (int s = 0; s < STAGES && s < nk; ++s) issue(s);
+  double af[2][Cfg::FM], bf[2][Cfg::FN];
+  if (nk > 0) {
+    mbar_wait(&full[0], 0);
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i) af[0][i] = sA[t * (Cfg::BM + PAD) + wm + i * 8 + g];
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) bf[0][j] = sB[t * (Cfg::BN + PAD) + wn + j * 8 + g];
+  }
+  for (int it = 0; it < nk; ++it) {
+    const int slot = it % STAGES;
+    const double* a_s = sA + slot * A_SLAB;
+    const double* b_s = sB + slot * B_SLAB;
+    const int ns = (it + 1) % STAGES;
+    const double* a_n = sA + ns * A_SLAB;
+    const double* b_n = sB + ns * B_SLAB;
+    const bool more = it + 1 < nk;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      const int cur = (kk >> 2) & 1, nx = cur ^ 1;
+      if (kk + 4 < BK) {
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[nx][i] = a_s[(kk + 4 + t) * (Cfg::BM + PAD) + wm + i * 8 + g];
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) bf[nx][j] = b_s[(kk + 4 + t) * (Cfg::BN + PAD) + wn + j * 8 + g];
+      } else if (more) {
+        mbar_wait(&full[ns], ((it + 1) / STAGES) & 1);
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[nx][i] = a_n[t * (Cfg::BM + PAD) + wm + i * 8 + g];
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) bf[nx][j] = b_n[t * (Cfg::BN + PAD) + wn + j * 8 + g];
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    // refill the slot of slab it-1 (one slab of slack: its readers are long done)
+    if (producer && it >= 1 && it - 1 + STAGES < nk) {
+      const int ps = (it - 1) % STAGES;
+      mbar_wait(&empty[ps], ((it - 1) / STAGES) & 1);
+      issue(it - 1 + STAGES);
+    }
+  }
+  __syncthreads();
+}
+
 // Visit every accumulator element with its (row, col) inside the CTA tile.
 template <class Cfg, class F>
 HG_DEVICE void for_each_acc(double (&acc)[Cfg::FM][Cfg::FN][2], F&& f) {

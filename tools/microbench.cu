@@ -50,6 +50,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, MINB) gemm_nt_bench_nd(const dou
 }
 
 template <class Cfg, int MINB = 1>
+__global__ void __launch_bounds__(Cfg::THREADS, MINB) gemm_nt_bench_mb(const double* A, const double* B, double* C, int nb) {
+  extern __shared__ double smem[];
+  size_t off = size_t(blockIdx.z) * nb * nb;
+  const double* a = A + off; const double* b = B + off; double* c = C + off;
+  int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
+  double acc[Cfg::FM][Cfg::FN][2];
+  hg::zero_acc<Cfg>(acc);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + hg::GemmSmem<Cfg, hg::M_MAJOR, hg::M_MAJOR>::DOUBLES);
+  hg::gemm_mainloop_mb<Cfg>(acc, smem, bars, a, nb, m0, b, nb, n0, 0, nb);
+  hg::sub_store<Cfg>(acc, c, nb, m0, n0);
+}
+
+template <class Cfg, int MINB = 1>
 __global__ void __launch_bounds__(Cfg::THREADS, MINB) gemm_nt_bench(const double* A, const double* B, double* C, int nb) {
   extern __shared__ double smem[];
   size_t off = size_t(blockIdx.z) * nb * nb;
@@ -80,15 +93,15 @@ __global__ void fill(double* p, size_t n, unsigned seed) {
   }
 }
 
-template <class Cfg, int MINB = 1, bool ND = false>
+template <class Cfg, int MINB = 1, int ND = 0>
 void bench_cfg(const char* name, int nb, int batch) {
-  auto kern = ND ? gemm_nt_bench_nd<Cfg, MINB> : gemm_nt_bench<Cfg, MINB>;
+  auto kern = ND == 2 ? gemm_nt_bench_mb<Cfg, MINB> : (ND ? gemm_nt_bench_nd<Cfg, MINB> : gemm_nt_bench<Cfg, MINB>);
   size_t n = size_t(nb) * nb * batch;
   double *A, *B, *C, *R;
   CK(cudaMalloc(&A, n * 8)); CK(cudaMalloc(&B, n * 8)); CK(cudaMalloc(&C, n * 8)); CK(cudaMalloc(&R, n * 8));
   fill<<<(n + 255) / 256, 256>>>(A, n, 1); fill<<<(n + 255) / 256, 256>>>(B, n, 2);
   fill<<<(n + 255) / 256, 256>>>(C, n, 3); CK(cudaMemcpy(R, C, n * 8, cudaMemcpyDeviceToDevice));
-  size_t smem = hg::GemmSmem<Cfg, hg::M_MAJOR, hg::M_MAJOR>::BYTES;
+  size_t smem = hg::GemmSmem<Cfg, hg::M_MAJOR, hg::M_MAJOR>::BYTES + (ND == 2 ? 2 * Cfg::STAGES * 8 : 0);
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid(nb / Cfg::BM, nb / Cfg::BN, batch);
   kern<<<grid, Cfg::THREADS, smem>>>(A, B, C, nb);
@@ -138,14 +151,12 @@ int main() {
   using C64k8s3 = hg::GemmCfg<64, 64, 8, 32, 32, 3>;
   using C64k32s3 = hg::GemmCfg<64, 64, 32, 32, 32, 3>;
   for (int batch : {32}) {
-    bench_cfg<C64, 4>("64x64x16_w32x32_s3_minb4", 1024, batch);
-    bench_cfg<C64, 4, true>("ND_64x64x16_w32x32_s3_minb4", 1024, batch);
-    bench_cfg<C64s4, 3, true>("ND_64x64x16_w32x32_s4_minb3", 1024, batch);
-    bench_cfg<C64k8s4, 5, true>("ND_64x64x8_w32x32_s4_minb5", 1024, batch);
-    bench_cfg<C64k8s4, 4, true>("ND_64x64x8_w32x32_s4_minb4", 1024, batch);
-    bench_cfg<C64k8s3, 5, true>("ND_64x64x8_w32x32_s3_minb5", 1024, batch);
-    bench_cfg<C64k8s4, 5>("64x64x8_w32x32_s4_minb5", 1024, batch);
-    bench_cfg<C64k32s3, 2, true>("ND_64x64x32_w32x32_s3_minb2", 1024, batch);
+    bench_cfg<C64, 4, 1>("ND_64x64x16_w32x32_s3_minb4", 1024, batch);
+    bench_cfg<C64s4, 3, 1>("ND_64x64x16_w32x32_s4_minb3", 1024, batch);
+    bench_cfg<C64, 4, 2>("MB_64x64x16_w32x32_s3_minb4", 1024, batch);
+    bench_cfg<C64s4, 3, 2>("MB_64x64x16_w32x32_s4_minb3", 1024, batch);
+    bench_cfg<C64k8s4, 4, 2>("MB_64x64x8_w32x32_s4_minb4", 1024, batch);
+    bench_cfg<C64k32s3, 2, 2>("MB_64x64x32_w32x32_s3_minb2", 1024, batch);
   }
   return 0;
 }
