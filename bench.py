@@ -67,7 +67,15 @@ def dist_env():
 
 
 def load_model(H, args):
-    path = args.timings or os.path.join(ROOT, "timings", f"b200_nb{args.nb}_ib{args.ib}.csv")
+    """Throughput-calibrated B200 cost model by default (per-task GPU capacity time
+    under concurrency, tools/kind_throughput.py): its k=1 makespan predictions are
+    within 2-4% of measured runs; the latency-calibrated table (one task alone,
+    tools/calibrate.py) is the `_ib128.csv` file, selectable with --timings."""
+    path = args.timings
+    if not path:
+        path = os.path.join(ROOT, "timings", f"b200_nb{args.nb}_ib{args.ib}_tput.csv")
+        if not os.path.exists(path):
+            path = os.path.join(ROOT, "timings", f"b200_nb{args.nb}_ib{args.ib}.csv")
     if os.path.exists(path):
         return H.PerfModel(H.load_timing_table(path)), os.path.relpath(path, ROOT)
     return H.PerfModel(H.default_timing_table(args.nb, args.ib)), "hetsim default synthetic table"

@@ -45,7 +45,7 @@ def point(fam, n, nb, ib, k, sched_name, alpha, model):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_alpha_sweep.json"))
-    ap.add_argument("--timings", default=os.path.join(ROOT, "timings", "b200_nb1024_ib128.csv"))
+    ap.add_argument("--timings", default=os.path.join(ROOT, "timings", "b200_nb1024_ib128_tput.csv"))
     args = ap.parse_args()
     model = H.PerfModel(H.load_timing_table(args.timings))
     rows = []

@@ -3,7 +3,13 @@ on concurrent streams, as inside the DAG) of the sm_100a tile kernels.
 
     python tools/kind_throughput.py [KIND ...]   -> one JSON line per kind
 
-throughput_tflops = conc * reps * flops / wall; sm_eff = that / DMMA peak."""
+throughput_tflops = conc * reps * flops / wall; sm_eff = that / DMMA peak.
+
+    HG_TPUT_CSV=timings/b200_nb1024_ib128_tput.csv HG_CONC=32 python tools/kind_throughput.py
+also writes a THROUGHPUT-calibrated cost model in the reference's timing format
+(perfmodel.py:170-199): GPU seconds per task = wall / (conc * reps) at the
+largest concurrency, i.e. the share of one B200 a task occupies when the DAG
+keeps the GPU full (the CPU column is copied from the latency-calibrated file)."""
 import ctypes as C
 import json
 import os
@@ -59,6 +65,7 @@ def operands(kind, conc):
     return sets
 
 
+results = []
 for kind in kinds:
     res = {"kind": kind}
     flops = H.kind_flops(kind, nb) if hasattr(H, "kind_flops") else None
@@ -99,4 +106,26 @@ for kind in kinds:
     if "tflops_conc8" in res and "peak" not in res:
         res["sm_eff_conc8"] = res["tflops_conc8"] / peak
     res["peak"] = peak
+    cmax = max(int(c) for c in os.environ.get("HG_CONC", "1,8").split(","))
+    res["capacity_s"] = flops / (res[f"tflops_conc{cmax}"] * 1e12)
     print(json.dumps(res), flush=True)
+    results.append(res)
+
+csv_out = os.environ.get("HG_TPUT_CSV")
+if csv_out:
+    lat = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "timings",
+                       f"b200_nb{nb}_ib{ib}.csv")
+    cpu = {}
+    for line in open(lat):
+        if line.startswith("#") or not line.strip():
+            continue
+        k, cls, sec = line.strip().split(",")
+        if cls == "CPU":
+            cpu[k] = sec
+    with open(csv_out, "w") as f:
+        f.write(f"# B200 (sm_100a) per-task GPU capacity time under concurrency (HG_CONC max streams), nb={nb} "
+                f"ib={ib}; CPU column from {os.path.basename(lat)}; written by tools/kind_throughput.py\n")
+        for r in results:
+            f.write(f"{r['kind']},GPU,{r['capacity_s']!r}\n")
+            if r["kind"] in cpu:
+                f.write(f"{r['kind']},CPU,{cpu[r['kind']]}\n")
