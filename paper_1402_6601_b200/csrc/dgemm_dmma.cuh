@@ -18,16 +18,24 @@ namespace hg {
 
 enum Layout { M_MAJOR = 0, K_MAJOR = 1 };
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+// KSWZ: K_MAJOR slabs unpadded (rows of BK = 8 doubles) with the k index XOR-swizzled
+// by bit 1 of the row, conflict-free for the fragment loads at 2/3 of the padded size.
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, bool KSWZ_ = false>
 struct GemmCfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr bool KSWZ = KSWZ_;
+  static_assert(!KSWZ_ || BK_ == 8, "swizzled K_MAJOR slabs are 8 doubles wide");
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;
   static constexpr int FM = WM / 8, FN = WN / 8;  // 8x8 fragments per warp
   static constexpr int PAD = 4;
   // smem footprint of one operand slab for each layout
   __host__ __device__ static constexpr int slab_mmaj(int rows) { return BK * (rows + PAD); }
-  __host__ __device__ static constexpr int slab_kmaj(int rows) { return rows * (BK + PAD); }
+  __host__ __device__ static constexpr int slab_kmaj(int rows) { return rows * (KSWZ ? BK : BK + PAD); }
+  // smem index of K_MAJOR slab element (row r, k)
+  __host__ __device__ static constexpr int kmaj(int r, int k) {
+    return KSWZ ? r * BK + (k ^ (((r >> 1) & 1) << 2)) : r * (BK + PAD) + k;
+  }
 };
 
 template <class Cfg, int LA, int LB>
@@ -70,12 +78,12 @@ HG_DEVICE void load_slab(double* s, const double* __restrict__ g, int ld, int r0
       for (int i = 0; i < CHUNKS / Cfg::THREADS; ++i) {
         const int c = threadIdx.x + i * Cfg::THREADS;
         const int rr = c / CH_PER_R, kk = (c % CH_PER_R) * 2;
-        cp_async16(s + rr * (BK + PAD) + kk, gb + size_t(rr) * ld + kk);
+        cp_async16(s + Cfg::kmaj(rr, kk), gb + size_t(rr) * ld + kk);
       }
     } else {
       for (int c = threadIdx.x; c < CHUNKS; c += Cfg::THREADS) {
         int rr = c / CH_PER_R, kk = (c % CH_PER_R) * 2;
-        cp_async16(s + rr * (BK + PAD) + kk, g + size_t(r0 + rr) * ld + k0 + kk);
+        cp_async16(s + Cfg::kmaj(rr, kk), g + size_t(r0 + rr) * ld + k0 + kk);
       }
     }
   }
@@ -84,7 +92,7 @@ HG_DEVICE void load_slab(double* s, const double* __restrict__ g, int ld, int r0
 template <class Cfg, int L, int ROWS>
 HG_DEVICE double frag_at(const double* s, int r, int k) {
   if constexpr (L == M_MAJOR) return s[k * (ROWS + Cfg::PAD) + r];
-  else return s[r * (Cfg::BK + Cfg::PAD) + k];
+  else return s[Cfg::kmaj(r, k)];
 }
 
 // Standard operand loader: a (ROWS x k) window of a tile addressed by layout.

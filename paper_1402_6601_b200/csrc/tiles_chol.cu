@@ -829,7 +829,7 @@ struct MRowLoader {  // rows j in [j0, j0+ROWS): element (j, k) = M(j, k)
       if (k < j) v = __ldcg(L + size_t(j) * ld + k);
       else if (k == j) v = 1.0 / __ldcg(L + size_t(j) * ld + j);
       else v = 0.0;
-      s[rr * (Cfg::BK + Cfg::PAD) + kk] = v;
+      s[Cfg::kmaj(rr, kk)] = v;
     }
   }
 };

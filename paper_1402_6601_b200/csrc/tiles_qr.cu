@@ -302,7 +302,7 @@ using CfgQ64 = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps; requires sb == 128
 using CfgQ32 = GemmCfg<128, 32, 16, 32, 16, 3>;  // 8 warps (32x16 warp tiles)
 using CfgQ16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
 using CfgQ4w = GemmCfg<128, 32, 8, 32, 32, 4>;    // 4 warps of 32x32: C -= V W stream (3 CTAs / SM)
-using CfgQ4w1 = GemmCfg<128, 32, 8, 32, 32, 2>;   //   and its W = V^T C / T^T W phases
+using CfgQ4w1 = GemmCfg<128, 32, 8, 32, 32, 3, true>;  //   and its W = V^T C / T^T W phases (swizzled K_MAJOR ring)
 constexpr int kWld = kQrMaxSb + 4;  // W stored [n][k]
 
 // Unit-lower reflector block V of panel ii, element (tile row tr, panel col pc):
@@ -331,7 +331,7 @@ struct VLoader {
     }
     for (int e = threadIdx.x; e < ROWS * BK; e += Cfg::THREADS) {
       int rr = e / BK, kk = e % BK;
-      if (L == K_MAJOR) s[rr * (BK + PAD) + kk] = val(k0 + kk, r0 + rr);
+      if (L == K_MAJOR) s[Cfg::kmaj(rr, kk)] = val(k0 + kk, r0 + rr);
       else s[kk * (ROWS + PAD) + rr] = val(r0 + rr, k0 + kk);
     }
   }
