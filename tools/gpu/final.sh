@@ -1,6 +1,8 @@
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?; tail -1 gpurun_out/smoke.log
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests_all.log 2>&1; echo tests=$?; tail -1 gpurun_out/gpu_tests_all.log
-timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo bench=$?
-tail -1 gpurun_out/bench_full.log | cut -c1-300
-for f in lu qr; do timeout 900 python bench.py --family $f --steps 3 --no-cpu-baseline > gpurun_out/bench_full_$f.log 2>&1; echo $f=$?; tail -1 gpurun_out/bench_full_$f.log | cut -c1-200; done
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/final_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/final_tests.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke.log 2>&1
+python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err
+python bench.py --impl reference > gpurun_out/final_bench_ref.json 2> gpurun_out/final_bench_ref.err
+python bench.py --family lu --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/final_bench_lu.json 2> /dev/null
+python bench.py --family qr --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/final_bench_qr.json 2> /dev/null
