@@ -803,11 +803,15 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
 // 64x64 block X(I, J) = sum_{K <= J} B(I, K) M(J, K)^T.  In place: X(I, J)
 // may only be written once every CTA of row strip I has finished reading B,
 // so each CTA computes two blocks (J, nJ-1-J: equal work), then meets the
-// other CTAs of its strip on a self-advancing counter, then writes.
+// other CTAs of its strip at a cluster barrier, then writes.  The P CTAs of a
+// strip form one thread-block cluster, which the hardware makes co-resident
+// all-or-nothing: a global-memory strip barrier could deadlock once many TRSMs
+// run at once (63 concurrent TRSMs at N=65536 leave every SM slot spinning on a
+// strip whose remaining CTAs cannot be scheduled).
 struct TrsmInvParams {
   const double* L;  // diagonal tile after POTRF (M^T in its upper triangle)
   double* B;
-  int* count;       // [2*nI] per-task scratch (arrivals, departures per strip)
+  int* count;       // per-task scratch (unused since the strip barrier became a cluster barrier)
   int ld;
 };
 
@@ -834,17 +838,11 @@ struct MRowLoader {  // rows j in [j0, j0+ROWS): element (j, k) = M(j, k)
   }
 };
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__global__ void __launch_bounds__(CfgG::THREADS, 3) k_trsm_inv(TrsmInvParams p) {
+template <int P>
+__global__ void __cluster_dims__(P, 1, 1) __launch_bounds__(CfgG::THREADS, 3) k_trsm_inv(TrsmInvParams p) {
   extern __shared__ double smem[];
-  const int ld = p.ld, nI = ld / kR, nJ = ld / kR, P = nJ / 2;
-  // strip-major ids: the P CTAs that meet on a strip counter are dispatched
-  // consecutively, so at most one strip per kernel is ever partially resident
+  const int ld = p.ld, nJ = ld / kR;
+  // strip-major ids: the P CTAs of row strip I are one cluster (rank = pair)
   const int I = blockIdx.x / P, pair = blockIdx.x % P;
   const int Js[2] = {pair, nJ - 1 - pair};
   double acc0[CfgG::FM][CfgG::FN][2], acc1[CfgG::FM][CfgG::FN][2];
@@ -859,25 +857,12 @@ __global__ void __launch_bounds__(CfgG::THREADS, 3) k_trsm_inv(TrsmInvParams p) 
     MRowLoader<CfgG, kR> lb{p.L, ld, Js[1] * kR};
     gemm_mainloop<CfgG>(acc1, smem, la, lb, 0, (Js[1] + 1) * kR);
   }
-  // all reads of B by this CTA are complete (mainloop ends with wait_group 0 + barrier).
-  // Strip barrier on two counters (arrivals, departures): the last CTA to depart
-  // resets both, so the scratch is clean for the next run whatever its shape.
-  if (threadIdx.x == 0) {
-    int* arr = p.count + 2 * I;
-    atomicAdd(arr, 1);
-    while (ld_acquire(arr) < P) __nanosleep(32);
-  }
-  __syncthreads();
+  // all reads of B by this CTA are complete (mainloop ends with wait_group 0 + barrier);
+  // the cluster barrier (release / acquire) extends that to the whole strip
+  cg::this_cluster().sync();
   double* B = p.B;
   for_each_acc<CfgG>(acc0, [&](int r, int c, double v) { B[size_t(Js[0] * kR + c) * ld + I * kR + r] = v; });
   for_each_acc<CfgG>(acc1, [&](int r, int c, double v) { B[size_t(Js[1] * kR + c) * ld + I * kR + r] = v; });
-  if (threadIdx.x == 0) {
-    int* arr = p.count + 2 * I;
-    if (atomicAdd(arr + 1, 1) == P - 1) {  // every CTA of the strip has passed its wait
-      atomicExch(arr, 0);
-      atomicExch(arr + 1, 0);
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -897,7 +882,9 @@ bool init_chol_attributes() {
   HG_ATTR((k_gemm_nt<CfgG, 4>), cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem());
   HG_ATTR((k_gemm_nt<CfgG4, 3>), cudaFuncAttributeMaxDynamicSharedMemorySize,
           (int)(GemmSmem<CfgG4, M_MAJOR, M_MAJOR>::BYTES));
-  HG_ATTR(k_trsm_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
+  HG_ATTR(k_trsm_inv<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
+  HG_ATTR(k_trsm_inv<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
+  HG_ATTR(k_trsm_inv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
   HG_ATTR(k_potrf_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPotrfDynDoubles * sizeof(double)));
   HG_ATTR(k_potrf_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return true;
@@ -944,13 +931,15 @@ bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc
         set_error("TRSM needs per-task scratch (%d ints)", 2 * nJ);
         return false;
       }
-      if (nJ % 2) {
-        set_error("TRSM needs an even number of 64-blocks per tile (nb=%d)", nb);
+      const int P = nJ / 2;  // CTAs per row strip = cluster size
+      if (nJ % 2 || (P != 2 && P != 4 && P != 8)) {
+        set_error("TRSM needs nb in {256, 512, 1024} (nb=%d)", nb);
         return false;
       }
       LaunchDesc d;
       TrsmInvParams tp{o.t[0], o.t[1], o.scratch, nb};
-      d.set((const void*)k_trsm_inv, dim3(nJ * (nJ / 2)), dim3(CfgG::THREADS), trsm_smem(), tp);
+      const void* f = P == 8 ? (const void*)k_trsm_inv<8> : (P == 4 ? (const void*)k_trsm_inv<4> : (const void*)k_trsm_inv<2>);
+      d.set(f, dim3(nJ * P), dim3(CfgG::THREADS), trsm_smem(), tp);
       out.push_back(d);
       return true;
     }
