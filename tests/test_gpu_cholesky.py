@@ -107,3 +107,28 @@ def test_cholesky_two_nodes_peer_jobs():
     assert stats.bytes_d2d == plan.bytes_d2d
     assert stats.bytes_h2d == plan.bytes_h2d
     assert _rel(L, Lo) < TOL
+
+
+@pytest.mark.timeout(600)
+def test_cholesky_nt64_many_concurrent_trsms():
+    """nt = 64 (N=32768, nb=512), the DAG shape of the N=65536 bench that once hung:
+    after POTRF(0) 63 TRSMs are ready at once (with a global-memory strip barrier their
+    spinning CTAs could fill every SM slot; TRSM strips are thread-block clusters now).
+    The run must finish and factor correctly (randomized residual, O(n^2))."""
+    psutil = pytest.importorskip("psutil")
+    if psutil.virtual_memory().available < 48e9:
+        pytest.skip("needs ~25 GB of free host memory")
+    n, b = 32768, 512
+    g = H.gen_cholesky(n // b, b)
+    plat = H.build_platform(1, 1, 1, link_bandwidth=6e11, link_latency=3e-6, switch_cap=float("inf"), p2p=True)
+    A = O.spd_matrix(n, 3)
+    img = runtime.to_tile_major(A, g)
+    plan, stats, out = runtime.execute(g, plat, H.make_scheduler("dada", alpha=0.5, cp=True),
+                                       H.PerfModel(H.default_timing_table(b, 128)), img)
+    del img
+    assert stats.bytes_h2d == plan.bytes_h2d
+    L = np.tril(runtime.from_tile_major(out, g))
+    x = np.random.default_rng(4).standard_normal(n)
+    ax = A @ x
+    res = np.linalg.norm(ax - L @ (L.T @ x)) / np.linalg.norm(ax)
+    assert res < 1e-14, res
