@@ -490,6 +490,15 @@ static std::vector<int> task_priorities(const hg_exec* ex, int dev) {
   return prio;
 }
 
+// HG_URGENT=1: zero-slack tasks use the low-latency variant of their kind (experiment)
+static bool urgent_variants() {
+  static const bool v = [] {
+    const char* e = getenv("HG_URGENT");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 static int build_graph(hg_exec* ex) {
   const int n = ex->n_tasks;
   const Partition part = partition(ex);
@@ -511,6 +520,11 @@ static int build_graph(hg_exec* ex) {
   }
   const std::vector<int> prio = task_priorities(ex, 0);
   const bool use_prio = ex->priority_levels > 0 && !ex->task_weight.empty();
+  int prio_greatest = 0;
+  {
+    int least = 0;
+    if (cudaDeviceGetStreamPriorityRange(&least, &prio_greatest) != cudaSuccess) cudaGetLastError();
+  }
 
   // Delivery of a block version to a node: a task must wait for the copy job
   // that brought the version it reads to its node, even when that job was
@@ -685,6 +699,7 @@ static int build_graph(hg_exec* ex) {
       return HG_EINVAL;
     }
     for (int64_t a = a0; a < a1; ++a) ops.t[ops.n_t++] = ex->slot_ptr(node, ex->acc_block[a]);
+    ops.urgent = (use_prio && urgent_variants() && prio[t] == prio_greatest) ? 1 : 0;
     launches.clear();
     if (!build_task_launches(ex->task_kind[t], ops, launches)) return HG_EINVAL;
     deps.clear();

@@ -40,6 +40,8 @@ struct TaskOperands {
   int* status = nullptr;  // device word; kernels OR error bits into it
   int* scratch = nullptr; // per-task device ints (task_scratch_ints), zero-initialised once;
                           // kernels keep them self-consistent across runs
+  int urgent = 0;         // 1: the task has (near) zero slack in the DAG (runtime priority level 0):
+                          // kinds with a latency/throughput trade-off pick their low-latency variant
 };
 
 // Device ints of per-task scratch a kind needs (0 for most kinds).

@@ -1316,14 +1316,14 @@ bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
     }
     case K_GESSM:
       if (use_cluster_apply(nb, ib)) {
-        push_apply_cl(out, o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF);
+        push_apply_cl(out, o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF, o.urgent ? 16 : 32);
         return true;
       }
       for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[1], nb, P, 0, LU_GETRF);
       return true;
     case K_SSSSM:
       if (use_cluster_apply(nb, ib)) {
-        push_apply_cl(out, o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF);
+        push_apply_cl(out, o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF, o.urgent ? 16 : 32);
         return true;
       }
       for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[2], nb, P, 0, LU_TSTRF);

@@ -1024,10 +1024,10 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
       return true;
     }
     case K_UNMQR:
-      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], nullptr, nb, ib, 0, np, 0, QR_GEQRT}, 32);
+      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], nullptr, nb, ib, 0, np, 0, QR_GEQRT}, o.urgent ? 16 : 32);
       return true;
     case K_TSMQR:
-      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, QR_TSQRT}, 32);
+      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, QR_TSQRT}, o.urgent ? 16 : 32);
       return true;
     default:
       set_error("kind %d is not a QR kind", kind);
