@@ -230,7 +230,9 @@ int hg_tile_run(int32_t kind, int32_t device, void* stream, double* const* t, in
                 int32_t nb, int32_t ib, int32_t* status_dev);
 /* the same with caller-owned scratch (hg_task_scratch_ints(kind, nb, ib) ints on the device,
  * zeroed once): independent tasks may then run concurrently on different streams
- * (the online executor, paper_1402_6601_b200/online.py) */
+ * (the online executor, paper_1402_6601_b200/online.py).  No kernel of this build
+ * needs scratch any more (the TRSM strip barrier is a cluster barrier); the size
+ * query stays so callers remain valid if a kind needs it again. */
 int hg_tile_run_scratch(int32_t kind, int32_t device, void* stream, double* const* t, int32_t n_t,
                         int32_t nb, int32_t ib, int32_t* status_dev, int32_t* scratch_dev);
 int hg_task_scratch_ints(int32_t kind, int32_t nb, int32_t ib);
