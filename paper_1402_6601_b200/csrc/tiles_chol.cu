@@ -811,7 +811,7 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
 struct TrsmInvParams {
   const double* L;  // diagonal tile after POTRF (M^T in its upper triangle)
   double* B;
-  int* count;       // per-task scratch (unused since the strip barrier became a cluster barrier)
+  int* count;       // unused (the strip barrier is a cluster barrier); kept for the param layout
   int ld;
 };
 
@@ -907,7 +907,9 @@ static void push_gemm(std::vector<LaunchDesc>& out, const double* A, const doubl
 }
 
 int chol_scratch_ints(int kind, int nb) {
-  return kind == K_TRSM ? 2 * (nb / kR) : 0;
+  (void)kind;
+  (void)nb;
+  return 0;  // the TRSM strip barrier is a cluster barrier: no per-task counters
 }
 
 bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out) {
@@ -927,10 +929,6 @@ bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc
       return true;
     }
     case K_TRSM: {
-      if (!o.scratch) {
-        set_error("TRSM needs per-task scratch (%d ints)", 2 * nJ);
-        return false;
-      }
       const int P = nJ / 2;  // CTAs per row strip = cluster size
       if (nJ % 2 || (P != 2 && P != 4 && P != 8)) {
         set_error("TRSM needs nb in {256, 512, 1024} (nb=%d)", nb);
