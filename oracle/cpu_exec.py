@@ -1,22 +1,38 @@
 """ORACLE -- test infrastructure / CPU baseline only, never a product path.
 
 The reference's CPU path for a tile factorization, restated: the same tile
-DAG (kernels.py:112-212) executed by ``threads`` host workers running the
-oracle's SciPy/OpenBLAS tile kernels (oracle/tiles.py), one BLAS thread per
-worker (threadpoolctl), dynamic list scheduling in task-id priority.  Used
-by ``bench.py`` for ``cpu_baseline`` and the ``--impl reference`` arm.
+DAG (/root/reference/pkg/src/hetsim/kernels.py:112-212) executed by ``workers``
+host PROCESSES running the oracle's SciPy/OpenBLAS/NumPy tile kernels
+(oracle/tiles.py, oracle/tiles_lu_qr.py), one BLAS thread each, with dynamic
+list scheduling in task-id priority (the reference engine's ready order,
+sim.py:375-382, without its simulated clock).
+
+Why processes: SciPy's f2py BLAS/LAPACK wrappers hold the GIL, so a thread
+pool of them runs at roughly one core (measured: 1 / 4 / 8 threads of
+``blas.dgemm`` on 1024^2 tiles = 37.6 / 39.6 / 39.4 GF/s).  Here every worker
+is a forked process; tiles and the LU/QR side areas (IPIV, dL, T) live in one
+anonymous ``MAP_SHARED`` arena created before the fork, so workers update
+them in place and the parent only ships task ids over pipes.  The arena is
+not a /dev/shm segment, so container shm limits do not apply.
+
+Used by ``tests/`` (full-size parity references), ``bench.py``'s
+``cpu_baseline`` and its ``--impl reference`` arm.
 """
 
 from __future__ import annotations
 
 import heapq
+import mmap
+import multiprocessing as mp
 import os
-import threading
 import time
+import traceback
+from multiprocessing.connection import wait as mp_wait
 
 import numpy as np
 
 from . import tiles as O
+from . import tiles_lu_qr as LQ
 
 
 def host_threads() -> int:
@@ -26,69 +42,179 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def run_dag(graph, tiles: dict, threads: int) -> float:
-    """Execute every task of ``graph`` on ``tiles`` with ``threads`` workers; returns seconds."""
+class TileArena:
+    """Tiles of a tile-layout graph (+ LU/QR side areas) in one shared anonymous mapping.
+
+    Per tile block d: ``tiles[d]`` (b x b, Fortran order), and for LU/QR
+    ``aux[d]`` (ib x b: dL for LU, T for QR) and ``piv[d]`` (b pivots stored as
+    float64, exact for integers).
+    """
+
+    def __init__(self, graph):
+        lay = graph.layout
+        self.layout = lay
+        self.family = lay.family
+        b, ib = lay.b, lay.ib
+        self.ids = sorted(lay.tiles)
+        side = 0 if self.family == "cholesky" else ib * b + b
+        per = b * b + side
+        self._mm = mmap.mmap(-1, max(1, len(self.ids) * per * 8))  # MAP_SHARED | MAP_ANONYMOUS
+        buf = np.frombuffer(self._mm, np.float64)
+        self.tiles, self.aux, self.piv = {}, {}, {}
+        for i, d in enumerate(self.ids):
+            o = i * per
+            self.tiles[d] = buf[o:o + b * b].reshape(b, b, order="F")
+            if side:
+                self.aux[d] = buf[o + b * b:o + b * b + ib * b].reshape(ib, b, order="F")
+                self.piv[d] = buf[o + b * b + ib * b:o + per]
+
+    def load(self, A: np.ndarray):
+        b = self.layout.b
+        for d in self.ids:
+            i, j = self.layout.tiles[d]
+            self.tiles[d][...] = A[i * b:(i + 1) * b, j * b:(j + 1) * b]
+        return self
+
+    def side(self) -> dict:
+        """The side areas in oracle.tiles_lu_qr's dict form (for its lu_solve / qr_apply_qt)."""
+        if self.family == "lu":
+            return {d: {"ipiv": self.piv[d].astype(np.int64), "dl": self.aux[d]} for d in self.ids}
+        if self.family == "qr":
+            return {d: {"t": self.aux[d]} for d in self.ids}
+        return {}
+
+
+def run_task(arena: TileArena, task):
+    """One oracle tile kernel on the arena (kernels.py access lists)."""
+    lay = arena.layout
+    T = arena.tiles
+    ids = [d for d, _ in task.accesses if d in lay.tiles]
+    kind, ib = task.kind, lay.ib
+    if arena.family == "cholesky":
+        O.CHOLESKY[kind](*[T[d] for d in ids])
+    elif kind == "GETRF_INC":
+        ipiv, _ = LQ.getrf_inc(T[ids[0]], ib)
+        arena.piv[ids[0]][:] = ipiv
+    elif kind == "GESSM":
+        LQ.gessm(T[ids[0]], arena.piv[ids[0]].astype(np.int64), T[ids[1]], ib)
+    elif kind == "TSTRF":
+        ipiv, dl, _ = LQ.tstrf(T[ids[0]], T[ids[1]], ib)
+        arena.piv[ids[1]][:] = ipiv
+        arena.aux[ids[1]][...] = dl
+    elif kind == "SSSSM":
+        a = ids[0]
+        LQ.ssssm(T[a], arena.piv[a].astype(np.int64), arena.aux[a], T[ids[1]], T[ids[2]], ib)
+    elif kind == "GEQRT":
+        t = LQ.geqrt(T[ids[0]], ib)
+        arena.aux[ids[0]][:t.shape[0], :t.shape[1]] = t
+    elif kind == "UNMQR":
+        LQ.unmqr(T[ids[0]], arena.aux[ids[0]], T[ids[1]])
+    elif kind == "TSQRT":
+        t = LQ.tsqrt(T[ids[0]], T[ids[1]], ib)
+        arena.aux[ids[1]][:t.shape[0], :t.shape[1]] = t
+    elif kind == "TSMQR":
+        LQ.tsmqr(T[ids[0]], arena.aux[ids[0]], T[ids[1]], T[ids[2]])
+    else:
+        raise ValueError(f"oracle: unknown kind {kind}")
+
+
+_CTX = {}  # inherited by forked workers
+
+
+def _worker(conn):
     from threadpoolctl import threadpool_limits
 
-    n = len(graph)
-    left = graph.in_degrees()
-    ready = [t for t in range(n) if left[t] == 0]
-    heapq.heapify(ready)
-    lock = threading.Condition()
-    done = [0]
-    err = []
-    fam = graph.layout.family
-    side = {}
-
-    def work():
+    graph, arena = _CTX["graph"], _CTX["arena"]
+    with threadpool_limits(1):
+        conn.send("ready")
         while True:
-            with lock:
-                while not ready and done[0] < n and not err:
-                    lock.wait()
-                if done[0] >= n or err:
-                    return
-                tid = heapq.heappop(ready)
+            tid = conn.recv()
+            if tid is None:
+                break
             try:
-                t = graph.tasks[tid]
-                if fam == "cholesky":
-                    O.CHOLESKY[t.kind](*[tiles[d] for d, _ in t.accesses])
-                else:
-                    from . import tiles_lu_qr
+                run_task(arena, graph.tasks[tid])
+                conn.send(tid)
+            except Exception:
+                conn.send(("error", tid, traceback.format_exc()))
+                break
+    conn.close()
 
-                    ids = [d for d, _ in t.accesses if d in graph.layout.tiles]
-                    tiles_lu_qr.KERNELS[fam][t.kind](graph.layout, ids, tiles, side)
-            except Exception as e:  # surface in the caller
-                with lock:
-                    err.append(e)
-                    lock.notify_all()
-                return
-            with lock:
-                done[0] += 1
-                for s in graph.successors(tid):
+
+def run_dag(graph, arena: TileArena, workers: int | None = None) -> float:
+    """Execute every task of ``graph`` on ``arena`` with ``workers`` forked processes
+    (default: every core in this process's affinity mask); returns the seconds
+    from the first dispatch to the last completion (worker start-up excluded)."""
+    workers = max(1, workers or host_threads())
+    n = len(graph)
+    ctx = mp.get_context("fork")
+    _CTX["graph"], _CTX["arena"] = graph, arena
+    procs, conns = [], []
+    try:
+        for _ in range(workers):
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_worker, args=(b,), daemon=True)
+            p.start()
+            b.close()
+            procs.append(p)
+            conns.append(a)
+    finally:
+        _CTX.clear()
+    try:
+        for c in conns:
+            if c.recv() != "ready":
+                raise RuntimeError("oracle worker failed to start")
+        left = graph.in_degrees()
+        ready = [t for t in range(n) if left[t] == 0]
+        heapq.heapify(ready)
+        idle = list(range(workers))
+        busy = {}
+        done = 0
+        t0 = time.perf_counter()
+        while done < n:
+            while ready and idle:
+                w = idle.pop()
+                tid = heapq.heappop(ready)
+                conns[w].send(tid)
+                busy[conns[w]] = w
+            if not busy:
+                raise RuntimeError("oracle DAG executor: no ready task and nothing running (cycle?)")
+            for c in mp_wait(list(busy)):
+                msg = c.recv()
+                if isinstance(msg, tuple):
+                    raise RuntimeError(f"oracle task {msg[1]} failed:\n{msg[2]}")
+                done += 1
+                for s in graph.successors(msg):
                     left[s] -= 1
                     if left[s] == 0:
                         heapq.heappush(ready, s)
-                lock.notify_all()
+                idle.append(busy.pop(c))
+        secs = time.perf_counter() - t0
+    finally:
+        for c in conns:
+            try:
+                c.send(None)
+            except (OSError, BrokenPipeError):
+                pass
+        for p in procs:
+            p.join(timeout=10)
+            if p.is_alive():
+                p.kill()
+    return secs
 
-    t0 = time.perf_counter()
-    with threadpool_limits(1):
-        pool = [threading.Thread(target=work) for _ in range(threads)]
-        for th in pool:
-            th.start()
-        for th in pool:
-            th.join()
-    if err:
-        raise err[0]
-    return time.perf_counter() - t0
+
+def factor(graph, A: np.ndarray, workers: int | None = None):
+    """Tile factorization of the dense matrix ``A`` by the oracle: returns (arena, seconds)."""
+    arena = TileArena(graph).load(A)
+    secs = run_dag(graph, arena, workers)
+    return arena, secs
 
 
-def cholesky_sample(n: int, nb: int, threads: int, seed: int = 0):
+def cholesky_sample(n: int, nb: int, workers: int, seed: int = 0):
     """One bounded CPU factorization; returns (seconds, flops, residual)."""
     import paper_1402_6601_b200 as H
 
     g = H.gen_cholesky(n // nb, nb)
     A = O.spd_matrix(n, seed)
-    T = O.tiles_of(A, g.layout)
-    secs = run_dag(g, T, threads)
-    L = O.assemble(T, g.layout, lower_only=True)
+    arena, secs = factor(g, A, workers)
+    L = O.assemble(arena.tiles, g.layout, lower_only=True)
     return secs, H.flops_of("cholesky", n), O.cholesky_residual(A, L)

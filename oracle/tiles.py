@@ -10,8 +10,11 @@ Parity status: the reference package has NO numerics ("numerical
 correctness of factorizations" is out of scope; sim.py only sleeps
 ``true_exec``), so numeric parity is **unpinned at the reference**.  This
 oracle is pinned instead against the LAPACK monolithic factorizations on the
-same matrices (tests/test_oracle_numeric.py: tile Cholesky == dpotrf, tile QR's
-R == dgeqrf's R up to row signs, tile LU residuals at LAPACK level).
+same matrices, hand-traced core_dtstrf cases and an independent scalar-loop
+restatement of core_dtstrf / core_dssssm (tests/test_oracle_numeric.py: tile
+Cholesky == dpotrf, tile QR's R == LAPACK's R up to row signs with Q^T
+orthogonal, GETRF_INC pivots/U == dgetrf's, TSTRF/SSSSM == the scalar PLASMA
+restatement, tile LU-incpiv solve residual at LAPACK level).
 
 Tiles are ``b x b`` float64 arrays in Fortran order (PLASMA column-major).
 """
