@@ -15,8 +15,14 @@ Timing: W untimed warm-up steps, then K steps bracketed by barrier +
 cudaDeviceSynchronize, CUDA events on the launching stream, max over ranks.
 Inputs (4.4 GB of tiles) exceed L2 (126 MB), so no explicit flush.
 
-``--impl reference`` times the reference's CPU path (the oracle's tile DAG
-on the host's cores, oracle/cpu_exec.py) on a bounded sample.
+``--impl reference`` times the reference's CPU path on the host's cores: the
+configured workload's tile DAG executed by the oracle's tile kernels on one
+forked worker process per core (oracle/cpu_exec.py; GIL-free), the whole
+N=--n factorization run exactly once, split into K flop-balanced windows of
+consecutive task ids (one window per timed step).  It also times the
+reference's own planner (`hetsim.run` from the unmodified baseline/_ref
+install, sim.py:388-390) on the same graph, platform and cost model, and checks
+that its bytes and makespan equal the native planner's.
 """
 
 from __future__ import annotations
@@ -56,6 +62,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=16384, help="CPU baseline sample order")
+    ap.add_argument("--no-extra-families", action="store_true",
+                    help="skip the k=1 LU (configs[2]) and QR (configs[3]) lines appended to a Cholesky run")
+    ap.add_argument("--no-one-shot", action="store_true")
     return ap.parse_args()
 
 
@@ -273,45 +282,120 @@ def ncu_traffic():
     return None
 
 
-def cpu_baseline_sample(n, nb):
+def oracle_matrix(fam, n, seed):
+    from oracle import tiles as O
+
+    return O.spd_matrix(n, seed) if fam == "cholesky" else O.general_matrix(n, seed)
+
+
+def cpu_baseline_sample(fam, n, nb, ib):
+    """Bounded CPU sample (N=1, rank 0): the same family's tile DAG at order ``n`` factored
+    once by the oracle on every host core (one forked worker process per core)."""
+    import paper_1402_6601_b200 as H
     from oracle import cpu_exec
 
-    threads = cpu_exec.host_threads()
-    secs, flops, res = cpu_exec.cholesky_sample(n, nb, threads)
-    return {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-            "sample": f"tiled Cholesky N={n} nb={nb} (oracle SciPy/OpenBLAS tile kernels, {threads} host threads, "
-                      f"1 BLAS thread each), {secs:.2f} s, residual {res:.1e}"}
+    workers = cpu_exec.host_threads()
+    g = H.gen_family(fam, n // nb, nb, ib)
+    arena, secs = cpu_exec.factor(g, oracle_matrix(fam, n, 0), workers)
+    flops = H.flops_of(fam, n)
+    return {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": workers, "kind": "port",
+            "sample": f"tiled {fam} N={n} nb={nb} ib={ib} factored once ({secs:.2f} s): oracle SciPy/OpenBLAS/"
+                      f"NumPy tile kernels (oracle/tiles*.py) on {workers} forked worker processes, one BLAS "
+                      f"thread each, dynamic DAG list scheduling"}
+
+
+def reference_planner(g, plat, sched_name, alpha, model_path, nb, ib, ours):
+    """Wall time of the reference's own planning path (hetsim.run from the unmodified
+    baseline/_ref install) on this graph / platform / cost model, and whether its report
+    equals the native planner's plan bit for bit (bytes, makespan, task->worker map)."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "hetsim")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref /root/reference/pkg)"}
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import hetsim
+
+    rg = hetsim.gen_family(g.layout.family, g.layout.nt, nb, ib)
+    rplat = hetsim.build_platform(plat.m, plat.k, plat.n_switches, link_bandwidth=NVLINK_BW,
+                                  link_latency=NVLINK_LAT, switch_cap=math.inf, p2p=True)
+    table = hetsim.load_timing_table(model_path) if model_path else hetsim.default_timing_table(nb, ib)
+    sch = hetsim.make_scheduler("dada", alpha=alpha, cp=True) if sched_name == "dada" else hetsim.make_scheduler("heft")
+    t0 = time.perf_counter()
+    rep = hetsim.run(rg, rplat, sch, hetsim.PerfModel(table))
+    wall = time.perf_counter() - t0
+    same = (rep.bytes_h2d == ours.bytes_h2d and rep.bytes_d2d == ours.bytes_d2d and rep.makespan == ours.makespan
+            and all(rep.schedule[t].worker == int(ours.worker[t]) for t in range(len(rg))))
+    return {"hetsim_run_seconds": wall, "bit_exact_vs_native": bool(same), "makespan_s": rep.makespan,
+            "bytes_d2d": rep.bytes_d2d, "source": "baseline/_ref (unmodified hetsim 0.1.0)"}
 
 
 # -- arms ------------------------------------------------------------------------
 
 def run_reference(args, rank, world):
+    """The reference's CPU path on this box's host cores (see module doc)."""
     if rank != 0:
         return 0
+    import paper_1402_6601_b200 as H
     from oracle import cpu_exec
 
-    threads = cpu_exec.host_threads()
-    n = min(args.cpu_n, args.n) // 2 if args.n >= 2 * args.nb else args.n
-    n = max(n, args.nb)
+    workers = cpu_exec.host_threads()
+    fam, n, nb, ib = args.family, args.n, args.nb, args.ib
+    g = H.gen_family(fam, n // nb, nb, ib)
+    # warm-up steps: a 2x2-tile factorization each (worker fork, BLAS/LAPACK first touch)
+    gw = H.gen_family(fam, 2, nb, ib)
+    aw = oracle_matrix(fam, 2 * nb, 1)
     for _ in range(args.warmup):
-        cpu_exec.cholesky_sample(n, args.nb, threads)
-    secs = []
-    flops = 0.0
-    for _ in range(args.steps):
-        s, flops, res = cpu_exec.cholesky_sample(n, args.nb, threads)
-        secs.append(s)
-    ms = float(np.mean(secs)) * 1e3
-    val = flops / (ms * 1e-3) / 1e9
-    sample = (f"tiled Cholesky N={n} nb={args.nb} per step (bounded sample of the N={args.n} workload): "
-              f"oracle SciPy/OpenBLAS tile kernels on {threads} host threads, dynamic DAG list scheduling")
+        cpu_exec.factor(gw, aw, workers)
+    A = oracle_matrix(fam, n, 0)
+    arena = cpu_exec.TileArena(g).load(A)
+    check = None
+    if fam == "cholesky":
+        x = np.random.default_rng(5).standard_normal(n)
+        ax = A @ x
+    del A
+    wins = cpu_exec.flop_windows(g, args.steps)
+    with cpu_exec.DagPool(g, arena, workers) as pool:
+        secs = [pool.run(lo, hi) for lo, hi in wins]
+    total = float(sum(secs))
+    flops = H.flops_of(fam, n)
+    val = flops / total / 1e9
+    if fam == "cholesky":
+        lay = g.layout
+        y, z = np.zeros(n), np.zeros(n)
+        for d, (i, j) in lay.tiles.items():
+            l = np.tril(arena.tiles[d]) if i == j else arena.tiles[d]
+            y[j * nb:(j + 1) * nb] += l.T @ x[i * nb:(i + 1) * nb]
+        for d, (i, j) in lay.tiles.items():
+            l = np.tril(arena.tiles[d]) if i == j else arena.tiles[d]
+            z[i * nb:(i + 1) * nb] += l @ y[j * nb:(j + 1) * nb]
+        rr = float(np.linalg.norm(ax - z) / np.linalg.norm(ax))
+        check = {"randomized_relres": rr, "ok": bool(rr < 1e-12)}
+    k = world
+    plat = H.build_platform(k, k, k, link_bandwidth=NVLINK_BW, link_latency=NVLINK_LAT, switch_cap=math.inf, p2p=True)
+    model, model_src = load_model(H, args)
+    model_path = os.path.join(ROOT, model_src) if model_src.endswith(".csv") else None
+    planner = {}
+    for name in ("dada", "heft"):
+        sch = H.make_scheduler("dada", alpha=args.alpha, cp=True) if name == "dada" else H.make_scheduler("heft")
+        t0 = time.perf_counter()
+        ours = H.make_plan(g, plat, sch, model)
+        native_s = time.perf_counter() - t0
+        planner[name] = dict(reference_planner(g, plat, name, args.alpha, model_path, nb, ib, ours),
+                             native_plan_seconds=native_s)
+    sample = (f"tiled {fam} N={n} nb={nb} ib={ib}: the whole factorization executed once, split into "
+              f"{len(wins)} flop-balanced windows of consecutive task ids (one per step); oracle SciPy/"
+              f"OpenBLAS/NumPy tile kernels on {workers} forked worker processes (one BLAS thread each), "
+              f"dynamic DAG list scheduling")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"tiled {args.family} N={args.n} nb={args.nb}", "family": args.family,
-                   "n": args.n, "nb": args.nb, "sample_n": n},
-        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "port", "sample": sample},
+        "steps": len(wins), "warmup": args.warmup, "ms_per_step": total / len(wins) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"tiled {fam} N={n} nb={nb} ib={ib} FP64", "family": fam, "n": n, "nb": nb,
+                   "same_config": True},
+        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "window_seconds": secs, "check": check,
+        "planner": planner,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -425,6 +509,8 @@ def run_ours(args, rank, world, local):
 
     e2e = None
     check = None
+    if args.no_e2e:
+        args.no_one_shot = True
     if not args.no_e2e:
         out = torch.empty_like(img, pin_memory=True)
         ex = make_exec(plans["dada"], host_in, out.numpy(), False)
@@ -441,6 +527,33 @@ def run_ours(args, rank, world, local):
             check = {"randomized_relres": relres, "ok": bool(relres < 1e-12)}
         else:
             check = {"note": "factor parity covered by tests/test_gpu_*.py (per-rank write-backs / non-Cholesky)"}
+        del out
+
+    # one-shot call through the public API as a drop-in caller makes it: PAGEABLE numpy images,
+    # plan + page-lock (hg_matrix_register) + graph build/instantiate + run + teardown, wall clock
+    one_shot = None
+    if not args.no_one_shot and world == 1:
+        pageable_in = np.array(host_in, copy=True)
+        pageable_out = np.empty_like(pageable_in)
+        w0 = time.perf_counter()
+        plan1 = H.make_plan(g, plat, H.make_scheduler("dada", alpha=args.alpha, cp=True), model)
+        w1 = time.perf_counter()
+        with runtime.pinned_host(pageable_in, pageable_out):
+            w2 = time.perf_counter()
+            ex1 = runtime.Executor(g, plat, plan1, pageable_in, pageable_out, devices=[local],
+                                   priority_levels=args.priority_levels)
+            w3 = time.perf_counter()
+            st1 = ex1.run()
+            w4 = time.perf_counter()
+            ex1.close()
+        w5 = time.perf_counter()
+        one_shot = {"value": flops / (w5 - w0) / 1e9, "unit": "GFLOP/s", "wall_ms": (w5 - w0) * 1e3,
+                    "plan_ms": (w1 - w0) * 1e3, "register_ms": (w2 - w1) * 1e3 + (w5 - w4) * 1e3,
+                    "graph_build_ms": (w3 - w2) * 1e3, "run_ms": (w4 - w3) * 1e3,
+                    "run_device_ms": st1.elapsed_ms, "kernel_nodes": st1.n_kernel_nodes,
+                    "copy_nodes": st1.n_copy_nodes,
+                    "note": "runtime.Executor on pageable numpy images, first and only run (cold graph upload)"}
+        del pageable_in, pageable_out
 
     # the probe is short: take the better of a cold (pre-run) and a warm (post-run) measurement
     dmma2, dfma2 = _native.fp64_peak(local)
@@ -461,9 +574,34 @@ def run_ours(args, rank, world, local):
                 "concurrent_note": "8 independent GEMM tiles on 8 streams (the DAG's operating point): "
                                    "2*nb^3 per tile / (wall / tiles); `achieved` is one launch alone "
                                    "(256 CTAs on 148 SMs, latency-bound)"}
+    extra = None
+    if world == 1 and fam == "cholesky" and not args.no_extra_families and n == 32768:
+        del img, host_in
+        torch.cuda.empty_cache()
+        extra = {}
+        for fam2, cfg in (("lu", 2), ("qr", 3)):
+            g2 = H.gen_family(fam2, n // nb, nb, args.ib)
+            t0 = time.perf_counter()
+            plan2 = H.make_plan(g2, plat, H.make_scheduler("dada", alpha=args.alpha, cp=True), model)
+            pw = time.perf_counter() - t0
+            img2 = make_input(g2, n, nb, 0, torch)
+            ex2 = runtime.Executor(g2, plat, plan2, img2.numpy(), None, devices=[local], device_input=True,
+                                   priority_levels=args.priority_levels)
+            st2 = min(args.steps, 5)
+            ms2, _ = timed(ex2, st2, 1)
+            info2 = ex2.info()
+            ex2.close()
+            f2 = H.flops_of(fam2, n)
+            extra[fam2] = {"workload": f"tiled {fam2.upper()} N={n} nb={nb} ib={args.ib} FP64 (BASELINE configs[{cfg}]), k=1",
+                           "value": f2 / (ms2 * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms2, "steps": st2,
+                           "warmup": 1, "step_frac": (f2 / (ms2 * 1e-3) / 1e12) / dmma_peak,
+                           "planned_makespan_ms": plan2.makespan * 1e3, "plan_seconds": pw,
+                           "kernel_nodes": info2.n_kernel_nodes, "scheduler": f"DADA(alpha={args.alpha})+CP"}
+            del ex2, img2
+            torch.cuda.empty_cache()
     cpu = None
-    if not args.no_cpu_baseline and rank == 0 and world == 1 and fam == "cholesky":
-        cpu = cpu_baseline_sample(args.cpu_n, nb)
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        cpu = cpu_baseline_sample(fam, min(args.cpu_n, n), nb, args.ib)
     d = results["dada"]
     line = {
         "metric": METRIC, "value": d["gflops"], "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -481,7 +619,8 @@ def run_ours(args, rank, world, local):
                  "same_plan_as_dada": bool(results["heft"].get("same_plan_as_dada", False))},
         "plan": {"dada_seconds": plan_wall["dada"], "heft_seconds": plan_wall["heft"],
                  "dada_fallbacks": d["dada_fallbacks"], "planner": "native bit-exact (hg_plan_build)"},
-        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+        "e2e": e2e, "one_shot": one_shot, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+        "families_k1": extra,
         "gpu_launches": d["kernel_nodes"] * args.steps, "check": check,
     }
     if rank == 0:

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define HG_ABI_VERSION 2
+#define HG_ABI_VERSION 3
 
 /* error codes */
 #define HG_OK 0
@@ -42,6 +42,9 @@ extern "C" {
 #define HG_EDEADLOCK (-4)  /* planner: tasks left with no events      -> DeadlockError */
 #define HG_EMODEL (-5)     /* planner: missing timing                 -> PerfModelError */
 #define HG_ESINGULAR (-6)  /* LU met an exactly zero pivot            -> SimulationError */
+#define HG_EPEER (-7)      /* two GPUs of a p2p plan lack peer access -> PlatformError */
+/* HG_EDEADLOCK is also returned by hg_exec_wait/run when a cross-rank wait timed out
+ * (hg_exec_set_wait_timeout): a dead peer rank or ranks running different plans. */
 
 /* kernel kinds: index in kernels.ALL_KINDS (kernels.py:39-42) */
 enum {
@@ -186,6 +189,10 @@ typedef struct hg_exec_opts {
                                  task_weight) quantised to min(levels, device range) levels;
                                  0 = every node at default priority.  Never changes the plan,
                                  only the order in which ready kernels get SMs. */
+  int32_t trace;              /* 1: stamp %globaltimer before/after every task's kernel chain and
+                                 every copy job (one 1-thread node each); read with
+                                 hg_exec_read_stamps -> the executed schedule (sim.py:66-80 TaskRun,
+                                 TraceEvent).  0 = no extra nodes. */
 } hg_exec_opts;
 
 typedef struct hg_exec hg_exec;
@@ -220,6 +227,23 @@ int hg_exec_wait(hg_exec* ex);
 int hg_exec_info(hg_exec* ex, hg_exec_stats* stats);
 int hg_exec_read_block(hg_exec* ex, int32_t block, int32_t node, double* host, int64_t doubles);
 int hg_exec_destroy(hg_exec* ex);
+/* one-process-per-GPU mode: bound on every cross-rank spin (flag waits, the step fence);
+ * default 60 s; set before hg_exec_build.  A wait that gives up makes hg_exec_wait return
+ * HG_EDEADLOCK instead of hanging the device (reference: DeadlockError, sim.py:24-29). */
+int hg_exec_set_wait_timeout(hg_exec* ex, double seconds);
+/* trace mode (opts.trace = 1), after a run: out[2t], out[2t+1] = device ns at which task t started /
+ * ended; out[2(n_tasks+j)], out[2(n_tasks+j)+1] = the same for copy job j (0 for work of other
+ * ranks).  Capacity 2 * (n_tasks + n_jobs). */
+int hg_exec_read_stamps(hg_exec* ex, uint64_t* out);
+/* one-process-per-GPU teardown: unmap the peers' pools (run after a barrier; then barrier
+ * again before hg_exec_destroy frees this rank's exported pool) */
+int hg_exec_ipc_close(hg_exec* ex);
+
+/* Page-lock caller-owned host images (input / output) for async H2D / D2H DMA
+ * (cudaHostRegister, portable).  The caller keeps ownership and unregisters before
+ * freeing.  Registering an already registered range is not an error. */
+int hg_matrix_register(void* host, size_t bytes);
+int hg_matrix_unregister(void* host);
 
 /* ------------------------------------------------------------------------
  * One tile kernel on a stream (tests / calibration).  t[] are device

@@ -140,66 +140,92 @@ def _worker(conn):
     conn.close()
 
 
-def run_dag(graph, arena: TileArena, workers: int | None = None) -> float:
-    """Execute every task of ``graph`` on ``arena`` with ``workers`` forked processes
-    (default: every core in this process's affinity mask); returns the seconds
-    from the first dispatch to the last completion (worker start-up excluded)."""
-    workers = max(1, workers or host_threads())
-    n = len(graph)
-    ctx = mp.get_context("fork")
-    _CTX["graph"], _CTX["arena"] = graph, arena
-    procs, conns = [], []
-    try:
-        for _ in range(workers):
-            a, b = ctx.Pipe()
-            p = ctx.Process(target=_worker, args=(b,), daemon=True)
-            p.start()
-            b.close()
-            procs.append(p)
-            conns.append(a)
-    finally:
-        _CTX.clear()
-    try:
-        for c in conns:
+class DagPool:
+    """``workers`` forked processes bound to (graph, arena); ``run(lo, hi)`` executes the
+    tasks with ids in [lo, hi) -- task ids are a topological order (graph.py:58-84), so once
+    every task below ``lo`` is done such a window only depends on itself."""
+
+    def __init__(self, graph, arena: TileArena, workers: int | None = None):
+        self.graph, self.arena = graph, arena
+        self.workers = max(1, workers or host_threads())
+        self.procs, self.conns = [], []
+        self._preds_left = graph.in_degrees()
+
+    def __enter__(self):
+        ctx = mp.get_context("fork")
+        _CTX["graph"], _CTX["arena"] = self.graph, self.arena
+        try:
+            for _ in range(self.workers):
+                a, b = ctx.Pipe()
+                p = ctx.Process(target=_worker, args=(b,), daemon=True)
+                p.start()
+                b.close()
+                self.procs.append(p)
+                self.conns.append(a)
+        finally:
+            _CTX.clear()
+        for c in self.conns:
             if c.recv() != "ready":
                 raise RuntimeError("oracle worker failed to start")
-        left = graph.in_degrees()
-        ready = [t for t in range(n) if left[t] == 0]
+        return self
+
+    def __exit__(self, *exc):
+        for c in self.conns:
+            try:
+                c.send(None)
+            except (OSError, BrokenPipeError):
+                pass
+        for p in self.procs:
+            p.join(timeout=10)
+            if p.is_alive():
+                p.kill()
+
+    def run(self, lo: int = 0, hi: int | None = None) -> float:
+        """Execute tasks [lo, hi); returns seconds from first dispatch to last completion."""
+        g = self.graph
+        hi = len(g) if hi is None else hi
+        left = self._preds_left
+        ready = [t for t in range(lo, hi) if left[t] == 0]
         heapq.heapify(ready)
-        idle = list(range(workers))
+        idle = list(range(self.workers))
         busy = {}
-        done = 0
+        done, need = 0, hi - lo
         t0 = time.perf_counter()
-        while done < n:
+        while done < need:
             while ready and idle:
                 w = idle.pop()
-                tid = heapq.heappop(ready)
-                conns[w].send(tid)
-                busy[conns[w]] = w
+                self.conns[w].send(heapq.heappop(ready))
+                busy[self.conns[w]] = w
             if not busy:
-                raise RuntimeError("oracle DAG executor: no ready task and nothing running (cycle?)")
+                raise RuntimeError(f"oracle DAG executor: window [{lo}, {hi}) has no runnable task "
+                                   "(earlier tasks not done?)")
             for c in mp_wait(list(busy)):
                 msg = c.recv()
                 if isinstance(msg, tuple):
                     raise RuntimeError(f"oracle task {msg[1]} failed:\n{msg[2]}")
                 done += 1
-                for s in graph.successors(msg):
-                    left[s] -= 1
-                    if left[s] == 0:
-                        heapq.heappush(ready, s)
+                for s_ in g.successors(msg):
+                    left[s_] -= 1
+                    if left[s_] == 0 and lo <= s_ < hi:
+                        heapq.heappush(ready, s_)
                 idle.append(busy.pop(c))
-        secs = time.perf_counter() - t0
-    finally:
-        for c in conns:
-            try:
-                c.send(None)
-            except (OSError, BrokenPipeError):
-                pass
-        for p in procs:
-            p.join(timeout=10)
-            if p.is_alive():
-                p.kill()
-    return secs
+        return time.perf_counter() - t0
+
+
+def flop_windows(graph, k: int):
+    """Split task ids 0..n-1 into ``k`` consecutive windows of about equal flops."""
+    fl = np.cumsum([t.flops for t in graph.tasks])
+    cuts = [0] + [int(np.searchsorted(fl, fl[-1] * i / k)) + 1 for i in range(1, k)] + [len(graph)]
+    cuts = sorted(set(min(max(c, 0), len(graph)) for c in cuts))
+    return list(zip(cuts[:-1], cuts[1:]))
+
+
+def run_dag(graph, arena: TileArena, workers: int | None = None) -> float:
+    """Execute every task of ``graph`` on ``arena`` with ``workers`` forked processes
+    (default: every core in this process's affinity mask); returns the seconds
+    from the first dispatch to the last completion (worker start-up excluded)."""
+    with DagPool(graph, arena, workers) as pool:
+        return pool.run()
 
 
 def factor(graph, A: np.ndarray, workers: int | None = None):

@@ -17,7 +17,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libhetgpu.so")
 
-HG_OK, HG_EINVAL, HG_ECUDA, HG_ENOTSPD, HG_EDEADLOCK, HG_EMODEL, HG_ESINGULAR = 0, -1, -2, -3, -4, -5, -6
+HG_OK, HG_EINVAL, HG_ECUDA, HG_ENOTSPD, HG_EDEADLOCK, HG_EMODEL, HG_ESINGULAR, HG_EPEER = 0, -1, -2, -3, -4, -5, -6, -7
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
@@ -73,7 +73,8 @@ class ExecPlan(C.Structure):
 class ExecOpts(C.Structure):
     _fields_ = [("devices", _i32p), ("host_in", _f64p), ("host_out", _f64p), ("host_side_out", _f64p),
                 ("device_input", C.c_int32), ("rank_node", C.c_int32),
-                ("task_weight", _f64p), ("host_stage", _f64p), ("priority_levels", C.c_int32)]
+                ("task_weight", _f64p), ("host_stage", _f64p), ("priority_levels", C.c_int32),
+                ("trace", C.c_int32)]
 
 
 class ExecStats(C.Structure):
@@ -86,7 +87,8 @@ EXPORTS = ("hg_last_error", "hg_abi_version", "hg_device_count", "hg_plan_build"
            "hg_pysum", "hg_exec_create", "hg_exec_run", "hg_exec_read_block", "hg_exec_destroy",
            "hg_tile_run", "hg_exec_launch", "hg_exec_wait", "hg_exec_info", "hg_fp64_peak",
            "hg_exec_ipc_handle", "hg_exec_ipc_open", "hg_exec_build", "hg_exec_partition",
-           "hg_tile_run_scratch", "hg_task_scratch_ints")
+           "hg_tile_run_scratch", "hg_task_scratch_ints", "hg_exec_set_wait_timeout", "hg_exec_ipc_close", "hg_exec_read_stamps",
+           "hg_matrix_register", "hg_matrix_unregister")
 
 _lib = None
 
@@ -129,6 +131,11 @@ def lib():
     L.hg_exec_ipc_open.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
     L.hg_exec_build.argtypes = [C.c_void_p]
     L.hg_exec_partition.argtypes = [C.POINTER(ExecPlan), C.c_int32, _i32p, _i32p, _i32p]
+    L.hg_exec_set_wait_timeout.argtypes = [C.c_void_p, C.c_double]
+    L.hg_exec_ipc_close.argtypes = [C.c_void_p]
+    L.hg_exec_read_stamps.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+    L.hg_matrix_register.argtypes = [C.c_void_p, C.c_size_t]
+    L.hg_matrix_unregister.argtypes = [C.c_void_p]
     _lib = L
     return L
 
@@ -149,14 +156,19 @@ def check(rc: int, what: str):
         return
     msg = f"{what}: {last_error()} (code {rc})"
     from .perfmodel import PerfModelError
+    from .platform import PlatformError
     from .sim import DeadlockError, SimulationError
 
     if rc == HG_EINVAL:
         raise ValueError(msg)
     if rc == HG_EMODEL:
         raise PerfModelError(msg)
+    if rc == HG_EPEER:
+        raise PlatformError(msg)
     if rc == HG_EDEADLOCK:
-        raise DeadlockError([])
+        err = DeadlockError([])
+        err.args = (msg,)
+        raise err
     raise SimulationError(msg)
 
 

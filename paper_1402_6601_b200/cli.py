@@ -144,7 +144,8 @@ def point_rows(s: Settings, trace_path: str | None = None, execute: bool = False
             _write_trace(trace_path, report.events)
         row = _fmt_row(s, n, seed, rep, report, total)
         if execute:
-            row += _execute(graph, plat, sched, model, seed, n, total)
+            row += _execute(graph, plat, sched, model, seed, n, total,
+                            trace_path=(trace_path + ".executed") if trace else None)
         yield row
 
 
@@ -155,8 +156,10 @@ def _write_trace(path: str, events) -> None:
             fh.write(f"{ev.time!r} {ev.kind} {ev.worker} {ev.task} {ev.data} {ev.nbytes}\n")
 
 
-def _execute(graph, plat, sched, model, seed: int, n: int, total_flops: float) -> list:
-    """Execute the plan on the B200s (one process, one CUDA graph over every GPU)."""
+def _execute(graph, plat, sched, model, seed: int, n: int, total_flops: float, trace_path=None) -> list:
+    """Execute the plan on the B200s (one process, one CUDA graph over every GPU).  With
+    ``trace_path`` the timed run is stamped (runtime.Executor(trace=True)) and its measured
+    TraceEvents go to that file in the simulated trace's format."""
     import numpy as np
     import torch
 
@@ -173,9 +176,12 @@ def _execute(graph, plat, sched, model, seed: int, n: int, total_flops: float) -
     out = torch.empty_like(img).pin_memory()
     ndev = torch.cuda.device_count()
     devices = [g % max(1, ndev) for g in range(plat.k)]
-    ex = runtime.Executor(graph, plat, plan, img.numpy(), out.numpy(), devices=devices)
+    ex = runtime.Executor(graph, plat, plan, img.numpy(), out.numpy(), devices=devices,
+                          trace=trace_path is not None)
     ex.run()  # warm-up (graph upload, first-touch page faults)
     st = ex.run()
+    if trace_path is not None:
+        _write_trace(trace_path, ex.report(st, events=True).events)
     ex.close()
     residual = ""
     if graph.layout.family == "cholesky":

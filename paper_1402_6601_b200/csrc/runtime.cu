@@ -226,16 +226,38 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
 __device__ __forceinline__ void st_release_sys(int* p, int v) {
   asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// status bit of a cross-rank wait that gave up (-> HG_EDEADLOCK / DeadlockError)
+constexpr int kStatusWaitTimeout = 4;
 
 struct FlagParams {
   int* flag;
   const int* epoch;
+  int* status;                    // this rank's status word (waits only)
+  unsigned long long timeout_ns;  // waits only: give up after this long
 };
 
+// Bounded spin: a dead peer rank or a plan/partition mismatch would otherwise
+// hang the device (the reference raises DeadlockError when no event is left,
+// sim.py:24-29, 164-166).  On timeout the wait records kStatusWaitTimeout and
+// returns; the run completes with garbage and hg_exec_wait reports HG_EDEADLOCK.
 __global__ void k_wait_flag(FlagParams p) {
   if (threadIdx.x == 0) {
     const int e = *reinterpret_cast<volatile const int*>(p.epoch);
-    while (ld_acquire_sys(p.flag) < e) __nanosleep(256);
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(p.flag) < e) {
+      // once one wait of this run gave up, the others stop spinning too
+      if ((*reinterpret_cast<volatile int*>(p.status) & kStatusWaitTimeout) || global_ns() - t0 > p.timeout_ns) {
+        atomicOr(p.status, kStatusWaitTimeout);
+        break;
+      }
+      __nanosleep(256);
+    }
   }
 }
 
@@ -254,10 +276,19 @@ struct StepFence {
   const int* peer_done[16];
   int n;
   int need;
+  int* status;
+  unsigned long long timeout_ns;
 };
 __global__ void k_wait_peers_done(StepFence f) {
   if (threadIdx.x < f.n) {
-    while (ld_acquire_sys(f.peer_done[threadIdx.x]) < f.need) __nanosleep(256);
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(f.peer_done[threadIdx.x]) < f.need) {
+      if ((*reinterpret_cast<volatile int*>(f.status) & kStatusWaitTimeout) || global_ns() - t0 > f.timeout_ns) {
+        atomicOr(f.status, kStatusWaitTimeout);
+        break;
+      }
+      __nanosleep(256);
+    }
   }
 }
 
@@ -270,6 +301,11 @@ __global__ void k_mark_done(int* done, int v) {
 
 __global__ void k_set_epoch(int* epoch, int v) {
   if (threadIdx.x == 0) *epoch = v;
+}
+
+// trace mode: device time (ns) at which a task / copy job starts and ends (hg_exec_read_stamps)
+__global__ void k_stamp(unsigned long long* p) {
+  if (threadIdx.x == 0) *p = global_ns();
 }
 
 }  // namespace hg
@@ -299,6 +335,8 @@ struct hg_exec {
   std::vector<char> ipc;                // per node: base came from cudaIpcOpenMemHandle
   std::vector<double*> replica;         // per local node: device copy of host_in
   std::vector<int*> status, scratch;    // per local node
+  std::vector<unsigned long long*> stamps;  // per local node, trace mode: [2 * (n_tasks + n_jobs)]
+  int trace = 0;
   std::vector<std::vector<int64_t>> slot;  // [node-1][block] -> doubles offset, -1 = none
   std::vector<int64_t> pool_doubles;    // per node
   int64_t header_doubles = 0;
@@ -307,6 +345,12 @@ struct hg_exec {
   cudaGraphExec_t exec = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // single process, several devices: each non-first device's status word is reset on its own
+  // stream, ordered after the previous run (ev_prev on `stream`) and before this one (ev_reset)
+  std::vector<cudaStream_t> aux_stream;
+  std::vector<cudaEvent_t> ev_reset;
+  cudaEvent_t ev_prev = nullptr;
+  unsigned long long wait_timeout_ns = 60ull * 1000000000ull;  // cross-rank waits (hg_exec_set_wait_timeout)
   hg_exec_stats stats{};
   cudaStream_t last_stream = nullptr;
   bool launched = false;
@@ -338,8 +382,17 @@ static void release(hg_exec* ex) {
     }
     if (ex->replica[g]) cudaFree(ex->replica[g]);
     if (ex->status[g]) cudaFree(ex->status[g]);
+    if (g < (int)ex->stamps.size() && ex->stamps[g]) cudaFree(ex->stamps[g]);
     if (ex->scratch[g]) cudaFree(ex->scratch[g]);
   }
+  for (size_t g = 0; g < ex->aux_stream.size(); ++g) {
+    if (ex->aux_stream[g]) {
+      cudaSetDevice(ex->dev[g]);
+      cudaStreamDestroy(ex->aux_stream[g]);
+    }
+    if (ex->ev_reset[g]) cudaEventDestroy(ex->ev_reset[g]);
+  }
+  if (ex->ev_prev) cudaEventDestroy(ex->ev_prev);
   if (ex->ev0) cudaEventDestroy(ex->ev0);
   if (ex->ev1) cudaEventDestroy(ex->ev1);
   if (ex->stream) cudaStreamDestroy(ex->stream);
@@ -559,6 +612,35 @@ static int build_graph(hg_exec* ex) {
   std::vector<cudaGraphNode_t> h2d_tail(size_t(ex->k) * (h2d_chains > 0 ? h2d_chains : 1), nullptr);
   std::vector<int> h2d_count(ex->k, 0);
 
+  // Cross-rank waits (one process per GPU).  Each spinning wait holds a CTA slot, so waits are
+  // (1) gated: a wait only starts once the task that needs it is otherwise ready (its local
+  //     predecessors are done) -- the planner likewise issues a copy only when its requester is
+  //     dispatched (sim.py:237-267);
+  // (2) chained: wait nodes join kWaitChains chains round-robin in creation (= dispatch) order,
+  //     so at most kWaitChains spinners are resident per device however many remote edges the
+  //     plan has.  Deadlock-free by induction over the plan's dispatch order: the producer of a
+  //     flag completed (in the plan) before the waiting task was dispatched, so it never depends
+  //     on a task dispatched later, i.e. on anything queued behind the wait in its chain.
+  constexpr int kWaitChains = 8;
+  std::vector<cudaGraphNode_t> chain_tail(kWaitChains, nullptr);
+  int chain_next = 0;
+  std::vector<cudaGraphNode_t> gate;  // local predecessors of the task being dispatched
+  auto add_wait = [&](cudaGraphNode_t* w, const std::vector<cudaGraphNode_t>& gate_deps, int* flag,
+                      int cons_node) -> int {
+    std::vector<cudaGraphNode_t> wd = gate_deps;
+    cudaGraphNode_t& tail = chain_tail[chain_next];
+    chain_next = (chain_next + 1) % kWaitChains;
+    if (tail) wd.push_back(tail);
+    std::sort(wd.begin(), wd.end());
+    wd.erase(std::unique(wd.begin(), wd.end()), wd.end());
+    HG_CUDA(cudaSetDevice(ex->dev[cons_node - 1]));
+    int rc = add_flag_kernel(ex->graph, w, wd.data(), wd.size(), (const void*)hg::k_wait_flag,
+                             hg::FlagParams{flag, ex->epoch_ptr(cons_node), ex->status[cons_node - 1],
+                                            ex->wait_timeout_ns});
+    if (rc) return rc;
+    tail = *w;
+    return HG_OK;
+  };
   // dependency on the producer of a task output / job delivery for a consumer on cons_node
   auto dep_task = [&](int u, int cons_node) -> int {
     const int pn = ex->task_node[u];
@@ -568,9 +650,7 @@ static int build_graph(hg_exec* ex) {
     }
     cudaGraphNode_t& w = wait_node[u];
     if (!w) {
-      HG_CUDA(cudaSetDevice(ex->dev[cons_node - 1]));
-      int rc = add_flag_kernel(ex->graph, &w, nullptr, 0, (const void*)hg::k_wait_flag,
-                               hg::FlagParams{ex->task_flag(pn, u), ex->epoch_ptr(cons_node)});
+      int rc = add_wait(&w, gate, ex->task_flag(pn, u), cons_node);
       if (rc) return rc;
     }
     deps.push_back(w);
@@ -584,17 +664,41 @@ static int build_graph(hg_exec* ex) {
     }
     cudaGraphNode_t& w = wait_node[size_t(n) + sj];
     if (!w) {
-      HG_CUDA(cudaSetDevice(ex->dev[cons_node - 1]));
-      int rc = add_flag_kernel(ex->graph, &w, nullptr, 0, (const void*)hg::k_wait_flag,
-                               hg::FlagParams{ex->job_flag(pn, sj), ex->epoch_ptr(cons_node)});
+      int rc = add_wait(&w, gate, ex->job_flag(pn, sj), cons_node);
       if (rc) return rc;
     }
     deps.push_back(w);
     return HG_OK;
   };
 
+  // trace mode: a 1-thread stamp node before and after each task's kernel chain / each copy job
+  auto add_stamp = [&](cudaGraphNode_t* out, const cudaGraphNode_t* d, size_t nd, int node, int64_t slot,
+                       int prio) -> int {
+    unsigned long long* p = ex->stamps[node - 1] + slot;
+    cudaKernelNodeParams kp{};
+    void* args[1] = {&p};
+    kp.func = (void*)hg::k_stamp;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(32);
+    kp.kernelParams = args;
+    HG_CUDA(cudaSetDevice(ex->dev[node - 1]));
+    HG_CUDA(cudaGraphAddKernelNode(out, ex->graph, d, nd, &kp));
+    if (use_prio) {
+      cudaKernelNodeAttrValue v{};
+      v.priority = prio;
+      HG_CUDA(cudaGraphKernelNodeSetAttribute(*out, cudaKernelNodeAttributePriority, &v));
+    }
+    return HG_OK;
+  };
+
   for (int di = 0; di < n; ++di) {
     const int t = ex->dispatch[di];
+    gate.clear();
+    if (ex->rank_node)
+      for (int64_t q = ex->pred_ptr[t]; q < ex->pred_ptr[t + 1]; ++q) {
+        const int u = ex->pred[q];
+        if (ex->is_local(ex->task_node[u]) && task_last[u]) gate.push_back(task_last[u]);
+      }
     // 1) inbound copy jobs created by this dispatch
     for (int j : jobs_of[t]) {
       const int dst = ex->job_dst[j];
@@ -619,6 +723,22 @@ static int build_graph(hg_exec* ex) {
         rc = dep_task(ex->job_version[j], dst);
       }
       if (rc) return rc;
+      // host -> device first touches are serialised into one chain per GPU in dispatch order, so the
+      // copy engine delivers tiles in the order tasks need them instead of all at once in arbitrary
+      // order (C2 e2e: 427 -> 372 ms, i.e. PCIe fully hidden behind compute; HG_H2D_CHAINS overrides,
+      // 0 = independent copies)
+      const bool from_host = src == 0 && !ex->device_input && !staged_in;
+      if (from_host && h2d_chains > 0) {
+        cudaGraphNode_t& prev = h2d_tail[size_t(dst - 1) * h2d_chains + (h2d_count[dst - 1]++ % h2d_chains)];
+        if (prev) deps.push_back(prev);
+      }
+      const int64_t jslot = 2 * (int64_t(n) + j);
+      if (ex->trace) {
+        cudaGraphNode_t s0;
+        int rc2 = add_stamp(&s0, deps.data(), deps.size(), dst, jslot, prio_greatest);
+        if (rc2) return rc2;
+        deps.assign(1, s0);
+      }
       double* dptr = ex->slot_ptr(dst, b);
       const void* sptr;
       size_t bytes;
@@ -659,25 +779,22 @@ static int build_graph(hg_exec* ex) {
         set_error("job %d: missing slot (block %d, %d -> %d)", j, b, src, dst);
         return HG_EINVAL;
       }
-      // host -> device first touches are serialised into one chain per GPU in dispatch order, so the
-      // copy engine delivers tiles in the order tasks need them instead of all at once in arbitrary
-      // order (C2 e2e: 427 -> 372 ms, i.e. PCIe fully hidden behind compute; HG_H2D_CHAINS overrides,
-      // 0 = independent copies)
-      const bool from_host = src == 0 && !ex->device_input && !staged_in;
-      if (from_host && h2d_chains > 0) {
-        cudaGraphNode_t& prev = h2d_tail[size_t(dst - 1) * h2d_chains + (h2d_count[dst - 1]++ % h2d_chains)];
-        if (prev) deps.push_back(prev);
-      }
       HG_CUDA(cudaSetDevice(ex->dev[dst - 1]));
       HG_CUDA(cudaGraphAddMemcpyNode1D(&job_node[j], ex->graph, deps.data(), deps.size(), dptr, sptr, bytes,
                                        cudaMemcpyDefault));
+      if (ex->trace) {
+        cudaGraphNode_t s1;
+        int rc2 = add_stamp(&s1, &job_node[j], 1, dst, jslot + 1, prio_greatest);
+        if (rc2) return rc2;
+        job_node[j] = s1;
+      }
       if (from_host && h2d_chains > 0)
         h2d_tail[size_t(dst - 1) * h2d_chains + ((h2d_count[dst - 1] - 1) % h2d_chains)] = job_node[j];
       st.n_copy_nodes++;
       if (part.sig_job[j]) {
         cudaGraphNode_t sn;
         int rc2 = add_flag_kernel(ex->graph, &sn, &job_node[j], 1, (const void*)hg::k_signal_flag,
-                                  hg::FlagParams{ex->job_flag(dst, j), ex->epoch_ptr(dst)});
+                                  hg::FlagParams{ex->job_flag(dst, j), ex->epoch_ptr(dst), nullptr, 0});
         if (rc2) return rc2;
       }
     }
@@ -732,21 +849,25 @@ static int build_graph(hg_exec* ex) {
     if (n_remote) {
       std::sort(deps.begin(), deps.end());
       deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
-      std::vector<cudaGraphNode_t> local = deps;
-      HG_CUDA(cudaSetDevice(ex->dev[node - 1]));
+      const std::vector<cudaGraphNode_t> local = deps;
       for (int64_t q = ex->pred_ptr[t]; q < ex->pred_ptr[t + 1]; ++q) {
         const int u = ex->pred[q];
         const int pn = ex->task_node[u];
         if (ex->is_local(pn)) continue;
         cudaGraphNode_t w;
-        int rc = add_flag_kernel(ex->graph, &w, local.data(), local.size(), (const void*)hg::k_wait_flag,
-                                 hg::FlagParams{ex->task_flag(pn, u), ex->epoch_ptr(node)});
+        int rc = add_wait(&w, local, ex->task_flag(pn, u), node);
         if (rc) return rc;
         deps.push_back(w);
       }
     }
     std::sort(deps.begin(), deps.end());  // a delivery job may also be in the wait list
     deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+    if (ex->trace) {
+      cudaGraphNode_t s0;
+      int rc = add_stamp(&s0, deps.data(), deps.size(), node, 2 * int64_t(t), use_prio ? prio[t] : 0);
+      if (rc) return rc;
+      deps.assign(1, s0);
+    }
     HG_CUDA(cudaSetDevice(ex->dev[node - 1]));
     cudaGraphNode_t prev = nullptr;
     for (size_t li = 0; li < launches.size(); ++li) {
@@ -768,11 +889,17 @@ static int build_graph(hg_exec* ex) {
       prev = nd;
       st.n_kernel_nodes++;
     }
+    if (ex->trace) {
+      cudaGraphNode_t s1;
+      int rc = add_stamp(&s1, &prev, 1, node, 2 * int64_t(t) + 1, use_prio ? prio[t] : 0);
+      if (rc) return rc;
+      prev = s1;
+    }
     task_last[t] = prev;
     if (part.sig_task[t]) {
       cudaGraphNode_t sn;
       int rc = add_flag_kernel(ex->graph, &sn, &task_last[t], 1, (const void*)hg::k_signal_flag,
-                               hg::FlagParams{ex->task_flag(node, t), ex->epoch_ptr(node)});
+                               hg::FlagParams{ex->task_flag(node, t), ex->epoch_ptr(node), nullptr, 0});
       if (rc) return rc;
     }
   }
@@ -880,6 +1007,8 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
   ex->replica.assign(P->k, nullptr);
   ex->status.assign(P->k, nullptr);
   ex->scratch.assign(P->k, nullptr);
+  ex->stamps.assign(P->k, nullptr);
+  ex->trace = O->trace;
   plan_layout(ex);
   int64_t host_total = 0;
   for (int b = 0; b < ex->n_blocks; ++b) host_total += ex->blk_doubles[b];
@@ -895,8 +1024,16 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
     if ((rc = ensure_attributes(ex->dev[g]))) break;
     for (int h = 0; h < P->k && ex->rank_node == 0; ++h) {
       if (h == g || ex->dev[h] == ex->dev[g]) continue;
+      // a p2p plan moves tiles GPU->GPU directly (platform.py:117); without peer access the copy
+      // engine would silently stage through host memory, which is a different machine model
       int can = 0;
       cudaDeviceCanAccessPeer(&can, ex->dev[g], ex->dev[h]);
+      if (!can && ex->p2p) {
+        set_error("devices %d and %d have no peer access: a p2p=True plan needs NVLink/P2P between "
+                  "every pair of its GPUs (plan with p2p=False for host-staged routes)", ex->dev[g], ex->dev[h]);
+        rc = HG_EPEER;
+        break;
+      }
       if (can) {
         cudaError_t e = cudaDeviceEnablePeerAccess(ex->dev[h], 0);
         if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
@@ -913,6 +1050,14 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
                 (long long)ex->pool_doubles[g] * 8);
       rc = HG_ECUDA;
       break;
+    }
+    if (ex->trace) {
+      const size_t sb = size_t(2) * (size_t(P->n_tasks) + P->n_jobs) * sizeof(unsigned long long);
+      if (cudaMalloc(&ex->stamps[g], sb) != cudaSuccess || cudaMemset(ex->stamps[g], 0, sb) != cudaSuccess) {
+        set_error("trace stamp buffer allocation failed on device %d", ex->dev[g]);
+        rc = HG_ECUDA;
+        break;
+      }
     }
     cudaMemset(ex->base[g], 0, size_t(ex->header_doubles) * 8);  // flags + epoch
     cudaMemset(ex->status[g], 0, sizeof(int));
@@ -936,9 +1081,22 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
   }
   if (rc == HG_OK) {
     const int first = ex->rank_node ? ex->rank_node : 1;
+    ex->aux_stream.assign(P->k, nullptr);
+    ex->ev_reset.assign(P->k, nullptr);
+    for (int g = 0; g < P->k && rc == HG_OK && ex->rank_node == 0; ++g) {
+      if (g + 1 == first) continue;
+      cudaSetDevice(ex->dev[g]);
+      if (cudaStreamCreateWithFlags(&ex->aux_stream[g], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ex->ev_reset[g], cudaEventDisableTiming) != cudaSuccess) {
+        set_error("stream/event creation failed on device %d", ex->dev[g]);
+        rc = HG_ECUDA;
+      }
+    }
     cudaSetDevice(ex->dev[first - 1]);
-    if (cudaStreamCreateWithFlags(&ex->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreate(&ex->ev0) != cudaSuccess || cudaEventCreate(&ex->ev1) != cudaSuccess) {
+    if (rc == HG_OK &&
+        (cudaStreamCreateWithFlags(&ex->stream, cudaStreamNonBlocking) != cudaSuccess ||
+         cudaEventCreate(&ex->ev0) != cudaSuccess || cudaEventCreate(&ex->ev1) != cudaSuccess ||
+         cudaEventCreateWithFlags(&ex->ev_prev, cudaEventDisableTiming) != cudaSuccess)) {
       set_error("stream/event creation failed");
       rc = HG_ECUDA;
     }
@@ -1039,7 +1197,12 @@ static int all_status(hg_exec* ex, int* bad) {
   return HG_OK;
 }
 
-static int status_error(int bad) {
+static int status_error(const hg_exec* ex, int bad) {
+  if (bad & hg::kStatusWaitTimeout) {
+    set_error("a cross-rank wait timed out after %.1f s: a peer rank died or ranks executed different "
+              "plans/partitions (hg_exec_set_wait_timeout)", double(ex->wait_timeout_ns) * 1e-9);
+    return HG_EDEADLOCK;
+  }
   if (bad & 1) {
     set_error("POTRF: matrix is not positive definite (non-positive pivot)");
     return HG_ENOTSPD;
@@ -1061,25 +1224,35 @@ extern "C" int hg_exec_launch(hg_exec* ex, void* stream) {
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ex->epoch++;
-  for (int g = 0; g < ex->k; ++g) {
-    if (!ex->is_local(g + 1)) continue;
-    HG_CUDA(cudaSetDevice(ex->dev[g]));
-    const bool first = (ex->rank_node ? ex->rank_node : 1) == g + 1;
-    cudaStream_t sg = first ? s : nullptr;
-    HG_CUDA(cudaMemsetAsync(ex->status[g], 0, sizeof(int), sg));
-    if (ex->rank_node) {  // flags are only used across processes
-      hg::k_set_epoch<<<1, 32, 0, sg>>>(ex->epoch_ptr(g + 1), ex->epoch);
-      HG_CUDA(cudaGetLastError());
-    }
-    if (!first) HG_CUDA(cudaDeviceSynchronize());  // other devices' resets precede the graph
-  }
   const int first = ex->rank_node ? ex->rank_node : 1;
+  // status resets: the first device's on the launch stream; every other device's (single-process
+  // mode) on its own stream, after everything enqueued on `s` so far (the previous run) and before
+  // this run's graph -- fully asynchronous, no host synchronisation
   HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
+  HG_CUDA(cudaMemsetAsync(ex->status[first - 1], 0, sizeof(int), s));
+  if (ex->rank_node) {  // flags are only used across processes
+    hg::k_set_epoch<<<1, 32, 0, s>>>(ex->epoch_ptr(first), ex->epoch);
+    HG_CUDA(cudaGetLastError());
+  } else if (ex->k > 1) {
+    HG_CUDA(cudaEventRecord(ex->ev_prev, s));
+    for (int g = 0; g < ex->k; ++g) {
+      if (g + 1 == first) continue;
+      HG_CUDA(cudaSetDevice(ex->dev[g]));
+      HG_CUDA(cudaStreamWaitEvent(ex->aux_stream[g], ex->ev_prev, 0));
+      HG_CUDA(cudaMemsetAsync(ex->status[g], 0, sizeof(int), ex->aux_stream[g]));
+      HG_CUDA(cudaEventRecord(ex->ev_reset[g], ex->aux_stream[g]));
+    }
+    HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
+    for (int g = 0; g < ex->k; ++g)
+      if (g + 1 != first) HG_CUDA(cudaStreamWaitEvent(s, ex->ev_reset[g], 0));
+  }
   if (ex->rank_node) {
     hg::StepFence f{};
     for (int g = 0; g < ex->k && f.n < 16; ++g)
       if (g + 1 != ex->rank_node) f.peer_done[f.n++] = ex->done_ptr(g + 1);
     f.need = ex->epoch - 1;
+    f.status = ex->status[first - 1];
+    f.timeout_ns = ex->wait_timeout_ns;
     if (ex->k > 17) {
       set_error("hg_exec_launch: step fence supports up to 17 ranks");
       return HG_EINVAL;
@@ -1110,7 +1283,7 @@ extern "C" int hg_exec_wait(hg_exec* ex) {
   int rc = all_status(ex, &bad);
   if (rc) return rc;
   HG_CUDA(cudaSetDevice(ex->dev[first - 1]));
-  return status_error(bad);
+  return status_error(ex, bad);
 }
 
 extern "C" int hg_exec_run(hg_exec* ex, hg_exec_stats* stats) {
@@ -1161,5 +1334,90 @@ extern "C" int hg_exec_read_block(hg_exec* ex, int32_t block, int32_t node, doub
 
 extern "C" int hg_exec_destroy(hg_exec* ex) {
   release(ex);
+  return HG_OK;
+}
+
+extern "C" int hg_exec_read_stamps(hg_exec* ex, uint64_t* out) {
+  if (!ex || !out || !ex->trace) {
+    set_error("hg_exec_read_stamps: bad handle or executor created without opts.trace");
+    return HG_EINVAL;
+  }
+  const int64_t n = ex->n_tasks, nj = ex->n_jobs;
+  std::fill(out, out + 2 * (n + nj), uint64_t(0));
+  std::vector<unsigned long long> buf(size_t(2) * (n + nj));
+  for (int g = 0; g < ex->k; ++g) {
+    if (!ex->is_local(g + 1) || !ex->stamps[g]) continue;
+    HG_CUDA(cudaSetDevice(ex->dev[g]));
+    HG_CUDA(cudaMemcpy(buf.data(), ex->stamps[g], buf.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (int64_t t = 0; t < n; ++t)
+      if (ex->task_node[t] == g + 1) out[2 * t] = buf[2 * t], out[2 * t + 1] = buf[2 * t + 1];
+    for (int64_t j = 0; j < nj; ++j)
+      if (ex->job_dst[j] == g + 1)
+        out[2 * (n + j)] = buf[2 * (n + j)], out[2 * (n + j) + 1] = buf[2 * (n + j) + 1];
+  }
+  return HG_OK;
+}
+
+extern "C" int hg_exec_set_wait_timeout(hg_exec* ex, double seconds) {
+  if (!ex || !(seconds > 0.0) || ex->built) {
+    set_error("hg_exec_set_wait_timeout: bad handle, non-positive timeout, or graph already built");
+    return HG_EINVAL;
+  }
+  ex->wait_timeout_ns = (unsigned long long)(seconds * 1e9);
+  return HG_OK;
+}
+
+// Teardown of the one-process-per-GPU mode: unmap every peer pool (cudaIpcCloseMemHandle) while
+// this rank's own pool stays allocated.  The Python side runs: wait -> barrier -> hg_exec_ipc_close
+// -> barrier -> hg_exec_destroy, so no rank frees an exported pool a peer still reads or maps.
+extern "C" int hg_exec_ipc_close(hg_exec* ex) {
+  if (!ex || ex->rank_node == 0) {
+    set_error("hg_exec_ipc_close: needs a per-rank executor");
+    return HG_EINVAL;
+  }
+  HG_CUDA(cudaSetDevice(ex->dev[ex->rank_node - 1]));
+  for (int g = 0; g < ex->k; ++g) {
+    if (ex->ipc[g] && ex->base[g]) {
+      HG_CUDA(cudaIpcCloseMemHandle(ex->base[g]));
+      ex->base[g] = nullptr;
+      ex->ipc[g] = 0;
+    }
+  }
+  return HG_OK;
+}
+
+// Page-lock caller-owned host memory (the tile-major input / output images) so the plan's H2D
+// jobs and the write-back run as async DMA instead of staged pageable copies.  The caller keeps
+// ownership; hg_matrix_unregister before freeing it.
+extern "C" int hg_matrix_register(void* host, size_t bytes) {
+  if (!host || bytes == 0) {
+    set_error("hg_matrix_register: null pointer or empty range");
+    return HG_EINVAL;
+  }
+  cudaError_t e = cudaHostRegister(host, bytes, cudaHostRegisterPortable);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return HG_OK;
+  }
+  if (e != cudaSuccess) {
+    set_error("cudaHostRegister(%p, %zu): %s", host, bytes, cudaGetErrorString(e));
+    cudaGetLastError();
+    return HG_ECUDA;
+  }
+  return HG_OK;
+}
+
+extern "C" int hg_matrix_unregister(void* host) {
+  if (!host) {
+    set_error("hg_matrix_unregister: null pointer");
+    return HG_EINVAL;
+  }
+  cudaError_t e = cudaHostUnregister(host);
+  if (e != cudaSuccess && e != cudaErrorHostMemoryNotRegistered) {
+    set_error("cudaHostUnregister(%p): %s", host, cudaGetErrorString(e));
+    cudaGetLastError();
+    return HG_ECUDA;
+  }
+  cudaGetLastError();
   return HG_OK;
 }

@@ -23,7 +23,7 @@ from . import _native
 from .graph import AccessMode
 from .kernels import ALL_KINDS
 from .platform import PlatformError, ResourceClass
-from .sim import make_plan
+from .sim import SimReport, TaskRun, TraceEvent, make_plan
 
 
 # -- host layout helpers --------------------------------------------------------
@@ -80,6 +80,39 @@ class ExecStats:
     n_copy_nodes: int
 
 
+@dataclass(eq=True)
+class ExecReport(SimReport):
+    """The reference's ``SimReport`` (sim.py:66-80) filled from an EXECUTED run in trace
+    mode: ``schedule[t] = TaskRun(worker, start, end)`` are measured device times (s,
+    origin = the first stamp of the run), ``makespan`` / ``gflops`` measured, the byte
+    counters those the copy nodes moved, ``busy[w]`` the time GPU worker ``w`` had at least
+    one task running (tasks overlap on a B200, so this is the union of their intervals),
+    ``events`` (``trace=True``) the measured ``task_start`` / ``task_end`` /
+    ``transfer_start`` / ``transfer_end`` TraceEvents (sim.py:145-147, 169-188) sorted by
+    time.  Extras: ``planned`` (the plan's own SimReport, for planned-vs-measured),
+    ``task_seconds[w]`` (sum of task durations on ``w``), ``jobs[j] = (worker, start, end,
+    block, nbytes)`` and ``elapsed_ms`` (CUDA-event time of the graph)."""
+
+    planned: SimReport = None
+    task_seconds: tuple = ()
+    jobs: dict = None
+    elapsed_ms: float = 0.0
+
+
+def _union_length(intervals) -> float:
+    tot, cur_s, cur_e = 0.0, None, None
+    for a, b in sorted(intervals):
+        if cur_e is None or a > cur_e:
+            if cur_e is not None:
+                tot += cur_e - cur_s
+            cur_s, cur_e = a, b
+        else:
+            cur_e = max(cur_e, b)
+    if cur_e is not None:
+        tot += cur_e - cur_s
+    return tot
+
+
 def _gpu_nodes(plan, platform):
     if platform.n_cpu_workers:
         cpu_tasks = int(np.count_nonzero(plan.worker < platform.n_cpu_workers))
@@ -95,7 +128,7 @@ class Executor:
 
     def __init__(self, graph, platform, plan, host_in: np.ndarray, host_out: np.ndarray | None = None,
                  devices=None, device_input: bool = False, host_side_out: np.ndarray | None = None,
-                 rank_node: int = 0, priority_levels: int = 6):
+                 rank_node: int = 0, priority_levels: int = 6, trace: bool = False):
         L = _native.lib()
         lay = graph.layout
         if lay is None:
@@ -130,6 +163,9 @@ class Executor:
         self.host_out = host_out
         self.host_side_out = host_side_out
         self.plan = plan
+        self.graph = graph
+        self.platform = platform
+        self.trace = bool(trace)
         self.devices = devices
         # node priorities from the plan's own predicted durations (end - start):
         # changes only which ready kernel gets SMs first, never the plan
@@ -155,7 +191,7 @@ class Executor:
             int(bool(device_input)), int(rank_node),
             _native.ptr(self.task_weight, C.c_double),
             _native.ptr(self.host_stage, C.c_double) if self.host_stage is not None else None,
-            int(priority_levels))
+            int(priority_levels), int(self.trace))
         h = C.c_void_p()
         _native.check(L.hg_exec_create(C.byref(ep), C.byref(opts), C.byref(h)), "hg_exec_create")
         self._h = h
@@ -181,6 +217,63 @@ class Executor:
         _native.check(_native.lib().hg_exec_info(self._h, C.byref(st)), "hg_exec_info")
         return ExecStats(st.elapsed_ms, st.bytes_h2d, st.bytes_d2d, st.bytes_d2h, st.bytes_side,
                          st.n_kernel_nodes, st.n_copy_nodes)
+
+    def stamps(self) -> np.ndarray:
+        """Trace mode: device ns [start, end] per task (rows 0..n-1) then per copy job."""
+        if not self.trace:
+            raise ValueError("executor was created without trace=True")
+        n = len(self.graph) + self.plan.n_jobs
+        out = np.zeros(2 * n, np.uint64)
+        _native.check(_native.lib().hg_exec_read_stamps(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64))),
+                      "hg_exec_read_stamps")
+        return out.reshape(n, 2)
+
+    def report(self, stats: ExecStats | None = None, events: bool = False) -> ExecReport:
+        """The last run as an :class:`ExecReport` (needs ``trace=True``)."""
+        st = self.stamps().astype(np.int64)
+        stats = stats or self.info()
+        plan, graph, plat = self.plan, self.graph, self.platform
+        n = len(graph)
+        mine = st[:, 0] > 0
+        if not mine.any():
+            raise RuntimeError("no stamps recorded: run the executor first")
+        t0 = int(st[mine, 0].min())
+        sec = (st - t0) * 1e-9
+        ncpu = plat.n_cpu_workers
+        sched, per_w, per_w_sum = {}, {}, {}
+        for t in range(n):
+            if st[t, 0] == 0:
+                continue
+            w = int(plan.worker[t])
+            sched[t] = TaskRun(w, float(sec[t, 0]), float(sec[t, 1]))
+            per_w.setdefault(w, []).append((sec[t, 0], sec[t, 1]))
+            per_w_sum[w] = per_w_sum.get(w, 0.0) + float(sec[t, 1] - sec[t, 0])
+        jobs = {}
+        for j in range(plan.n_jobs):
+            if st[n + j, 0] == 0:
+                continue
+            jobs[j] = (ncpu + int(plan.job_dst[j]) - 1, float(sec[n + j, 0]), float(sec[n + j, 1]),
+                       int(plan.job_block[j]), int(plan.job_bytes[j]))
+        span = max((r.end for r in sched.values()), default=0.0)
+        work = sum(t.flops for t in graph.tasks if t.id in sched)
+        busy = tuple(_union_length(per_w.get(w, [])) for w in range(plat.n_workers))
+        ev = None
+        if events:
+            ev = []
+            for t, r in sched.items():
+                ev.append(TraceEvent(r.start, "task_start", r.worker, t, -1, 0))
+                ev.append(TraceEvent(r.end, "task_end", r.worker, t, -1, 0))
+            for j, (w, a, b, blk, nbytes) in jobs.items():
+                ev.append(TraceEvent(a, "transfer_start", w, int(plan.job_requester[j]), blk, nbytes))
+                ev.append(TraceEvent(b, "transfer_end", w, int(plan.job_requester[j]), blk, nbytes))
+            ev.sort(key=lambda e: (e.time, e.kind))
+        return ExecReport(
+            makespan=span, gflops=work / span / 1e9 if span > 0 else 0.0,
+            bytes_h2d=int(stats.bytes_h2d), bytes_d2h=int(stats.bytes_d2h), bytes_d2d=int(stats.bytes_d2d),
+            bytes_total=int(stats.bytes_h2d + stats.bytes_d2h + stats.bytes_d2d), steals_ok=0, steals_failed=0,
+            busy=busy, schedule=sched, events=ev, planned=plan.report(),
+            task_seconds=tuple(per_w_sum.get(w, 0.0) for w in range(plat.n_workers)), jobs=jobs,
+            elapsed_ms=float(stats.elapsed_ms))
 
     def read_block(self, block: int, node: int, doubles: int) -> np.ndarray:
         out = np.empty(doubles, np.float64)
@@ -212,7 +305,8 @@ class DistributedExecutor(Executor):
     """
 
     def __init__(self, graph, platform, plan, host_in, host_out=None, rank=None, world=None, device=None,
-                 device_input=False, host_side_out=None, group=None, priority_levels: int = 6):
+                 device_input=False, host_side_out=None, group=None, priority_levels: int = 6,
+                 wait_timeout: float = 60.0):
         import torch.distributed as dist
 
         rank = dist.get_rank(group) if rank is None else rank
@@ -225,6 +319,9 @@ class DistributedExecutor(Executor):
                          device_input=device_input, host_side_out=host_side_out, rank_node=rank + 1,
                          priority_levels=priority_levels)
         L = _native.lib()
+        self._group = group
+        # every cross-rank spin is bounded: a dead peer raises DeadlockError instead of hanging
+        _native.check(L.hg_exec_set_wait_timeout(self._h, float(wait_timeout)), "hg_exec_set_wait_timeout")
         mine = (C.c_char * 64)()
         _native.check(L.hg_exec_ipc_handle(self._h, mine), "hg_exec_ipc_handle")
         handles = exchange_handles(bytes(mine), world, group)
@@ -234,6 +331,28 @@ class DistributedExecutor(Executor):
                 _native.check(L.hg_exec_ipc_open(self._h, r + 1, buf), "hg_exec_ipc_open")
         _native.check(L.hg_exec_build(self._h), "hg_exec_build")
         dist.barrier(group=group)
+
+    def close(self):
+        """Collective teardown: wait for this rank's runs, barrier (every peer is done pulling
+        from this rank's pool), unmap the peers' pools, barrier (nobody maps this pool any
+        more), then free.  Freeing an exported allocation while an importer still maps or reads
+        it is undefined behaviour (cudaIpcCloseMemHandle)."""
+        if not getattr(self, "_h", None):
+            return
+        import torch.distributed as dist
+
+        L = _native.lib()
+        try:
+            L.hg_exec_wait(self._h)
+        finally:
+            dist.barrier(group=self._group)
+            L.hg_exec_ipc_close(self._h)
+            dist.barrier(group=self._group)
+            super().close()
+
+    def __del__(self):
+        # no collectives from a finaliser: an un-closed per-rank executor leaks its pool
+        pass
 
 
 def check_same_plan(plan, world, group=None):
@@ -312,20 +431,57 @@ def ExecPlan_from(plan, n, n_blocks, k, lay, ex, fl):
         P(plan.job_stage_job, C.c_int32), int(bool(ex.p2p)))
 
 
+class pinned_host:
+    """Context manager: page-lock caller-owned NumPy images for the duration of a run
+    (``hg_matrix_register`` = cudaHostRegister), so the plan's H2D jobs and the write-back
+    are async DMA rather than staged pageable copies.  Already pinned memory (e.g. torch
+    ``pin_memory``) is left alone."""
+
+    def __init__(self, *arrays):
+        self.arrays = [a for a in arrays if a is not None and a.nbytes > 0]
+        self.done = []
+
+    def __enter__(self):
+        L = _native.lib()
+        for a in self.arrays:
+            if not a.flags.c_contiguous:
+                raise ValueError("host images must be contiguous")
+            _native.check(L.hg_matrix_register(C.c_void_p(a.ctypes.data), a.nbytes), "hg_matrix_register")
+            self.done.append(a)
+        return self
+
+    def __exit__(self, *exc):
+        L = _native.lib()
+        for a in self.done:
+            L.hg_matrix_unregister(C.c_void_p(a.ctypes.data))
+        self.done = []
+
+
 def execute(graph, platform, scheduler, model, host_in: np.ndarray, host_out: np.ndarray | None = None,
-            devices=None, plan=None):
-    """Plan (bit-exact, native) and execute one factorization; returns (plan, stats).
+            devices=None, plan=None, host_side_out: np.ndarray | None = None, register_host: bool = True,
+            report: bool = False, trace: bool = False):
+    """Plan (bit-exact, native) and execute one factorization; returns (plan, stats, host_out),
+    with ``report=True`` (plan, ExecReport, host_out) -- the executed run in the reference's
+    ``SimReport`` form (``trace=True`` adds the measured TraceEvents).
 
     ``host_in`` is the tile-major input image; the factor is written to
-    ``host_out`` (defaults to a fresh array) in the same layout.
+    ``host_out`` (defaults to a fresh array) in the same layout.  With
+    ``register_host`` the images are page-locked for the call (``hg_matrix_register``).
     """
+    report = report or trace
     if plan is None:
         plan = make_plan(graph, platform, scheduler, model)
+    host_in = np.ascontiguousarray(host_in, np.float64)
     if host_out is None:
         host_out = np.zeros_like(host_in)
-    ex = Executor(graph, platform, plan, host_in, host_out, devices=devices)
-    try:
-        stats = ex.run()
-    finally:
-        ex.close()
+    pin = pinned_host(host_in, host_out, host_side_out) if register_host else pinned_host()
+    with pin:
+        ex = Executor(graph, platform, plan, host_in, host_out, devices=devices, host_side_out=host_side_out,
+                      trace=report)
+        try:
+            stats = ex.run()
+            if report:
+                stats = ex.report(stats, events=trace)
+        finally:
+            ex.close()
     return plan, stats, host_out

@@ -27,6 +27,6 @@ def test_library_exports_every_declared_symbol():
 
 def test_cpu_only_host_calls():
     L = _native.lib()
-    assert L.hg_abi_version() == 2
+    assert L.hg_abi_version() == 3
     assert L.hg_device_count() >= 0
     assert isinstance(_native.last_error(), str)

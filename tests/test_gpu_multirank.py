@@ -1,7 +1,11 @@
 """One process per GPU node on a real device: two ranks (both on cuda:0 here,
 the only GPU a gpurun box has) execute a k=2 plan through CUDA IPC pools and
 cross-process device flags; the union of their write-backs must equal the
-CPU oracle's factor and the executed copy bytes must equal the plan's."""
+CPU oracle's factor and the executed copy bytes must equal the plan's.  The
+nt=16 cases have hundreds of cross-rank pulls and flag waits (the gated,
+chained wait nodes of runtime.cu keep at most 8 spinners resident per rank).
+A rank whose peer never launches must fail with DeadlockError after the wait
+timeout instead of hanging the device."""
 import math
 import os
 import socket
@@ -19,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank_main(rank, world, port, family, q):
+def _rank_main(rank, world, port, family, q, n=2048, b=512):
     import torch.distributed as dist
 
     import paper_1402_6601_b200 as H
@@ -29,7 +33,7 @@ def _rank_main(rank, world, port, family, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        n, b, ib = 2048, 512, 128
+        ib = 128 if b >= 512 else 64
         g = H.gen_family(family, n // b, b, ib)
         plat = H.build_platform(world, world, world, link_bandwidth=7.7e11, link_latency=3e-6,
                                 switch_cap=math.inf, p2p=True)
@@ -53,8 +57,9 @@ def _rank_main(rank, world, port, family, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("family", ["cholesky", "lu"])
-def test_two_ranks_one_gpu(family):
+@pytest.mark.parametrize("family,n,b", [("cholesky", 2048, 512), ("lu", 2048, 512),
+                                        ("cholesky", 8192, 512), ("lu", 4096, 256)])
+def test_two_ranks_one_gpu(family, n, b):
     import torch.multiprocessing as mp
 
     import paper_1402_6601_b200 as H
@@ -64,14 +69,14 @@ def test_two_ranks_one_gpu(family):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, family, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, family, q, n, b)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]
     for p in procs:
         p.join(60)
         assert p.exitcode == 0
-    n, b, ib = 2048, 512, 128
+    ib = 128 if b >= 512 else 64
     g = H.gen_family(family, n // b, b, ib)
     plat = H.build_platform(2, 2, 2, link_bandwidth=7.7e11, link_latency=3e-6, switch_cap=math.inf, p2p=True)
     plan = H.make_plan(g, plat, H.make_scheduler("dada", alpha=0.5, cp=True), H.PerfModel(H.default_timing_table(b, ib)))
@@ -87,3 +92,57 @@ def test_two_ranks_one_gpu(family):
     if family == "cholesky":
         ref, got = np.tril(ref), np.tril(got)
     assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-11
+
+
+def _dead_peer_main(rank, world, port, q):
+    """Rank 1 builds its graph but never launches it (a dead / stuck peer)."""
+    import time
+
+    import torch.distributed as dist
+
+    import paper_1402_6601_b200 as H
+    from paper_1402_6601_b200 import runtime
+    from paper_1402_6601_b200.sim import DeadlockError
+    from oracle import tiles as O
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, b = 2048, 512
+        g = H.gen_cholesky(n // b, b)
+        plat = H.build_platform(2, 2, 2, link_bandwidth=7.7e11, link_latency=3e-6, switch_cap=math.inf, p2p=True)
+        plan = H.make_plan(g, plat, H.make_scheduler("dada", alpha=0.5, cp=True),
+                           H.PerfModel(H.default_timing_table(b, 128)))
+        img = runtime.to_tile_major(O.spd_matrix(n, 1), g)
+        ex = runtime.DistributedExecutor(g, plat, plan, img, np.zeros_like(img), rank=rank, world=world,
+                                         device=0, wait_timeout=2.0)
+        outcome = "idle"
+        if rank == 0:
+            t0 = time.perf_counter()
+            ex.launch(0)
+            try:
+                ex.wait()
+                outcome = "finished"
+            except DeadlockError as e:
+                outcome = f"deadlock {time.perf_counter() - t0:.1f}s {e}"
+        ex.close()
+        q.put((rank, outcome))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dead_peer_raises_deadlock():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dead_peer_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    assert res[0].startswith("deadlock"), res
+    assert "timed out" in res[0]
