@@ -31,8 +31,29 @@ Side areas (ride inside their tile) are kept in a dict:
 
 from __future__ import annotations
 
+import ctypes
+import os
+
 import numpy as np
 from scipy.linalg import lapack, solve_triangular
+
+# Optional plain-C restatement of the two column loops below (oracle/lu_panel.c, bit-identical;
+# `make -C oracle`).  HG_ORACLE_PURE=1 forces the NumPy loops.
+_C = None
+_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liboracle.so")
+if os.path.exists(_LIB) and os.environ.get("HG_ORACLE_PURE") != "1":
+    try:
+        _C = ctypes.CDLL(_LIB)
+        _dp, _i64p, _i = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), ctypes.c_int
+        _C.ora_getrf_panel.argtypes = [_dp, _i, _i, _i, _i, _i64p]
+        _C.ora_tstrf_panel.argtypes = [_dp, _i, _dp, _i, _i, _i, _i, _i64p, _dp, _i]
+    except OSError:
+        _C = None
+
+
+def _fptr(x):
+    assert x.flags.f_contiguous and x.dtype == np.float64
+    return x.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
 def _panels(nb, ib):
@@ -47,11 +68,18 @@ def _unit_lower_solve(L, B):
 # -- LU ------------------------------------------------------------------------
 
 
-def getrf_inc(a: np.ndarray, ib: int):
+def getrf_inc(a: np.ndarray, ib: int, pure: bool = False):
     nb = a.shape[0]
     ipiv = np.zeros(nb, np.int64)
     singular = False
+    use_c = _C is not None and not pure and a.flags.f_contiguous
     for ii, sb in _panels(nb, ib):
+        if use_c:
+            singular |= bool(_C.ora_getrf_panel(_fptr(a), a.shape[0], a.shape[0], ii, sb,
+                                                ipiv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+            if ii + sb < nb:
+                _apply_getrf_panel(a, ipiv, ii, sb, a[:, ii + sb:])
+            continue
         for j in range(ii, ii + sb):
             p = j + int(np.argmax(np.abs(a[j:, j])))
             ipiv[j] = p
@@ -100,12 +128,20 @@ def _apply_ts_panel(ipiv, dl, la, ii, sb, top, bot):
     bot -= la[:, ii:ii + sb] @ top
 
 
-def tstrf(u: np.ndarray, a: np.ndarray, ib: int):
+def tstrf(u: np.ndarray, a: np.ndarray, ib: int, pure: bool = False):
     nb = u.shape[0]
     ipiv = np.full(nb, -1, np.int64)
-    dl = np.zeros((ib, nb))
+    dl = np.zeros((ib, nb), order="F")
     singular = False
+    use_c = _C is not None and not pure and u.flags.f_contiguous and a.flags.f_contiguous
     for ii, sb in _panels(nb, ib):
+        if use_c:
+            singular |= bool(_C.ora_tstrf_panel(_fptr(u), u.shape[0], _fptr(a), a.shape[0], a.shape[0], ii, sb,
+                                                ipiv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                                _fptr(dl), ib))
+            if ii + sb < nb:
+                _apply_ts_panel(ipiv, dl, a, ii, sb, u[ii:ii + sb, ii + sb:], a[:, ii + sb:])
+            continue
         for j in range(ii, ii + sb):
             r = int(np.argmax(np.abs(a[:, j])))
             if abs(a[r, j]) > abs(u[j, j]):

@@ -255,3 +255,23 @@ def test_process_executor_matches_sequential(fam):
     for d in side:
         for key, v in side[d].items():
             assert np.array_equal(np.asarray(s2[d][key])[: v.shape[0]], v), (d, key)
+
+
+@pytest.mark.parametrize("nb,ib", [(64, 16), (128, 32), (96, 96)])
+def test_c_panels_match_numpy(nb, ib):
+    """oracle/lu_panel.c (the fast column loops) == the NumPy loops bit for bit."""
+    if LQ._C is None:
+        pytest.skip("oracle/liboracle.so not built (make -C oracle)")
+    rng = np.random.default_rng(nb + ib)
+    a0 = np.asfortranarray(rng.uniform(-0.5, 0.5, (nb, nb)))
+    a1, a2 = a0.copy(order="F"), a0.copy(order="F")
+    p1, s1 = LQ.getrf_inc(a1, ib)
+    p2, s2 = LQ.getrf_inc(a2, ib, pure=True)
+    assert np.array_equal(p1, p2) and s1 == s2 and np.array_equal(a1, a2)
+    u0 = np.asfortranarray(np.triu(rng.uniform(-0.5, 0.5, (nb, nb))) + np.diag(rng.uniform(0.05, 0.2, nb)))
+    u1, u2 = u0.copy(order="F"), u0.copy(order="F")
+    b1, b2 = a0.copy(order="F"), a0.copy(order="F")
+    q1, d1, _ = LQ.tstrf(u1, b1, ib)
+    q2, d2, _ = LQ.tstrf(u2, b2, ib, pure=True)
+    assert (q1 >= 0).any()
+    assert np.array_equal(q1, q2) and np.array_equal(u1, u2) and np.array_equal(b1, b2) and np.array_equal(d1, d2)

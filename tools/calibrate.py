@@ -25,6 +25,7 @@ sys.path.insert(0, ROOT)
 
 import paper_1402_6601_b200 as H  # noqa: E402
 from paper_1402_6601_b200 import _native  # noqa: E402
+from paper_1402_6601_b200 import kernels as K  # noqa: E402
 
 PROJECTED_TF = {"GEMM": 30, "SSSSM": 28, "TSMQR": 26, "SYRK": 25, "UNMQR": 22, "TRSM": 20, "GESSM": 20,
                 "TSQRT": 5, "TSTRF": 4, "POTRF": 3, "GEQRT": 3, "GETRF_INC": 2}
@@ -87,41 +88,65 @@ def gpu_times(nb, ib, reps):
 
 
 def cpu_times(nb, ib, reps):
-    from scipy.linalg import blas, lapack
+    """One host core per kind, running the ORACLE's own tile kernels (oracle/cpu_exec.run_task:
+    SciPy dpotrf/dtrsm/dsyrk/dgemm, the NumPy GETRF_INC/GESSM/TSTRF/SSSSM restatement, LAPACK
+    dgeqrt/dgemqrt/dtpqrt/dtpmqrt) on the access lists of kernels.py -- the CPU path the
+    cost model's CPU column stands for (kernels.py:62-105, perfmodel.py:170-199).  Median of
+    ``reps`` runs, inputs restored before each run (outside the timing)."""
     from threadpoolctl import threadpool_limits
 
-    rng = np.random.default_rng(1)
-    a = np.asfortranarray(rng.uniform(-0.5, 0.5, (nb, nb)))
-    b = np.asfortranarray(rng.uniform(-0.5, 0.5, (nb, nb)))
-    c = np.asfortranarray(rng.uniform(-0.5, 0.5, (nb, nb)))
-    spd = np.asfortranarray((a + a.T) / 2 + nb * np.eye(nb))
-    lo = np.asfortranarray(np.linalg.cholesky(spd))
-    two = np.asfortranarray(np.vstack([np.triu(a), b]))
-
-    def med(f):
-        f()
-        ts = []
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            f()
-            ts.append(time.perf_counter() - t0)
-        return float(np.median(ts))
+    from oracle import cpu_exec
 
     out = {}
-    with threadpool_limits(1):
-        out["POTRF"] = med(lambda: lapack.dpotrf(spd, lower=1))
-        out["TRSM"] = med(lambda: blas.dtrsm(1.0, lo, b, side=1, lower=1, trans_a=1))
-        out["SYRK"] = med(lambda: blas.dsyrk(-1.0, a, beta=1.0, c=c, lower=1))
-        out["GEMM"] = med(lambda: blas.dgemm(-1.0, a, b, beta=1.0, c=c, trans_b=1))
-        out["GETRF_INC"] = med(lambda: lapack.dgetrf(a))
-        out["GESSM"] = med(lambda: blas.dtrsm(1.0, lo, b, side=0, lower=1, diag=1))
-        out["TSTRF"] = med(lambda: lapack.dgetrf(two))
-        out["SSSSM"] = med(lambda: blas.dgemm(-1.0, a, b, beta=1.0, c=c))
-        out["GEQRT"] = med(lambda: lapack.dgeqrt(ib, a))
-        out["UNMQR"] = out["GEMM"]
-        out["TSQRT"] = med(lambda: lapack.dgeqrf(two))
-        out["TSMQR"] = 2.0 * out["GEMM"]
+    for fam, kinds in (("cholesky", K.CHOLESKY_KINDS), ("lu", K.LU_KINDS), ("qr", K.QR_KINDS)):
+        g = H.gen_family(fam, 3, nb, ib)  # 3x3 tiles: at least one task of every kind
+        rng = np.random.default_rng(7)
+        n = 3 * nb
+        R = rng.uniform(-0.5, 0.5, (n, n))
+        A = (R + R.T) / 2 + n * np.eye(n) if fam == "cholesky" else R
+        arena = cpu_exec.TileArena(g).load(A)
+        first = {}
+        for t in g.tasks:
+            first.setdefault(t.kind, t.id)
+        with threadpool_limits(1):
+            for kind in kinds:
+                tid = first[kind]
+                # state right before task tid: replay the tasks before it once
+                arena.load(A)
+                for u in range(tid):
+                    cpu_exec.run_task(arena, g.tasks[u])
+                snap = {d: arena.tiles[d].copy() for d in arena.ids}
+                side = {d: (arena.aux[d].copy(), arena.piv[d].copy()) for d in arena.aux}
+                ts = []
+                for _ in range(reps + 1):
+                    for d in arena.ids:
+                        arena.tiles[d][...] = snap[d]
+                    for d, (a, p) in side.items():
+                        arena.aux[d][...] = a
+                        arena.piv[d][...] = p
+                    t0 = time.perf_counter()
+                    cpu_exec.run_task(arena, g.tasks[tid])
+                    ts.append(time.perf_counter() - t0)
+                out[kind] = float(np.median(ts[1:]))
     return out
+
+
+def update_cpu_column(paths, cpu, nb, ib):
+    """Rewrite the CPU lines of existing timing tables with ``cpu`` (GPU lines untouched)."""
+    for path in paths:
+        lines = open(path).read().splitlines()
+        outl = []
+        for ln in lines:
+            if ln.startswith("#") or not ln.strip():
+                outl.append(ln)
+                continue
+            kind, cls, _ = ln.split(",")
+            outl.append(f"{kind},CPU,{cpu[kind]!r}" if cls == "CPU" else ln)
+        note = (f"# CPU column: 1 host core running the oracle's own tile kernels (oracle/cpu_exec.run_task), "
+                f"nb={nb} ib={ib}, median; written by tools/calibrate.py --cpu-only")
+        outl = [l for l in outl if not l.startswith("# CPU column:")]
+        outl.insert(1 if outl and outl[0].startswith("#") else 0, note)
+        open(path, "w").write("\n".join(outl) + "\n")
 
 
 def main():
@@ -130,7 +155,15 @@ def main():
     ap.add_argument("--ib", type=int, default=128)
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--cpu-only", nargs="*", default=None, metavar="TABLE",
+                    help="only measure the CPU column and rewrite it in these existing tables")
     args = ap.parse_args()
+    if args.cpu_only is not None:
+        c = cpu_times(args.nb, args.ib, max(3, args.reps // 3))
+        for kind in H.ALL_KINDS:
+            print(f"{kind:10s} CPU {c[kind] * 1e3:9.2f} ms  {H.kind_flops(kind, args.nb) / c[kind] / 1e9:6.1f} GF/s")
+        update_cpu_column(args.cpu_only, c, args.nb, args.ib)
+        return
     out = args.out or os.path.join(ROOT, "timings", f"b200_nb{args.nb}_ib{args.ib}.csv")
     g = gpu_times(args.nb, args.ib, args.reps)
     c = cpu_times(args.nb, args.ib, max(3, args.reps // 3))
