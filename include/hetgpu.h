@@ -167,6 +167,10 @@ typedef struct hg_exec_plan {
   const int8_t* acc_mode;     /* HG_ACCESS_* per access (CSR like acc_block) */
   const int32_t* job_stage_job; /* host-staged route: the job whose first leg stages the block, or -1 */
   int32_t p2p;                /* 0: every GPU->GPU job is host-staged (GPU->host->GPU, platform.py:117) */
+  int32_t push;               /* 1: producer-push fusion -- a peer job moving a version written by a
+                                 POTRF / TRSM / SYRK / GEMM task is done by that task's own kernels
+                                 (epilogue stores into the consumer GPU's slot), not a copy node;
+                                 bytes per (version, destination) stay the plan's */
 } hg_exec_plan;
 
 typedef struct hg_exec_opts {
@@ -205,6 +209,7 @@ typedef struct hg_exec_stats {
   int64_t bytes_side;         /* side-area bytes that rode along with peer copies */
   int32_t n_kernel_nodes;
   int32_t n_copy_nodes;
+  int32_t n_push_jobs;        /* plan jobs delivered by producer-push (no copy node) */
 } hg_exec_stats;
 
 int hg_exec_create(const hg_exec_plan* plan, const hg_exec_opts* opts, hg_exec** out);

@@ -67,7 +67,7 @@ class ExecPlan(C.Structure):
                 ("wait_job", _i32p), ("job_block", _i32p), ("job_src", _i32p), ("job_dst", _i32p),
                 ("job_version", _i32p), ("job_src_job", _i32p), ("job_requester", _i32p),
                 ("block_bytes", _i64p), ("final_writer", _i32p), ("acc_mode", _i8p),
-                ("job_stage_job", _i32p), ("p2p", C.c_int32)]
+                ("job_stage_job", _i32p), ("p2p", C.c_int32), ("push", C.c_int32)]
 
 
 class ExecOpts(C.Structure):
@@ -80,7 +80,7 @@ class ExecOpts(C.Structure):
 class ExecStats(C.Structure):
     _fields_ = [("elapsed_ms", C.c_double), ("bytes_h2d", C.c_int64), ("bytes_d2d", C.c_int64),
                 ("bytes_d2h", C.c_int64), ("bytes_side", C.c_int64), ("n_kernel_nodes", C.c_int32),
-                ("n_copy_nodes", C.c_int32)]
+                ("n_copy_nodes", C.c_int32), ("n_push_jobs", C.c_int32)]
 
 
 EXPORTS = ("hg_last_error", "hg_abi_version", "hg_device_count", "hg_plan_build", "hg_plan_free",

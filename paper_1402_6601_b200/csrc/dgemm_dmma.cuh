@@ -13,6 +13,7 @@
 // loads (4 k-rows x 8 consecutive rows per half-warp) hit 32 distinct banks.
 #pragma once
 #include "hg_common.cuh"
+#include "tiles.h"
 
 namespace hg {
 
@@ -469,7 +470,7 @@ namespace hg {
 // lower: skip r < c of a diagonal tile (m0 == n0).
 template <class Cfg>
 HG_DEVICE void sub_store(double (&acc)[Cfg::FM][Cfg::FN][2], double* __restrict__ C, int ldc, int m0, int n0,
-                         bool lower = false, bool init = false) {
+                         bool lower = false, bool init = false, const PushList* push = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = (warp % Cfg::WARPS_M) * Cfg::WM;
   const int wn = (warp / Cfg::WARPS_M) * Cfg::WN;
@@ -492,8 +493,16 @@ HG_DEVICE void sub_store(double (&acc)[Cfg::FM][Cfg::FN][2], double* __restrict_
     for (int j = 0; j < Cfg::FN; ++j) {
       const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t;
       const double b0 = init ? 0.0 : cv[i][j][0], b1 = init ? 0.0 : cv[i][j][1];
-      if (!diag || r >= c) C[size_t(n0 + c) * ldc + m0 + r] = b0 - acc[i][j][0];
-      if (!diag || r >= c + 1) C[size_t(n0 + c + 1) * ldc + m0 + r] = b1 - acc[i][j][1];
+      const size_t o0 = size_t(n0 + c) * ldc + m0 + r, o1 = o0 + ldc;
+      const double v0 = b0 - acc[i][j][0], v1 = b1 - acc[i][j][1];
+      const bool s0 = !diag || r >= c, s1 = !diag || r >= c + 1;
+      if (s0) C[o0] = v0;
+      if (s1) C[o1] = v1;
+      if (push)  // producer-push: the final value also goes to every consumer GPU's slot (peer stores)
+        for (int q = 0; q < push->n; ++q) {
+          if (s0) __stcg(push->dst[q] + o0, v0);
+          if (s1) __stcg(push->dst[q] + o1, v1);
+        }
     }
 }
 

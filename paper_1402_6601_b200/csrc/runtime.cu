@@ -319,6 +319,9 @@ struct hg_exec {
   std::vector<int32_t> job_block, job_src, job_dst, job_version, job_src_job, job_requester, final_writer;
   std::vector<int32_t> job_stage_job;
   int p2p = 1;
+  int push = 0;                          // producer-push fusion requested (hg_exec_plan.push)
+  std::vector<char> job_push;            // job delivered by its version's producer kernel (no copy node)
+  std::vector<std::vector<int>> push_to; // per task: destination nodes its kernels push the output to
   double* host_stage = nullptr;          // p2p = 0: pinned staging image, slot-sized regions
   std::vector<int64_t> stage_off;
   // options
@@ -435,6 +438,33 @@ static void plan_layout(hg_exec* ex) {
   for (int j = 0; j < ex->n_jobs; ++j) need(ex->job_dst[j], ex->job_block[j]);
 }
 
+// Producer-push fusion: a peer job that moves version v (written by task v)
+// to GPU node D is delivered by task v's own kernels -- their epilogue stores the final tile to
+// D's slot as well (peer / IPC pointers) -- when v's kind supports it (tiles.h kind_can_push)
+// and v has at most kMaxPush such destinations.  Bytes per (version, destination) equal the
+// plan's; the copy node disappears and the consumer depends on task v itself.  WAR-safe: every
+// reader of any older version of the block precedes v in the DAG (graph.py:58-84), and the
+// step fence orders runs across ranks.  Deterministic from the plan, so every rank agrees.
+static void plan_push(hg_exec* ex) {
+  ex->job_push.assign(ex->n_jobs, 0);
+  ex->push_to.assign(ex->n_tasks, {});
+  if (!ex->push || !ex->p2p || ex->k < 2) return;
+  for (int j = 0; j < ex->n_jobs; ++j) {
+    const int v = ex->job_version[j], dst = ex->job_dst[j];
+    if (v < 0 || dst < 1 || ex->job_src[j] < 1 || !kind_can_push(ex->task_kind[v])) continue;
+    auto& d = ex->push_to[v];
+    if (std::find(d.begin(), d.end(), dst) == d.end()) d.push_back(dst);
+  }
+  for (auto& d : ex->push_to)
+    if ((int)d.size() > kMaxPush) d.clear();
+  for (int j = 0; j < ex->n_jobs; ++j) {
+    const int v = ex->job_version[j];
+    if (v < 0) continue;
+    const auto& d = ex->push_to[v];
+    ex->job_push[j] = std::find(d.begin(), d.end(), ex->job_dst[j]) != d.end();
+  }
+}
+
 // Which producers must signal (consumer on another, non-local node) and which
 // consumers must wait (producer on another, non-local node).
 struct Partition {
@@ -464,7 +494,13 @@ static Partition partition(const hg_exec* ex) {
   for (int j = 0; j < ex->n_jobs; ++j) {
     const int cn = ex->job_dst[j];
     if (ex->is_local(cn)) P.n_local_jobs++;
-    if (ex->job_src_job[j] >= 0) {
+    if (!ex->job_push.empty() && ex->job_push[j]) {  // delivered by the producer task itself
+      const int v = ex->job_version[j];
+      if (cross(ex->task_node[v], cn)) {
+        P.sig_task[v] = 1;
+        if (ex->is_local(cn)) wt[v] = 1;
+      }
+    } else if (ex->job_src_job[j] >= 0) {
       const int sj = ex->job_src_job[j];
       if (cross(ex->job_dst[sj], cn)) {
         P.sig_job[sj] = 1;
@@ -481,7 +517,8 @@ static Partition partition(const hg_exec* ex) {
   for (char w : wt) P.n_waits += w;
   P.waited = wt;
   for (int t = 0; t < ex->n_tasks; ++t) P.n_signals += P.sig_task[t] && ex->is_local(ex->task_node[t]);
-  for (int j = 0; j < ex->n_jobs; ++j) P.n_signals += P.sig_job[j] && ex->is_local(ex->job_dst[j]);
+  for (int j = 0; j < ex->n_jobs; ++j)
+    P.n_signals += P.sig_job[j] && ex->is_local(ex->job_dst[j]) && !(ex->job_push.size() && ex->job_push[j]);
   return P;
 }
 
@@ -543,17 +580,9 @@ static std::vector<int> task_priorities(const hg_exec* ex, int dev) {
   return prio;
 }
 
-// HG_URGENT=1: zero-slack tasks use the low-latency variant of their kind (experiment)
-static bool urgent_variants() {
-  static const bool v = [] {
-    const char* e = getenv("HG_URGENT");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
 static int build_graph(hg_exec* ex) {
   const int n = ex->n_tasks;
+  plan_push(ex);
   const Partition part = partition(ex);
   HG_CUDA(cudaGraphCreate(&ex->graph, 0));
   std::vector<cudaGraphNode_t> task_last(n, nullptr);
@@ -605,11 +634,8 @@ static int build_graph(hg_exec* ex) {
     if (ex->job_dst[j] >= 1) delivery.emplace(dkey(ex->job_block[j], v, ex->job_dst[j]), j);
   }
 
-  static const int h2d_chains = [] {
-    const char* e = getenv("HG_H2D_CHAINS");
-    return e ? atoi(e) : 1;
-  }();
-  std::vector<cudaGraphNode_t> h2d_tail(size_t(ex->k) * (h2d_chains > 0 ? h2d_chains : 1), nullptr);
+  constexpr int h2d_chains = 1;
+  std::vector<cudaGraphNode_t> h2d_tail(size_t(ex->k) * h2d_chains, nullptr);
   std::vector<int> h2d_count(ex->k, 0);
 
   // Cross-rank waits (one process per GPU).  Each spinning wait holds a CTA slot, so waits are
@@ -706,6 +732,15 @@ static int build_graph(hg_exec* ex) {
       const int b = ex->job_block[j], src = ex->job_src[j];
       deps.clear();
       int rc = HG_OK;
+      if (ex->job_push[j]) {
+        // delivered by the producer's epilogue: "arrival" is the producer task's completion
+        rc = dep_task(ex->job_version[j], dst);
+        if (rc) return rc;
+        job_node[j] = deps[0];
+        st.bytes_d2d += size_t(ex->blk_doubles[b]) * 8;
+        st.n_push_jobs++;
+        continue;
+      }
       const bool staged_in = src == 0 && (ex->job_version[j] >= 0 || ex->job_src_job[j] >= 0 ||
                                           ex->job_stage_job[j] >= 0);
       const bool staged_move = src >= 1 && dst >= 1 && !ex->p2p;
@@ -725,8 +760,7 @@ static int build_graph(hg_exec* ex) {
       if (rc) return rc;
       // host -> device first touches are serialised into one chain per GPU in dispatch order, so the
       // copy engine delivers tiles in the order tasks need them instead of all at once in arbitrary
-      // order (C2 e2e: 427 -> 372 ms, i.e. PCIe fully hidden behind compute; HG_H2D_CHAINS overrides,
-      // 0 = independent copies)
+      // order (C2 e2e: 427 -> 372 ms, i.e. PCIe fully hidden behind compute)
       const bool from_host = src == 0 && !ex->device_input && !staged_in;
       if (from_host && h2d_chains > 0) {
         cudaGraphNode_t& prev = h2d_tail[size_t(dst - 1) * h2d_chains + (h2d_count[dst - 1]++ % h2d_chains)];
@@ -816,7 +850,19 @@ static int build_graph(hg_exec* ex) {
       return HG_EINVAL;
     }
     for (int64_t a = a0; a < a1; ++a) ops.t[ops.n_t++] = ex->slot_ptr(node, ex->acc_block[a]);
-    ops.urgent = (use_prio && urgent_variants() && prio[t] == prio_greatest) ? 1 : 0;
+    if (!ex->push_to[t].empty()) {
+      int wb = -1;  // the block this task writes (last written access)
+      for (int64_t a = a0; a < a1; ++a)
+        if (ex->acc_mode.empty() || (ex->acc_mode[a] & HG_ACCESS_W)) wb = ex->acc_block[a];
+      for (int d : ex->push_to[t]) {
+        double* q = ex->slot_ptr(d, wb);
+        if (wb < 0 || !q) {
+          set_error("task %d: no slot of its output block on push destination node %d", t, d);
+          return HG_EINVAL;
+        }
+        ops.push.dst[ops.push.n++] = q;
+      }
+    }
     launches.clear();
     if (!build_task_launches(ex->task_kind[t], ops, launches)) return HG_EINVAL;
     deps.clear();
@@ -968,6 +1014,7 @@ extern "C" int hg_exec_create(const hg_exec_plan* P, const hg_exec_opts* O, hg_e
   ex->acc_mode = vcopy(P->acc_mode, P->acc_ptr[n]);
   ex->job_stage_job = vcopy(P->job_stage_job, P->n_jobs);
   ex->p2p = P->p2p;
+  ex->push = P->push;
   ex->host_stage = O->host_stage;
   if (!ex->p2p && P->k > 1) {
     if (!O->host_stage) {
@@ -1169,6 +1216,11 @@ extern "C" int hg_exec_partition(const hg_exec_plan* P, int32_t rank_node, int32
   ex.job_dst = vcopy(P->job_dst, nj);
   ex.job_version = vcopy(P->job_version, nj);
   ex.job_src_job = vcopy(P->job_src_job, nj);
+  ex.job_src = vcopy(P->job_src, nj);
+  ex.task_kind = vcopy(P->task_kind, n);
+  ex.p2p = P->p2p;
+  ex.push = P->push;
+  plan_push(&ex);
   Partition part = partition(&ex);
   counts4[0] = part.n_local_tasks;
   counts4[1] = part.n_local_jobs;

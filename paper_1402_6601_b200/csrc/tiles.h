@@ -15,6 +15,17 @@ namespace hg {
 
 constexpr int kParamBytes = 160;
 
+// Producer-push fusion: at most this many consumer GPUs receive a task's output tile
+// straight from the producing kernel (peer stores), see PushList / runtime.cu.
+constexpr int kMaxPush = 7;
+
+// Destinations of a pushed output tile: the same block's slot on up to kMaxPush other GPUs
+// (peer / IPC-mapped pointers; same nb x nb column-major layout as the local tile).
+struct PushList {
+  double* dst[kMaxPush];
+  int n;
+};
+
 struct LaunchDesc {
   const void* func = nullptr;
   dim3 grid, block;
@@ -40,9 +51,11 @@ struct TaskOperands {
   int* status = nullptr;  // device word; kernels OR error bits into it
   int* scratch = nullptr; // per-task device ints (task_scratch_ints), zero-initialised once;
                           // kernels keep them self-consistent across runs
-  int urgent = 0;         // 1: the task has (near) zero slack in the DAG (runtime priority level 0):
-                          // kinds with a latency/throughput trade-off pick their low-latency variant
+  PushList push{};        // producer-push: where the written tile also goes (kinds with push support)
 };
+
+// Kinds whose kernels can push their output tile to consumer GPUs in the epilogue.
+inline bool kind_can_push(int kind) { return kind >= 0 && kind <= 3; }  // POTRF, TRSM, SYRK, GEMM
 
 // Device ints of per-task scratch a kind needs (0 for most kinds).
 int task_scratch_ints(int kind, int nb, int ib);

@@ -39,13 +39,13 @@ struct GemmNTParams {
   double* C;
   int ld, M, N, K;
   int lower;  // 1: update only C(i, j) with i >= j (SYRK)
+  PushList push;  // producer-push destinations of C (runtime.cu), n = 0: none
 };
 
 using CfgG4 = GemmCfg<64, 64, 16, 32, 32, 4>;  // 4-stage ring, 3 CTAs / SM (default GEMM / SYRK tile)
 
-// CfgG: 3-stage ring, 4 CTAs / SM (smem allows 4)
-template <class G = CfgG, int MINB = 4>
-__global__ void __launch_bounds__(G::THREADS, MINB) k_gemm_nt(GemmNTParams p) {
+template <class G = CfgG4, int MINB = 3>
+__global__ void __launch_bounds__(G::THREADS, MINB) k_gemm_nt(const __grid_constant__ GemmNTParams p) {
   extern __shared__ double smem[];
   const int m0 = blockIdx.x * G::BM, n0 = blockIdx.y * G::BN;
   if (p.lower && m0 + G::BM - 1 < n0) return;  // tile strictly above the diagonal
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(G::THREADS, MINB) k_gemm_nt(GemmNTParams p) {
   TileLoader<G, M_MAJOR, G::BM> la{p.A, p.ld, m0};
   TileLoader<G, M_MAJOR, G::BN> lb{p.B, p.ld, n0};
   gemm_mainloop<G>(acc, smem, la, lb, 0, p.K);
-  sub_store<G>(acc, p.C, p.ld, m0, n0, p.lower != 0, false);
+  sub_store<G>(acc, p.C, p.ld, m0, n0, p.lower != 0, false, p.push.n ? &p.push : nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -652,6 +652,7 @@ struct PotrfParams {
   double* A;
   int nb;
   int* status;
+  PushList push;  // producer-push: the finished tile is also copied to these slots
 };
 
 constexpr int kSolveS = kR * (kR + 4);
@@ -737,7 +738,7 @@ __device__ void block_update(double* Cp, int ld, const LdA& la, const LdB& lb, b
   __syncthreads();
 }
 
-__global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS) k_potrf_cluster(PotrfParams p) {
+__global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS) k_potrf_cluster(const __grid_constant__ PotrfParams p) {
   extern __shared__ double smem[];
   // dynamic smem: [GEMM ring / solve buffers | s 64x65 | iv 64x65 | tm 32x33]
   auto s = reinterpret_cast<double(*)[kR + 1]>(smem + kPotrfSmemDoubles);
@@ -795,6 +796,16 @@ __global__ void __cluster_dims__(kPotrfCl, 1, 1) __launch_bounds__(CfgG::THREADS
     __threadfence();
     cl.sync();
   }
+  // producer-push: the finished tile (L_kk and M^T) streamed to the consumer GPUs' slots by the
+  // cluster that produced it (the last phase ended with a release/acquire cluster barrier)
+  if (p.push.n) {
+    const size_t n2 = size_t(nb) * nb / 2;
+    const double2* src = reinterpret_cast<const double2*>(A);
+    for (size_t e = size_t(q) * CfgG::THREADS + threadIdx.x; e < n2; e += size_t(kPotrfCl) * CfgG::THREADS) {
+      const double2 v = __ldcg(src + e);
+      for (int d = 0; d < p.push.n; ++d) __stcg(reinterpret_cast<double2*>(p.push.dst[d]) + e, v);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -813,6 +824,7 @@ struct TrsmInvParams {
   double* B;
   int* count;       // unused (the strip barrier is a cluster barrier); kept for the param layout
   int ld;
+  PushList push;    // producer-push destinations of B
 };
 
 template <class Cfg, int ROWS>
@@ -839,7 +851,7 @@ struct MRowLoader {  // rows j in [j0, j0+ROWS): element (j, k) = M(j, k)
 };
 
 template <int P>
-__global__ void __cluster_dims__(P, 1, 1) __launch_bounds__(CfgG::THREADS, 3) k_trsm_inv(TrsmInvParams p) {
+__global__ void __cluster_dims__(P, 1, 1) __launch_bounds__(CfgG::THREADS, 3) k_trsm_inv(const __grid_constant__ TrsmInvParams p) {
   extern __shared__ double smem[];
   const int ld = p.ld, nJ = ld / kR;
   // strip-major ids: the P CTAs of row strip I are one cluster (rank = pair)
@@ -861,12 +873,20 @@ __global__ void __cluster_dims__(P, 1, 1) __launch_bounds__(CfgG::THREADS, 3) k_
   // the cluster barrier (release / acquire) extends that to the whole strip
   cg::this_cluster().sync();
   double* B = p.B;
-  for_each_acc<CfgG>(acc0, [&](int r, int c, double v) { B[size_t(Js[0] * kR + c) * ld + I * kR + r] = v; });
-  for_each_acc<CfgG>(acc1, [&](int r, int c, double v) { B[size_t(Js[1] * kR + c) * ld + I * kR + r] = v; });
+  const int np = p.push.n;
+  for_each_acc<CfgG>(acc0, [&](int r, int c, double v) {
+    const size_t o = size_t(Js[0] * kR + c) * ld + I * kR + r;
+    B[o] = v;
+    for (int d = 0; d < np; ++d) __stcg(p.push.dst[d] + o, v);
+  });
+  for_each_acc<CfgG>(acc1, [&](int r, int c, double v) {
+    const size_t o = size_t(Js[1] * kR + c) * ld + I * kR + r;
+    B[o] = v;
+    for (int d = 0; d < np; ++d) __stcg(p.push.dst[d] + o, v);
+  });
 }
 
 // ---------------------------------------------------------------------------
-static unsigned gemm_smem() { return (unsigned)GemmSmem<CfgG, M_MAJOR, M_MAJOR>::BYTES; }
 static unsigned trsm_smem() { return (unsigned)GemmSmem<CfgG, M_MAJOR, K_MAJOR>::BYTES; }
 
 #define HG_ATTR(fn, attr, val)                                                                   \
@@ -879,7 +899,6 @@ static unsigned trsm_smem() { return (unsigned)GemmSmem<CfgG, M_MAJOR, K_MAJOR>:
   } while (0)
 
 bool init_chol_attributes() {
-  HG_ATTR((k_gemm_nt<CfgG, 4>), cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem());
   HG_ATTR((k_gemm_nt<CfgG4, 3>), cudaFuncAttributeMaxDynamicSharedMemorySize,
           (int)(GemmSmem<CfgG4, M_MAJOR, M_MAJOR>::BYTES));
   HG_ATTR(k_trsm_inv<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
@@ -891,18 +910,11 @@ bool init_chol_attributes() {
 }
 
 static void push_gemm(std::vector<LaunchDesc>& out, const double* A, const double* B, double* C,
-                      int ld, int M, int N, int K, int lower) {
+                      int ld, int M, int N, int K, int lower, const PushList& push) {
   LaunchDesc d;
-  GemmNTParams p{A, B, C, ld, M, N, K, lower};
-  static const bool four = [] {  // HG_GEMM_STAGES=3: the 3-stage, 4 CTAs / SM variant
-    const char* e = getenv("HG_GEMM_STAGES");
-    return !(e && e[0] == '3');
-  }();
-  if (four)
-    d.set((const void*)k_gemm_nt<CfgG4, 3>, dim3(M / CfgG::BM, N / CfgG::BN), dim3(CfgG::THREADS),
-          (unsigned)GemmSmem<CfgG4, M_MAJOR, M_MAJOR>::BYTES, p);
-  else
-    d.set((const void*)k_gemm_nt<CfgG, 4>, dim3(M / CfgG::BM, N / CfgG::BN), dim3(CfgG::THREADS), gemm_smem(), p);
+  GemmNTParams p{A, B, C, ld, M, N, K, lower, push};
+  d.set((const void*)k_gemm_nt<CfgG4, 3>, dim3(M / CfgG4::BM, N / CfgG4::BN), dim3(CfgG4::THREADS),
+        (unsigned)GemmSmem<CfgG4, M_MAJOR, M_MAJOR>::BYTES, p);
   out.push_back(d);
 }
 
@@ -922,7 +934,7 @@ bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc
   switch (kind) {
     case K_POTRF: {
       LaunchDesc d;
-      PotrfParams pp{o.t[0], nb, o.status};
+      PotrfParams pp{o.t[0], nb, o.status, o.push};
       d.set((const void*)k_potrf_cluster, dim3(kPotrfCl), dim3(CfgG::THREADS),
             unsigned(kPotrfDynDoubles * sizeof(double)), pp);
       out.push_back(d);
@@ -935,17 +947,17 @@ bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc
         return false;
       }
       LaunchDesc d;
-      TrsmInvParams tp{o.t[0], o.t[1], o.scratch, nb};
+      TrsmInvParams tp{o.t[0], o.t[1], o.scratch, nb, o.push};
       const void* f = P == 8 ? (const void*)k_trsm_inv<8> : (P == 4 ? (const void*)k_trsm_inv<4> : (const void*)k_trsm_inv<2>);
       d.set(f, dim3(nJ * P), dim3(CfgG::THREADS), trsm_smem(), tp);
       out.push_back(d);
       return true;
     }
     case K_SYRK:
-      push_gemm(out, o.t[0], o.t[0], o.t[1], nb, nb, nb, nb, 1);
+      push_gemm(out, o.t[0], o.t[0], o.t[1], nb, nb, nb, nb, 1, o.push);
       return true;
     case K_GEMM:
-      push_gemm(out, o.t[0], o.t[1], o.t[2], nb, nb, nb, nb, 0);
+      push_gemm(out, o.t[0], o.t[1], o.t[2], nb, nb, nb, nb, 0, o.push);
       return true;
     default:
       set_error("kind %d is not a Cholesky kind", kind);

@@ -295,8 +295,6 @@ struct LuApplyParams {
   double* bot;          // GETRF-type: == top; TSTRF-type: the other tile
   int nb, ib, p0, p1, col0, mode;
   int swap_only;        // 1: row interchanges + inv(L_uu)*top only (the bot update is a separate wide GEMM)
-  long long batch_stride;  // profiling only (HG_PROF_BATCH): CTA b works on operand set b / strips,
-                           // the sets batch_stride doubles apart; 0 = one set
 };
 
 template <int SB>
@@ -421,22 +419,8 @@ __global__ void __launch_bounds__(CfgN::THREADS) k_gemm_nn(GemmNNParams p) {
 static unsigned nn_smem() { return (unsigned)GemmSmem<CfgN, M_MAJOR, K_MAJOR>::BYTES; }
 
 // ---------------------------------------------------------------------------
-// k_lu_apply_cl -- applies panels [p0, p1) of an LU factor to a column strip
-// with the bottom rows split over a 4-CTA cluster (CTA q owns tile rows
-// [q*nb/4, (q+1)*nb/4) of bot and 8 of the strip's 32 columns for the row
-// interchanges), so one GESSM / SSSSM spreads over (N/32) x 4 SMs.  Per panel:
-//   0. every CTA turns the panel's ipiv into a list of row moves (dst <- src,
-//      values as they were before the panel; see lu_moves below);
-//   1. CTA q performs the moves of its 8 columns; cluster barrier;
-//   2. every CTA loads the 128 top rows, forms its 32-row slice of
-//      top' = inv(L_uu) top; cluster barrier;
-//   3. every CTA gathers top' over DSMEM, CTA q stores its slice, and
-//      bot[rows_q] -= L_a[rows_q] top' on the DMMA engine; cluster barrier.
-constexpr int kLcCl = 4;
-constexpr int kLcBN = 32;
-constexpr int kLcLd = kLuMaxSb + 4;             // smem [col][row] buffers
+constexpr int kLcLd = kLuMaxSb + 4;             // smem [col][row] buffers of the strip kernel
 constexpr int kLcMaxMoves = 2 * kLuMaxSb;
-using CfgLC = GemmCfg<128, kLcBN, 16, 32, 16, 3>;  // 8 warps
 
 // Row moves of one panel (values before the panel -> positions after it).
 // GETRF (rows of one tile): step j swaps rows j and p_j >= j.  Positions < j
@@ -524,100 +508,6 @@ __device__ int lu_moves(const int* steps, int ii, int sb, bool ts, int* sp, int*
   }
   __syncthreads();
   return *cnt;
-}
-
-__global__ void __cluster_dims__(kLcCl, 1, 1) __launch_bounds__(CfgLC::THREADS) k_lu_apply_cl(LuApplyParams p) {
-  extern __shared__ double sm[];
-  cg::cluster_group cl = cg::this_cluster();
-  const int q = (int)cl.block_rank();
-  constexpr int RING = GemmSmem<CfgLC, M_MAJOR, K_MAJOR>::DOUBLES;
-  constexpr int WBUF = kLcBN * kLcLd;
-  double* ring = sm;
-  double* Wp = sm + RING;            // [2][WBUF] top' slices by panel parity
-  double* Ts = Wp + 2 * WBUF;        // top rows after the moves, then gathered top'
-  double* mvv = Ts + WBUF;           // [kLcMaxMoves][8] moved values
-  int* mv_dst = reinterpret_cast<int*>(mvv + kLcMaxMoves * 8);
-  int* mv_src = mv_dst + kLcMaxMoves;
-  int* sp = mv_src + kLcMaxMoves;    // [3 * sb]
-  __shared__ int n_moves;
-  const int nb = p.nb, ib = p.ib, sb = ib;
-  const int n0 = p.col0 + (blockIdx.x / kLcCl) * kLcBN;
-  const int rows = nb / kLcCl;
-  const int r_begin = q * rows, r_end = r_begin + rows;
-  const bool ts = p.mode == LU_TSTRF;
-  const int tid = threadIdx.x;
-  const int* ipiv = reinterpret_cast<const int*>(p.side + size_t(ib) * nb);
-  double* top = p.top;
-  double* bot = ts ? p.bot : p.top;
-  for (int P = p.p0; P < p.p1; ++P) {
-    const int ii = P * ib;
-    double* wp = Wp + (P & 1) * WBUF;
-    // ---- 0/1. row moves of my 8 columns ------------------------------------------
-    const int nm = lu_moves(ipiv + ii, ii, sb, ts, sp, mv_dst, mv_src, &n_moves);
-    const int c8 = n0 + q * 8;
-    auto at = [&](int code, int c) -> double* {
-      return code >= 0 ? bot + size_t(c) * nb + code : top + size_t(c) * nb + ii + (-1 - code);
-    };
-    for (int e = tid; e < nm * 8; e += CfgLC::THREADS) {
-      const int m = e >> 3, c = c8 + (e & 7);
-      mvv[e] = __ldcg(at(mv_src[m], c));
-    }
-    __syncthreads();
-    for (int e = tid; e < nm * 8; e += CfgLC::THREADS) {
-      const int m = e >> 3, c = c8 + (e & 7);
-      *at(mv_dst[m], c) = mvv[e];
-    }
-    cl.sync();
-    // ---- 2. top rows -> smem, my slice of top' = inv(L_uu) top ---------------------
-    for (int e = tid; e < sb * kLcBN; e += CfgLC::THREADS) {
-      const int c = e / sb, r = e % sb;
-      Ts[c * kLcLd + r] = __ldcg(top + size_t(n0 + c) * nb + ii + r);
-    }
-    __syncthreads();
-    {
-      const double* inv = p.side + size_t(ii) * ib;  // inv(r, k) at inv[k*ib + r], unit lower
-      constexpr int SL = kLuMaxSb / kLcCl;
-      const int s0 = q * SL;
-      for (int e = tid; e < SL * kLcBN; e += CfgLC::THREADS) {
-        const int c = e / SL, r = s0 + e % SL;
-        const double* tc = Ts + c * kLcLd;
-        double a0 = tc[r], a1 = 0.0;
-        int k = 0;
-        for (; k + 1 < r; k += 2) {
-          a0 = fma(__ldg(inv + size_t(k) * ib + r), tc[k], a0);
-          a1 = fma(__ldg(inv + size_t(k + 1) * ib + r), tc[k + 1], a1);
-        }
-        if (k < r) a0 = fma(__ldg(inv + size_t(k) * ib + r), tc[k], a0);
-        wp[c * kLcLd + r] = a0 + a1;
-      }
-    }
-    cl.sync();
-    // ---- 3. gather top', store my slice, bot[rows] -= L_a top' ----------------------
-    {
-      constexpr int SL = kLuMaxSb / kLcCl;
-      for (int c2 = 0; c2 < kLcCl; ++c2) {
-        const double* src = cl.map_shared_rank(wp, c2);
-        for (int e = tid; e < SL * kLcBN; e += CfgLC::THREADS) {
-          const int c = e / SL, r = c2 * SL + e % SL;
-          const double v = src[c * kLcLd + r];
-          Ts[c * kLcLd + r] = v;
-          if (c2 == q) top[size_t(n0 + c) * nb + ii + r] = v;
-        }
-      }
-    }
-    __syncthreads();
-    if (!p.swap_only) {
-      const int m_lo = ts ? r_begin : max(r_begin, ii + sb);
-      for (int m0 = m_lo; m0 < r_end; m0 += 128) {
-        double acc[CfgLC::FM][CfgLC::FN][2];
-        zero_acc<CfgLC>(acc);
-        TileLoader<CfgLC, M_MAJOR, 128> la{p.L + size_t(ii) * nb, nb, m0};
-        gemm_mainloop_bsmem<CfgLC>(acc, ring, la, Ts, kLcLd, 0, sb);
-        sub_store<CfgLC>(acc, bot, nb, m0, n0);
-      }
-    }
-    cl.sync();
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1014,15 +904,7 @@ k_lu_apply_strip(LuApplyParams p) {
   int* sp = mv_src + kLcMaxMoves;         // [3 * sb]
   __shared__ int n_moves;
   const int nb = p.nb, ib = p.ib, sb = ib;
-  const int strips = (nb - p.col0) / BN;
-  const size_t set_off = p.batch_stride ? size_t(blockIdx.x / strips) * size_t(p.batch_stride) : 0;
-  if (set_off) {
-    p.L += set_off;
-    p.side += set_off;
-    p.top += set_off;
-    p.bot += set_off;
-  }
-  const int n0 = p.col0 + (blockIdx.x % strips) * BN;
+  const int n0 = p.col0 + blockIdx.x * BN;
   const bool ts = p.mode == LU_TSTRF;
   const int tid = threadIdx.x;
   const int* ipiv = reinterpret_cast<const int*>(p.side + size_t(ib) * nb);
@@ -1082,12 +964,8 @@ k_lu_apply_strip(LuApplyParams p) {
   }
 }
 
-using CfgLS16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
-using CfgLS32 = GemmCfg<128, 32, 16, 32, 16, 3>;  // 8 warps (32x16 warp tiles): 2 CTAs / SM -> 16 warps
-using CfgLS64 = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps
-using CfgLS32w4 = GemmCfg<128, 32, 16, 32, 32, 3>;  // 4 warps, 32x32 warp tiles (HG_LU_APPLY=33)
-using CfgLU256 = GemmCfg<256, 32, 8, 32, 32, 4>;    // update stream: 8 warps of 32x32, 4 x 8-wide k-slabs
-using CfgLS4w = GemmCfg<128, 32, 8, 32, 32, 4>;     // 4 warps of 32x32, 8-wide k-slabs: 3 CTAs / SM
+using CfgLS16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps, 16-column strips: the in-panel trailing columns
+using CfgLS4w = GemmCfg<128, 32, 8, 32, 32, 4>;     // 4 warps of 32x32, 8-wide k-slabs: 3 CTAs / SM (GESSM / SSSSM)
 
 template <class G, class GU = G>
 static unsigned lu_apply_strip_smem() {
@@ -1096,12 +974,6 @@ static unsigned lu_apply_strip_smem() {
   if (ru > ring) ring = ru;
   size_t d = ring + G::BN * kLcLd;
   if (d < size_t(kLcMaxMoves) * G::BN) d = size_t(kLcMaxMoves) * G::BN;
-  size_t ints = 2 * kLcMaxMoves + 3 * kLuMaxSb;
-  return unsigned(d * sizeof(double) + ints * sizeof(int));
-}
-
-static unsigned lu_apply_cl_smem() {
-  size_t d = GemmSmem<CfgLC, M_MAJOR, K_MAJOR>::DOUBLES + 3 * kLcBN * kLcLd + kLcMaxMoves * 8;
   size_t ints = 2 * kLcMaxMoves + 3 * kLuMaxSb;
   return unsigned(d * sizeof(double) + ints * sizeof(int));
 }
@@ -1120,21 +992,12 @@ static unsigned panel_smem(int nb, int sb) {
   return unsigned((bufs > inv ? bufs : inv) * sizeof(double));
 }
 
-// HG_LU_PANEL=reg selects the register-resident full-width panel kernel (experiments)
-static bool use_sp_panel(int nb, int ib) {
-  static const bool reg = [] {
-    const char* e = getenv("HG_LU_PANEL");
-    return e && e[0] == 'r';
-  }();
-  return !reg && ib == kSpSB && (nb == 1024 || nb == 512);
-}
+// ib = 128: the sub-panel kernel; ib = 64: the register-resident full-width panel kernel
+static bool use_sp_panel(int nb, int ib) { return ib == kSpSB && (nb == 1024 || nb == 512); }
 
 static const void* panel_kernel(int nb, int ib) {
   if (use_sp_panel(nb, ib)) return nb == 1024 ? (const void*)k_lu_panel_sp<128> : (const void*)k_lu_panel_sp<64>;
-  if (nb == 1024 && ib == 128) return (const void*)k_lu_panel<128, 128>;
-  if (nb == 512 && ib == 128) return (const void*)k_lu_panel<64, 128>;
   if (nb == 1024 && ib == 64) return (const void*)k_lu_panel<128, 64>;
-  if (nb == 512 && ib == 128) return (const void*)k_lu_panel<64, 128>;
   if (nb == 512 && ib == 64) return (const void*)k_lu_panel<64, 64>;
   return nullptr;
 }
@@ -1157,123 +1020,53 @@ static unsigned apply_smem(int nb) {
   } while (0)
 
 bool init_lu_attributes() {
-  HG_ATTR((k_lu_panel<128, 128>), cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
   HG_ATTR((k_lu_panel<128, 64>), cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
-  HG_ATTR((k_lu_panel<64, 128>), cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
   HG_ATTR((k_lu_panel<64, 64>), cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem(1024, 128));
-  HG_ATTR(k_lu_apply<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem<128>(1024));
   HG_ATTR(k_lu_apply<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_smem<64>(1024));
   HG_ATTR(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, nn_smem());
-  HG_ATTR(k_lu_apply_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_cl_smem());
-  HG_ATTR(k_lu_apply_strip<CfgLS16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS16>());
-  HG_ATTR(k_lu_apply_strip<CfgLS32>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS32>());
-  HG_ATTR(k_lu_apply_strip<CfgLS64>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS64>());
-  HG_ATTR(k_lu_apply_strip<CfgLS32w4>, cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS32w4>());
   HG_ATTR((k_lu_apply_strip<CfgLS16, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS16>());
-  HG_ATTR((k_lu_apply_strip<CfgLS32, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS32>());
   HG_ATTR((k_lu_apply_strip<CfgLS4w, true>), cudaFuncAttributeMaxDynamicSharedMemorySize,
           lu_apply_strip_smem<CfgLS4w>());
-  HG_ATTR((k_lu_apply_strip<CfgLS32, true, CfgLU256>), cudaFuncAttributeMaxDynamicSharedMemorySize,
-          (lu_apply_strip_smem<CfgLS32, CfgLU256>()));
   HG_ATTR(k_lu_panel_sp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpSmem<128>::BYTES);
   HG_ATTR(k_lu_panel_sp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(512));
   return true;
 }
 
-static void push_apply(std::vector<LaunchDesc>& out, int ib, const LuApplyParams& ap) {
+static void push_apply(std::vector<LaunchDesc>& out, const LuApplyParams& ap) {  // ib = 64
   LaunchDesc d;
   const int ncols = ap.nb - ap.col0;
-  if (ib == 128)
-    d.set((const void*)k_lu_apply<128>, dim3(ncols / ApplyCfg<128>::BN), dim3(ApplyCfg<128>::G::THREADS),
-          apply_smem<128>(ap.nb), ap);
-  else
-    d.set((const void*)k_lu_apply<64>, dim3(ncols / ApplyCfg<64>::BN), dim3(ApplyCfg<64>::G::THREADS),
-          apply_smem<64>(ap.nb), ap);
+  d.set((const void*)k_lu_apply<64>, dim3(ncols / ApplyCfg<64>::BN), dim3(ApplyCfg<64>::G::THREADS),
+        apply_smem<64>(ap.nb), ap);
   out.push_back(d);
 }
 
-// One panel applied to columns [col0, nb): narrow swap + inv(L_uu) kernel,
-// then the wide bot -= L_a * top GEMM.
-static bool use_cluster_apply(int nb, int ib) { return ib == kLuMaxSb && nb % (kLcCl * 128) == 0; }
+// ib = 128: every panel application is the strip kernel (one CTA per 16 / 32-column strip,
+// L2-reduction update).  ib = 64: narrow swap + inv(L_uu) kernel, then a wide GEMM.
+static bool use_strip_apply(int nb, int ib) { return ib == kLuMaxSb && nb % 512 == 0; }
 
-// HG_LU_APPLY env: "cl" = 4-CTA cluster kernel, 16 / 32 = strip width (experiments)
-static int lu_apply_env() {
-  static const int v = [] {
-    const char* e = getenv("HG_LU_APPLY");
-    if (!e) return 0;
-    if (e[0] == 'c') return -1;
-    return atoi(e);
-  }();
-  return v;
-}
-
-// HG_RED=0: trailing updates as load / subtract / store instead of L2 reductions (A/B)
-static bool use_red() {
-  static const bool v = [] {
-    const char* e = getenv("HG_RED");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
-// 32-column strip variants (A/B)
-static int strip_mode() {  // HG_WIDE: 0 = 4-warp strips (default), 1 = 256-row 8-warp update, 2 = 8 warps 32x16
-  static const int v = [] {
-    const char* e = getenv("HG_WIDE");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-// Panels [P0, P1) applied to columns [col0, nb): strip kernel (default) or cluster kernel.
-static void push_apply_cl(std::vector<LaunchDesc>& out, const double* L, const double* side, double* top,
-                          double* bot, int nb, int ib, int P0, int P1, int col0, int mode, int bn_default = 32) {
-  LuApplyParams ap{L, side, top, bot, nb, ib, P0, P1, col0, mode, 0, 0};
+// Panels [P0, P1) applied to columns [col0, nb) by the strip kernel.
+static void push_apply_strip(std::vector<LaunchDesc>& out, const double* L, const double* side, double* top,
+                             double* bot, int nb, int ib, int P0, int P1, int col0, int mode, int bn) {
+  LuApplyParams ap{L, side, top, bot, nb, ib, P0, P1, col0, mode, 0};
   LaunchDesc d;
-  // profiling hook: HG_PROF_BATCH=B HG_PROF_STRIDE=S launch B operand sets S doubles apart in
-  // one grid (a saturated single launch that ncu can capture); never set in production
-  static const int prof_batch = [] {
-    const char* e = getenv("HG_PROF_BATCH");
-    return e ? atoi(e) : 0;
-  }();
-  if (prof_batch > 1 && mode == LU_TSTRF && col0 == 0) {
-    const char* e = getenv("HG_PROF_STRIDE");
-    ap.batch_stride = e ? atoll(e) : 0;
-  }
-  const int batch = ap.batch_stride ? prof_batch : 1;
-  const int bn = lu_apply_env() ? lu_apply_env() : bn_default;
   const int ncols = nb - col0;
-  if (bn < 0)
-    d.set((const void*)k_lu_apply_cl, dim3(ncols / kLcBN * kLcCl), dim3(CfgLC::THREADS), lu_apply_cl_smem(), ap);
-  else if (bn == 16)
-    d.set(use_red() ? (const void*)k_lu_apply_strip<CfgLS16, true> : (const void*)k_lu_apply_strip<CfgLS16>,
-          dim3(ncols / 16), dim3(CfgLS16::THREADS), lu_apply_strip_smem<CfgLS16>(), ap);
-  else if (bn == 33)
-    d.set((const void*)k_lu_apply_strip<CfgLS32w4>, dim3(ncols / 32), dim3(CfgLS32w4::THREADS),
-          lu_apply_strip_smem<CfgLS32w4>(), ap);
-  else if (bn == 64 && ncols % 64 == 0)
-    d.set((const void*)k_lu_apply_strip<CfgLS64>, dim3(ncols / 64), dim3(CfgLS64::THREADS),
-          lu_apply_strip_smem<CfgLS64>(), ap);
-  else if (bn == 34 || (bn == 32 && use_red() && strip_mode() == 0))
-    d.set((const void*)k_lu_apply_strip<CfgLS4w, true>, dim3(ncols / 32 * batch), dim3(CfgLS4w::THREADS),
-          lu_apply_strip_smem<CfgLS4w>(), ap);
-  else if (bn == 32 && use_red() && strip_mode() == 1)
-    d.set((const void*)k_lu_apply_strip<CfgLS32, true, CfgLU256>, dim3(ncols / 32), dim3(CfgLS32::THREADS),
-          lu_apply_strip_smem<CfgLS32, CfgLU256>(), ap);
+  if (bn == 16)
+    d.set((const void*)k_lu_apply_strip<CfgLS16, true>, dim3(ncols / 16), dim3(CfgLS16::THREADS),
+          lu_apply_strip_smem<CfgLS16>(), ap);
   else
-    d.set(use_red() ? (const void*)k_lu_apply_strip<CfgLS32, true> : (const void*)k_lu_apply_strip<CfgLS32>,
-          dim3(ncols / 32), dim3(CfgLS32::THREADS), lu_apply_strip_smem<CfgLS32>(), ap);
+    d.set((const void*)k_lu_apply_strip<CfgLS4w, true>, dim3(ncols / 32), dim3(CfgLS4w::THREADS),
+          lu_apply_strip_smem<CfgLS4w>(), ap);
   out.push_back(d);
 }
 
 static void push_panel_apply(std::vector<LaunchDesc>& out, int ib, const double* L, const double* side,
                              double* top, double* bot, int nb, int P, int col0, int mode) {
-  if (use_cluster_apply(nb, ib)) {
-    push_apply_cl(out, L, side, top, bot, nb, ib, P, P + 1, col0, mode, 16);
+  if (use_strip_apply(nb, ib)) {
+    push_apply_strip(out, L, side, top, bot, nb, ib, P, P + 1, col0, mode, 16);
     return;
   }
   LuApplyParams ap{L, side, top, bot, nb, ib, P, P + 1, col0, mode, 1};
-  push_apply(out, ib, ap);
+  push_apply(out, ap);
   const int ii = P * ib;
   const bool ts = mode == LU_TSTRF;
   const int m0 = ts ? 0 : ii + ib;
@@ -1315,15 +1108,15 @@ bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
       return true;
     }
     case K_GESSM:
-      if (use_cluster_apply(nb, ib)) {
-        push_apply_cl(out, o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF, o.urgent ? 16 : 32);
+      if (use_strip_apply(nb, ib)) {
+        push_apply_strip(out, o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF, 32);
         return true;
       }
       for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[1], nb, P, 0, LU_GETRF);
       return true;
     case K_SSSSM:
-      if (use_cluster_apply(nb, ib)) {
-        push_apply_cl(out, o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF, o.urgent ? 16 : 32);
+      if (use_strip_apply(nb, ib)) {
+        push_apply_strip(out, o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF, 32);
         return true;
       }
       for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[2], nb, P, 0, LU_TSTRF);

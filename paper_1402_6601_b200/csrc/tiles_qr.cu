@@ -298,9 +298,7 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
 }
 
 // ---------------------------------------------------------------------------
-using CfgQ64 = GemmCfg<128, 64, 16, 32, 32, 3>;  // 8 warps; requires sb == 128
-using CfgQ32 = GemmCfg<128, 32, 16, 32, 16, 3>;  // 8 warps (32x16 warp tiles)
-using CfgQ16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps
+using CfgQ16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps: the in-panel trailing columns
 using CfgQ4w = GemmCfg<128, 32, 8, 32, 32, 4>;    // 4 warps of 32x32: C -= V W stream (3 CTAs / SM)
 using CfgQ4w1 = GemmCfg<128, 32, 8, 32, 32, 3, true>;  //   and its W = V^T C / T^T W phases (swizzled K_MAJOR ring)
 constexpr int kWld = kQrMaxSb + 4;  // W stored [n][k]
@@ -420,482 +418,6 @@ __global__ void __launch_bounds__(CfgQ::THREADS, CfgQ::THREADS == 128 ? 3 : 2) k
 }
 
 // ---------------------------------------------------------------------------
-// k_qr_apply_cl -- the same block-reflector application with the tile ROWS
-// split over a 4-CTA cluster, so one TSMQR / UNMQR (or a GEQRT / TSQRT
-// trailing update) spreads over (N/32) x 4 SMs instead of N/64:
-//   CTA q owns rows [q*nb/4, (q+1)*nb/4) of C (UNMQR) / bot (TSMQR) and a
-//   32-column strip.  Per panel:
-//     1. W_q = V[rows_q]^T C[rows_q]            (DMMA, split-K partial)
-//     2. cluster barrier; CTA q reduces W rows [32q, 32q+32) over DSMEM
-//        (+ top rows for TSMQR)
-//     3. cluster barrier; every CTA gathers W rows 0..32q+31, forms its
-//        slice of W' = T^T W (T upper triangular)
-//     4. cluster barrier; every CTA gathers W' (TSMQR: CTA q also applies
-//        top -= W' to its slice of the top rows)
-//     5. C[rows_q] -= V[rows_q] W'             (DMMA, W' resident in smem)
-// Partial / slice buffers alternate by panel parity, so a fast CTA writing
-// panel P+1's partials never overwrites a slice a slow CTA still gathers.
-constexpr int kQcCl = 4;
-constexpr int kQcBN = 32;
-using CfgQC = GemmCfg<128, kQcBN, 16, 32, 16, 3>;  // 8 warps, 32x16 warp tiles
-constexpr int kQcSlice = kQrMaxSb / kQcCl;          // W rows reduced per CTA
-
-__global__ void __cluster_dims__(kQcCl, 1, 1) __launch_bounds__(CfgQC::THREADS) k_qr_apply_cl(QrApplyParams p) {
-  extern __shared__ double sm[];
-  cg::cluster_group cl = cg::this_cluster();
-  const int q = (int)cl.block_rank();
-  constexpr int RING = GemmSmem<CfgQC, K_MAJOR, K_MAJOR>::DOUBLES;
-  constexpr int WBUF = kQcBN * kWld;
-  double* ring = sm;
-  double* Wp = sm + RING;             // [2][WBUF]: partials, then W' slices (by panel parity)
-  double* Ws = Wp + 2 * WBUF;         // reduced W slice + gathered W, then gathered W'
-  const int nb = p.nb, ib = p.ib;
-  const int n0 = p.col0 + (blockIdx.x / kQcCl) * kQcBN;
-  const int rows = nb / kQcCl;
-  const int r_begin = q * rows, r_end = r_begin + rows;
-  const bool ts = p.mode == QR_TSQRT;
-  const int tid = threadIdx.x;
-  for (int P = p.p0; P < p.p1; ++P) {
-    const int ii = P * ib;
-    const double* Vp = p.V + size_t(ii) * nb;
-    double* C = ts ? p.bot : p.top;
-    double* wp = Wp + (P & 1) * WBUF;
-    // rows of C this CTA touches in this panel (UNMQR: only tile rows >= ii)
-    const int k0 = ts ? r_begin : max(r_begin, ii);
-    // ---- 1. partial W_q --------------------------------------------------------
-    {
-      double acc[CfgQC::FM][CfgQC::FN][2];
-      zero_acc<CfgQC>(acc);
-      if (k0 < r_end) {
-        VLoader<CfgQC, K_MAJOR, 128> la{Vp, nb, 0, ii, ts ? 0 : 1};
-        TileLoader<CfgQC, K_MAJOR, kQcBN> lb{C, nb, n0};
-        gemm_mainloop<CfgQC>(acc, ring, la, lb, k0, r_end);
-      }
-      for_each_acc<CfgQC>(acc, [&](int r, int c, double v) { wp[c * kWld + r] = v; });
-    }
-    cl.sync();
-    // ---- 2. reduce my slice of W ------------------------------------------------
-    const int s0 = q * kQcSlice;
-    {
-      const double* parts[kQcCl];
-#pragma unroll
-      for (int c2 = 0; c2 < kQcCl; ++c2) parts[c2] = cl.map_shared_rank(wp, c2);
-      for (int e = tid; e < kQcSlice * kQcBN; e += CfgQC::THREADS) {
-        const int c = e / kQcSlice, r = s0 + e % kQcSlice;
-        double v[kQcCl];
-#pragma unroll
-        for (int c2 = 0; c2 < kQcCl; ++c2) v[c2] = parts[c2][c * kWld + r];
-        double t = ts ? p.top[size_t(n0 + c) * nb + ii + r] : 0.0;
-#pragma unroll
-        for (int c2 = 0; c2 < kQcCl; ++c2) t += v[c2];
-        Ws[c * kWld + r] = t;
-      }
-    }
-    cl.sync();
-    // ---- 3. gather W rows [0, s0) and form my slice of W' = T^T W -------------------
-    for (int c2 = 0; c2 < q; ++c2) {
-      const double* src = cl.map_shared_rank(Ws, c2);
-      for (int e = tid; e < kQcSlice * kQcBN; e += CfgQC::THREADS) {
-        const int c = e / kQcSlice, r = c2 * kQcSlice + e % kQcSlice;
-        Ws[c * kWld + r] = src[c * kWld + r];
-      }
-    }
-    __syncthreads();
-    {
-      const double* T = p.side + size_t(ii) * ib;  // T(k, r) at T[r*ib + k], upper triangular
-      for (int e = tid; e < kQcSlice * kQcBN; e += CfgQC::THREADS) {
-        const int c = e / kQcSlice, r = s0 + e % kQcSlice;
-        const double* tc = T + size_t(r) * ib;
-        const double* wc = Ws + c * kWld;
-        double a0 = 0.0, a1 = 0.0;
-        int k = 0;
-        for (; k + 1 <= r; k += 2) {
-          a0 = fma(__ldg(tc + k), wc[k], a0);
-          a1 = fma(__ldg(tc + k + 1), wc[k + 1], a1);
-        }
-        if (k <= r) a0 = fma(__ldg(tc + k), wc[k], a0);
-        wp[c * kWld + r] = a0 + a1;
-      }
-    }
-    cl.sync();
-    // ---- 4. gather W' ----------------------------------------------------------------
-    for (int c2 = 0; c2 < kQcCl; ++c2) {
-      const double* src = cl.map_shared_rank(wp, c2);
-      for (int e = tid; e < kQcSlice * kQcBN; e += CfgQC::THREADS) {
-        const int c = e / kQcSlice, r = c2 * kQcSlice + e % kQcSlice;
-        Ws[c * kWld + r] = src[c * kWld + r];
-      }
-    }
-    __syncthreads();
-    if (ts)
-      for (int e = tid; e < kQcSlice * kQcBN; e += CfgQC::THREADS) {
-        const int c = e / kQcSlice, r = s0 + e % kQcSlice;
-        p.top[size_t(n0 + c) * nb + ii + r] -= Ws[c * kWld + r];
-      }
-    // ---- 5. C[rows] -= V[rows] W' ------------------------------------------------------
-    for (int m0 = k0; m0 < r_end; m0 += 128) {
-      double acc[CfgQC::FM][CfgQC::FN][2];
-      zero_acc<CfgQC>(acc);
-      VLoader<CfgQC, M_MAJOR, 128> la{Vp, nb, m0, ii, ts ? 0 : 1};
-      gemm_mainloop_bsmem<CfgQC>(acc, ring, la, Ws, kWld, 0, 128);
-      sub_store<CfgQC>(acc, C, nb, m0, n0);
-    }
-    __syncthreads();
-  }
-  cl.sync();  // no CTA leaves while a peer may still read its W' slice
-}
-
-static unsigned qr_apply_cl_smem() {
-  return unsigned((GemmSmem<CfgQC, K_MAJOR, K_MAJOR>::DOUBLES + 3 * kQcBN * kWld) * sizeof(double));
-}
-
-// ---------------------------------------------------------------------------
-// k_qr_panel_sp -- the Householder panel (GEQRT / TSQRT semantics of
-// k_qr_panel) blocked into W = 16-column sub-panels held in registers, one
-// tile row per thread, 8-CTA cluster (CTA q owns rows [q*R, (q+1)*R)):
-//   per column: ONE cluster barrier for the column norm (+ alpha), dlarfg in
-//   every thread, ONE cluster barrier for w = v^T A over the <= 15 remaining
-//   sub-panel columns, rank-1 update in registers;
-//   per sub-panel: the block reflector I - V T V^T of its 16 columns is
-//   applied to the panel's right-hand columns with DMMA partials
-//   (W = V^T A_right, G = V^T V), a reduce-scatter / all-gather of W over
-//   DSMEM, T_sub from G and tau, W' = T_sub^T W, A_right -= V W';
-//   per panel: T = the compact-WY T factor of all 128 reflectors, from
-//   striu(V^T V) (DMMA partial Gram matrices reduced over DSMEM) and tau.
-// The per-column critical path touches 16 registers per row instead of the
-// whole 128-column panel (k_qr_panel: ~4.7 us per column).
-constexpr int kQsW = 16;
-constexpr int kQsThreads = 128;
-constexpr int kQsSB = 128;
-
-template <int R>
-struct QsSmem {
-  static constexpr int LDP = R + 4;                    // panel [col][row] (+4: conflict-free DMMA frags)
-  static constexpr int PS = kQsSB * LDP;
-  static constexpr int WB = kQsW * (kQsSB + kQsW);     // partial W (| G) [v][col], 16 x (16 + 112)
-  static constexpr int MISC = 4 + kQsW * kQsW + 2 * kQsW + kQsW * kQsW + kQsSB;  // slots, Rblk, wpart, Ts, taus
-  static constexpr int DOUBLES = PS + 3 * WB + MISC;
-  static constexpr int TFY = kQsSB * (kQsSB + 1) + kQsSB + 7 * 256;  // qr_t_from_y scratch
-  static constexpr size_t BYTES = size_t(DOUBLES > TFY ? DOUBLES : TFY) * 8;
-};
-
-template <int R>
-__global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQsThreads) k_qr_panel_sp(QrPanelParams p) {
-  constexpr int W = kQsW, SB = kQsSB;
-  using S = QsSmem<R>;
-  constexpr int LDP = S::LDP;
-  constexpr int WLD = SB + W;  // row stride of the W buffers
-  extern __shared__ double sm[];
-  cg::cluster_group cl = cg::this_cluster();
-  const int q = (int)cl.block_rank();
-  const int nb = p.nb, ii = p.ii, ib = p.ib;
-  const int row0 = q * R;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool ts = p.mode == QR_TSQRT;
-  const bool mine = tid < R;
-  const int gr = row0 + tid;
-  const bool live = mine && (ts || gr >= ii);
-  double* Ps = sm;
-  double* Wp = Ps + S::PS;             // partial [v][col]: W (cols 0..nR) | G (cols nR..nR+16)
-  double* Wr = Wp + S::WB;             // reduced rows of this CTA / gathered W
-  double* Wg = Wr + S::WB;             // gathered W' (after T_sub^T)
-  double* slot = Wg + S::WB;           // [2][2] norm^2, alpha
-  double* Rblk = slot + 4;             // [W][W] TSQRT: R rows of the sub-panel
-  double* wpart = Rblk + W * W;        // [2][W]
-  double* Ts = wpart + 2 * W;          // [W][W] T_sub, Ts[r*W + c]
-  double* taus = Ts + W * W;           // [SB]
-  __shared__ double red_n[kQsThreads / 32], red_a[kQsThreads / 32];
-  __shared__ double red_w[kQsThreads / 32][kQsW];
-  double* T = p.side + size_t(ii) * ib;  // this panel's T block (ib x sb, ld ib)
-  double* A = p.A;
-
-  for (int e = tid; e < SB * R; e += kQsThreads) {
-    const int c = e / R, r = e % R;
-    Ps[c * LDP + r] = (ts || row0 + r >= ii) ? A[size_t(ii + c) * nb + row0 + r] : 0.0;
-  }
-  __syncthreads();
-
-  // V(row r of this CTA, panel column c): GEQRT masks the unit lower structure
-  auto Vat = [&](int r, int c) -> double {
-    const int g2 = row0 + r, jd = ii + c;
-    if (ts) return Ps[c * LDP + r];
-    return g2 > jd ? Ps[c * LDP + r] : (g2 == jd ? 1.0 : 0.0);
-  };
-
-  for (int c0 = 0; c0 < SB; c0 += W) {
-    if (ts)
-      for (int e = tid; e < W * W; e += kQsThreads) {
-        const int u = e / W, v = e % W;
-        Rblk[e] = v >= u ? __ldcg(p.R + size_t(ii + c0 + v) * nb + ii + c0 + u) : 0.0;
-      }
-    double a[W];
-#pragma unroll
-    for (int v = 0; v < W; ++v) a[v] = mine ? Ps[(c0 + v) * LDP + tid] : 0.0;
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < W; ++u) {
-      const int jj = c0 + u, j = ii + jj, par = jj & 1;
-      const bool below = live && (ts || gr > j);
-      const bool isdiag = live && !ts && gr == j;
-      // ---- 1: norm^2 below the diagonal and alpha -> cluster --------------------------
-      {
-        double n2 = below ? a[u] * a[u] : 0.0;
-        double al = isdiag ? a[u] : 0.0;
-        n2 = warp_sum(n2);
-        al = warp_sum(al);
-        if (lane == 0) {
-          red_n[warp] = n2;
-          red_a[warp] = al;
-        }
-        __syncthreads();
-        if (tid == 0) {
-          double t1 = 0.0, t2 = 0.0;
-#pragma unroll
-          for (int w2 = 0; w2 < kQsThreads / 32; ++w2) {
-            t1 += red_n[w2];
-            t2 += red_a[w2];
-          }
-          slot[par * 2] = t1;
-          slot[par * 2 + 1] = t2;
-        }
-      }
-      cl.sync();
-      double xn2, alpha;
-      {
-        double v1 = 0.0, v2 = 0.0;
-        if (lane < kQrCl) {
-          const double* sl = cl.map_shared_rank(slot, lane) + par * 2;
-          v1 = sl[0];
-          v2 = sl[1];
-        }
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-          v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-          v2 += __shfl_xor_sync(0xffffffffu, v2, o);
-        }
-        xn2 = __shfl_sync(0xffffffffu, v1, 0);
-        alpha = ts ? Rblk[u * W + u] : __shfl_sync(0xffffffffu, v2, 0);
-      }
-      // ---- 2: dlarfg (every thread) ------------------------------------------------------
-      double tau = 0.0, beta = alpha, scal = 1.0;
-      if (xn2 != 0.0) {
-        const double xnorm = sqrt(xn2);
-        beta = -copysign(hypot(alpha, xnorm), alpha);
-        tau = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
-      }
-      double v = 0.0;
-      if (below) {
-        v = a[u] * scal;
-        a[u] = v;
-      } else if (isdiag) {
-        v = 1.0;
-        a[u] = beta;
-      }
-      if (tid == 0) taus[jj] = tau;
-      // ---- 3: w = v^T A(:, u+1..W) -> cluster -------------------------------------------
-#pragma unroll
-      for (int v2 = u + 1; v2 < W; ++v2) {
-        const double pw = warp_sum(v * a[v2]);
-        if (lane == 0) red_w[warp][v2] = pw;
-      }
-      __syncthreads();
-      if (tid < W && tid > u) {
-        double t1 = 0.0;
-#pragma unroll
-        for (int w2 = 0; w2 < kQsThreads / 32; ++w2) t1 += red_w[w2][tid];
-        wpart[par * W + tid] = t1;
-      }
-      cl.sync();
-      double wl = 0.0;  // lane l (< W) of every warp: w[l] summed over the cluster
-      if (lane < W && lane > u) {
-        double pt[kQrCl];
-#pragma unroll
-        for (int c2 = 0; c2 < kQrCl; ++c2) pt[c2] = cl.map_shared_rank(wpart, c2)[par * W + lane];
-#pragma unroll
-        for (int c2 = 0; c2 < kQrCl; ++c2) wl += pt[c2];
-        if (ts) wl += Rblk[u * W + lane];  // the unit of v_j sits in R row j
-      }
-      // ---- 4: rank-1 update of the sub-panel; TSQRT: R row j ----------------------------
-#pragma unroll
-      for (int v2 = u + 1; v2 < W; ++v2) {
-        const double w = __shfl_sync(0xffffffffu, wl, v2);
-        a[v2] = fma(-tau * v, w, a[v2]);
-        if (ts && q == 0 && tid == v2) p.R[size_t(ii + c0 + v2) * nb + j] = Rblk[u * W + v2] - tau * w;
-      }
-      if (ts && q == 0 && tid == 0) p.R[size_t(ii + jj) * nb + j] = beta;
-    }
-    if (mine) {
-#pragma unroll
-      for (int v = 0; v < W; ++v) Ps[(c0 + v) * LDP + tid] = a[v];
-    }
-    __syncthreads();
-    // ---- sub-panel block reflector on the right-hand columns ------------------------------------
-    const int cR = c0 + W, nR = SB - cR;
-    if (nR == 0) break;
-    // partial W = V^T A_right (16 x nR) and G = V^T V (16 x 16), DMMA over my R rows
-    {
-      const int ntile = 2 * ((nR + W) / 8);
-      for (int w = warp; w < ntile; w += kQsThreads / 32) {
-        const int ti = w & 1, tj = w >> 1;            // row tile (reflector), column tile
-        const int colt = tj * 8;                       // 0..nR+16 (last two tiles: G)
-        double d0 = 0.0, d1 = 0.0;
-        const int g = lane >> 2, t = lane & 3;
-        for (int k0 = 0; k0 < R; k0 += 4) {
-          const double av = Vat(k0 + t, c0 + ti * 8 + g);
-          const int cc = colt + g;
-          const double bv = cc < nR ? Ps[(cR + cc) * LDP + k0 + t] : Vat(k0 + t, c0 + cc - nR);
-          dmma_8x8x4(d0, d1, av, bv);
-        }
-        Wp[(ti * 8 + g) * WLD + colt + 2 * t] = d0;
-        Wp[(ti * 8 + g) * WLD + colt + 2 * t + 1] = d1;
-      }
-    }
-    cl.sync();
-    // reduce-scatter: CTA q owns rows v in {2q, 2q+1}; TSQRT adds the R rows (top) to W
-    {
-      const int ncol = nR + W;
-      for (int e = tid; e < 2 * ncol; e += kQsThreads) {
-        const int v = 2 * q + e / ncol, c = e % ncol;
-        double pt[kQrCl];
-#pragma unroll
-        for (int c2 = 0; c2 < kQrCl; ++c2) pt[c2] = cl.map_shared_rank(Wp, c2)[v * WLD + c];
-        double t1 = 0.0;
-#pragma unroll
-        for (int c2 = 0; c2 < kQrCl; ++c2) t1 += pt[c2];
-        if (ts && c < nR) t1 += __ldcg(p.R + size_t(ii + cR + c) * nb + ii + c0 + v);
-        Wr[v * WLD + c] = t1;
-      }
-    }
-    cl.sync();
-    // all-gather the 16 rows
-    {
-      const int ncol = nR + W;
-      for (int e = tid; e < W * ncol; e += kQsThreads) {
-        const int v = e / ncol, c = e % ncol;
-        if (v / 2 != q) Wr[v * WLD + c] = cl.map_shared_rank(Wr, v / 2)[v * WLD + c];
-      }
-    }
-    __syncthreads();
-    // T_sub from G (Wr[.][nR + .]) and tau: T(k,k) = tau_k, T(0:k, k) = -tau_k T(0:k, 0:k) G(0:k, k)
-    if (warp == 0) {
-      const int i = lane;
-      double trow[W];
-#pragma unroll
-      for (int k = 0; k < W; ++k) trow[k] = 0.0;
-#pragma unroll
-      for (int k = 0; k < W; ++k) {
-        const double tk = taus[c0 + k];
-        double acc = 0.0;
-#pragma unroll
-        for (int m = 0; m < k; ++m)
-          if (m >= i) acc = fma(trow[m], Wr[m * WLD + nR + k], acc);
-        if (i < k) trow[k] = -tk * acc;
-        else if (i == k) trow[k] = tk;
-      }
-      if (i < W) {
-#pragma unroll
-        for (int k = 0; k < W; ++k) Ts[i * W + k] = trow[k];
-      }
-    }
-    __syncthreads();
-    // W' = T_sub^T W: W'(i, c) = sum_{m <= i} T(m, i) W(m, c)
-    for (int c = tid; c < nR; c += kQsThreads) {
-      double wc[W];
-#pragma unroll
-      for (int m = 0; m < W; ++m) wc[m] = Wr[m * WLD + c];
-#pragma unroll
-      for (int i = 0; i < W; ++i) {
-        double acc = 0.0;
-#pragma unroll
-        for (int m = 0; m <= i; ++m) acc = fma(Ts[m * W + i], wc[m], acc);
-        Wg[i * WLD + c] = acc;
-        if (ts && q == 0) {  // R rows of the sub-panel: top -= W'
-          double* rp = p.R + size_t(ii + cR + c) * nb + ii + c0 + i;
-          *rp = __ldcg(rp) - acc;
-        }
-      }
-    }
-    __syncthreads();
-    // A_right -= V W'  (my row: V(r, v) from the registers of this sub-panel)
-    if (live) {
-      double vr[W];
-#pragma unroll
-      for (int v = 0; v < W; ++v) vr[v] = ts ? a[v] : (gr > ii + c0 + v ? a[v] : (gr == ii + c0 + v ? 1.0 : 0.0));
-      for (int c = 0; c < nR; ++c) {
-        double t1 = Ps[(cR + c) * LDP + tid];
-#pragma unroll
-        for (int v = 0; v < W; ++v) t1 = fma(-vr[v], Wg[v * WLD + c], t1);
-        Ps[(cR + c) * LDP + tid] = t1;
-      }
-    }
-    cl.sync();  // Wp / Wr of this sub-panel are no longer read by any CTA
-  }
-  // ---- write the panel back ------------------------------------------------------------------
-  for (int e = tid; e < SB * R; e += kQsThreads) {
-    const int c = e / R, r = e % R;
-    if (ts || row0 + r >= ii) A[size_t(ii + c) * nb + row0 + r] = Ps[c * LDP + r];
-  }
-  // ---- y = striu(V^T V) of the whole panel into the T area (tau on the diagonal) ---------------
-  // partial Gram over my rows by DMMA: the 136 upper 8x8 tiles (ti <= tj) of the 16 x 16 tile
-  // grid, 34 per warp held in registers until every warp has read the panel, then stored over
-  // the panel buffer as Gp[tile][64] for CTA 0 to reduce over DSMEM
-  {
-    constexpr int NT = 136 / (kQsThreads / 32);
-    double g0[NT], g1[NT];
-    const int g = lane >> 2, t = lane & 3;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const int w = warp + n * (kQsThreads / 32);
-      int ti = 0, rem = w;
-      while (rem >= 16 - ti) {
-        rem -= 16 - ti;
-        ++ti;
-      }
-      const int tj = ti + rem;
-      double d0 = 0.0, d1 = 0.0;
-      for (int k0 = 0; k0 < R; k0 += 4) dmma_8x8x4(d0, d1, Vat(k0 + t, ti * 8 + g), Vat(k0 + t, tj * 8 + g));
-      g0[n] = d0;
-      g1[n] = d1;
-    }
-    __syncthreads();
-    double* Gp = Ps;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const int w = warp + n * (kQsThreads / 32);
-      Gp[w * 64 + g * 8 + 2 * t] = g0[n];
-      Gp[w * 64 + g * 8 + 2 * t + 1] = g1[n];
-    }
-  }
-  __syncthreads();
-  cl.sync();
-  if (q == 0) {
-    // T column jc: rows k < jc = sum over CTAs of G(k, jc); k == jc: tau; below: 0
-    for (int e = tid; e < SB * SB; e += kQsThreads) {
-      const int jc = e / SB, k = e % SB;
-      double v = 0.0;
-      if (k < jc) {
-        const int ti = k / 8, tj = jc / 8;
-        const int w = ti * 16 - ti * (ti - 1) / 2 + (tj - ti);
-        const int off = w * 64 + (k % 8) * 8 + (jc % 8);
-        double pt[kQrCl];
-#pragma unroll
-        for (int c2 = 0; c2 < kQrCl; ++c2) pt[c2] = cl.map_shared_rank(Ps, c2)[off];
-#pragma unroll
-        for (int c2 = 0; c2 < kQrCl; ++c2) v += pt[c2];
-      } else if (k == jc) {
-        v = taus[jc];
-      }
-      T[size_t(jc) * ib + k] = v;
-    }
-  }
-  __threadfence();
-  cl.sync();  // every CTA's partial Gram has been read
-  if (q != 0) return;
-  qr_t_from_y(T, ib, SB, sm);
-}
-
-// ---------------------------------------------------------------------------
 static unsigned qr_panel_smem(int nb, int sb) {
   const int R = nb / kQrCl;
   size_t d = size_t(sb) * (R + 1);
@@ -921,16 +443,9 @@ static unsigned qr_apply_smem() {
 
 bool init_qr_attributes() {
   HG_QATTR(k_qr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_panel_smem(1024, 128));
-  HG_QATTR(k_qr_panel_sp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QsSmem<128>::BYTES);
-  HG_QATTR(k_qr_panel_sp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QsSmem<64>::BYTES);
-  HG_QATTR(k_qr_apply<CfgQ64>, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ64>());
-  HG_QATTR(k_qr_apply<CfgQ32>, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ32>());
-  HG_QATTR(k_qr_apply<CfgQ16>, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ16>());
-  HG_QATTR((k_qr_apply<CfgQ32, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ32>());
   HG_QATTR((k_qr_apply<CfgQ4w, true, CfgQ4w1>), cudaFuncAttributeMaxDynamicSharedMemorySize,
            (qr_apply_smem<CfgQ4w, CfgQ4w1>()));
   HG_QATTR((k_qr_apply<CfgQ16, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_smem<CfgQ16>());
-  HG_QATTR(k_qr_apply_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, qr_apply_cl_smem());
   return true;
 }
 
@@ -956,35 +471,17 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
   const size_t tile = size_t(nb) * nb;
   const int np = nb / ib;
   auto side = [&](int i) { return o.t[i] + tile; };
-  // strip width: HG_QR_APPLY env ("cl" = 4-CTA cluster kernel, or 16 / 32 / 64)
-  static const int mode_env = [] {
-    const char* e = getenv("HG_QR_APPLY");
-    if (!e) return 0;
-    if (e[0] == 'c') return -1;
-    return atoi(e);
-  }();
-  // HG_RED=0: C -= V W as load / subtract / store instead of L2 reductions (A/B)
-  static const bool red = [] {
-    const char* e = getenv("HG_RED");
-    return !(e && e[0] == '0');
-  }();
-  auto push_apply = [&](const QrApplyParams& ap, int bn_default) {
+  // block-reflector applications: 16-column strips inside a panel task (few trailing columns),
+  // 32-column strips of 4 warps at 3 CTAs / SM for UNMQR / TSMQR; C -= V W as L2 reductions
+  auto push_apply = [&](const QrApplyParams& ap, int bn) {
     LaunchDesc d;
-    const int bn = mode_env ? mode_env : bn_default;
     const int ncols = nb - ap.col0;
-    if (bn < 0 && nb % (kQcCl * 128) == 0)
-      d.set((const void*)k_qr_apply_cl, dim3(ncols / kQcBN * kQcCl), dim3(CfgQC::THREADS), qr_apply_cl_smem(), ap);
-    else if (bn == 16)
-      d.set(red ? (const void*)k_qr_apply<CfgQ16, true> : (const void*)k_qr_apply<CfgQ16>, dim3(ncols / 16),
-            dim3(CfgQ16::THREADS), qr_apply_smem<CfgQ16>(), ap);
-    else if (bn == 34 || (bn == 32 && red && mode_env == 0))
+    if (bn == 16)
+      d.set((const void*)k_qr_apply<CfgQ16, true>, dim3(ncols / 16), dim3(CfgQ16::THREADS),
+            qr_apply_smem<CfgQ16>(), ap);
+    else
       d.set((const void*)k_qr_apply<CfgQ4w, true, CfgQ4w1>, dim3(ncols / 32), dim3(CfgQ4w::THREADS),
             qr_apply_smem<CfgQ4w, CfgQ4w1>(), ap);
-    else if (bn == 32)
-      d.set(red ? (const void*)k_qr_apply<CfgQ32, true> : (const void*)k_qr_apply<CfgQ32>, dim3(ncols / 32),
-            dim3(CfgQ32::THREADS), qr_apply_smem<CfgQ32>(), ap);
-    else
-      d.set((const void*)k_qr_apply<CfgQ64>, dim3(ncols / 64), dim3(CfgQ64::THREADS), qr_apply_smem<CfgQ64>(), ap);
     out.push_back(d);
   };
   switch (kind) {
@@ -996,19 +493,7 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
         QrPanelParams pp{A, ts ? o.t[0] : nullptr, ts ? side(1) : side(0), nb, ib, P * ib, ib,
                          ts ? QR_TSQRT : QR_GEQRT};
         LaunchDesc d;
-        // HG_QR_PANEL=sp selects the sub-panel kernel: correct (tests pass) but measured
-        // slower (745 vs 600 us per panel: ~1070 instructions per column per warp in the
-        // shuffle reductions, I-cache misses of the unrolled column loop), so the
-        // column-at-a-time kernel stays the default
-        static const bool sp_panel = [] {
-          const char* e = getenv("HG_QR_PANEL");
-          return e && e[0] == 's';
-        }();
-        if (sp_panel && ib == kQsSB && (nb == 1024 || nb == 512))
-          d.set(nb == 1024 ? (const void*)k_qr_panel_sp<128> : (const void*)k_qr_panel_sp<64>, dim3(kQrCl),
-                dim3(kQsThreads), unsigned(nb == 1024 ? QsSmem<128>::BYTES : QsSmem<64>::BYTES), pp);
-        else
-          d.set((const void*)k_qr_panel, dim3(kQrCl), dim3(kQrThreads), qr_panel_smem(nb, ib), pp);
+        d.set((const void*)k_qr_panel, dim3(kQrCl), dim3(kQrThreads), qr_panel_smem(nb, ib), pp);
         out.push_back(d);
         if (P + 1 < np)
           push_apply(QrApplyParams{A, ts ? side(1) : side(0), ts ? o.t[0] : A, ts ? A : nullptr, nb, ib, P, P + 1,
@@ -1024,10 +509,10 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
       return true;
     }
     case K_UNMQR:
-      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], nullptr, nb, ib, 0, np, 0, QR_GEQRT}, o.urgent ? 16 : 32);
+      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], nullptr, nb, ib, 0, np, 0, QR_GEQRT}, 32);
       return true;
     case K_TSMQR:
-      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, QR_TSQRT}, o.urgent ? 16 : 32);
+      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, QR_TSQRT}, 32);
       return true;
     default:
       set_error("kind %d is not a QR kind", kind);

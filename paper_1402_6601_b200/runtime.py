@@ -78,6 +78,7 @@ class ExecStats:
     bytes_side: int
     n_kernel_nodes: int
     n_copy_nodes: int
+    n_push_jobs: int = 0
 
 
 @dataclass(eq=True)
@@ -128,7 +129,7 @@ class Executor:
 
     def __init__(self, graph, platform, plan, host_in: np.ndarray, host_out: np.ndarray | None = None,
                  devices=None, device_input: bool = False, host_side_out: np.ndarray | None = None,
-                 rank_node: int = 0, priority_levels: int = 6, trace: bool = False):
+                 rank_node: int = 0, priority_levels: int = 6, trace: bool = False, push: bool = True):
         L = _native.lib()
         lay = graph.layout
         if lay is None:
@@ -166,6 +167,9 @@ class Executor:
         self.graph = graph
         self.platform = platform
         self.trace = bool(trace)
+        # producer-push fusion: peer jobs of POTRF/TRSM/SYRK/GEMM outputs are
+        # stored into the consumer GPU's slot by the producing kernel instead of a copy node
+        self.push = bool(push) and os.environ.get("HG_PUSH", "1") != "0"
         self.devices = devices
         # node priorities from the plan's own predicted durations (end - start):
         # changes only which ready kernel gets SMs first, never the plan
@@ -202,7 +206,7 @@ class Executor:
         st = _native.ExecStats()
         _native.check(_native.lib().hg_exec_run(self._h, C.byref(st)), "hg_exec_run")
         return ExecStats(st.elapsed_ms, st.bytes_h2d, st.bytes_d2d, st.bytes_d2h, st.bytes_side,
-                         st.n_kernel_nodes, st.n_copy_nodes)
+                         st.n_kernel_nodes, st.n_copy_nodes, st.n_push_jobs)
 
     def launch(self, stream: int = 0):
         """Enqueue one run on ``stream`` (a cudaStream_t as int; 0 = the legacy default stream)."""
@@ -216,7 +220,7 @@ class Executor:
         st = _native.ExecStats()
         _native.check(_native.lib().hg_exec_info(self._h, C.byref(st)), "hg_exec_info")
         return ExecStats(st.elapsed_ms, st.bytes_h2d, st.bytes_d2d, st.bytes_d2h, st.bytes_side,
-                         st.n_kernel_nodes, st.n_copy_nodes)
+                         st.n_kernel_nodes, st.n_copy_nodes, st.n_push_jobs)
 
     def stamps(self) -> np.ndarray:
         """Trace mode: device ns [start, end] per task (rows 0..n-1) then per copy job."""
@@ -306,7 +310,7 @@ class DistributedExecutor(Executor):
 
     def __init__(self, graph, platform, plan, host_in, host_out=None, rank=None, world=None, device=None,
                  device_input=False, host_side_out=None, group=None, priority_levels: int = 6,
-                 wait_timeout: float = 60.0):
+                 wait_timeout: float = 60.0, push: bool = True):
         import torch.distributed as dist
 
         rank = dist.get_rank(group) if rank is None else rank
@@ -317,7 +321,7 @@ class DistributedExecutor(Executor):
         dev = int(device if device is not None else rank % max(1, _native.lib().hg_device_count()))
         super().__init__(graph, platform, plan, host_in, host_out, devices=[dev] * platform.k,
                          device_input=device_input, host_side_out=host_side_out, rank_node=rank + 1,
-                         priority_levels=priority_levels)
+                         priority_levels=priority_levels, push=push)
         L = _native.lib()
         self._group = group
         # every cross-rank spin is bounded: a dead peer raises DeadlockError instead of hanging
@@ -388,7 +392,7 @@ def plan_digest(plan) -> str:
     return h.hexdigest()
 
 
-def partition_counts(graph, platform, plan, rank_node: int, with_flags: bool = False):
+def partition_counts(graph, platform, plan, rank_node: int, with_flags: bool = False, push: bool = False):
     """CPU dry run of a rank's share: (local tasks, local copy jobs, remote waits, signals)
     [, waited flag ids, signalled flag ids]."""
     fl = graph.flat()
@@ -403,6 +407,7 @@ def partition_counts(graph, platform, plan, rank_node: int, with_flags: bool = F
     holder.pred = np.asarray([q for p in preds for q in p], np.int32)
     holder.final_writer = np.full(len(graph.data), -1, np.int32)
     holder.p2p = bool(platform.p2p) or platform.k == 1
+    holder.push = push
     lay = graph.layout
     ep = ExecPlan_from(plan, n, len(graph.data), platform.k, lay, holder, fl)
     out = np.zeros(4, np.int32)
@@ -428,7 +433,7 @@ def ExecPlan_from(plan, n, n_blocks, k, lay, ex, fl):
         P(plan.job_block, C.c_int32), P(plan.job_src, C.c_int32), P(plan.job_dst, C.c_int32),
         P(plan.job_version, C.c_int32), P(plan.job_src_job, C.c_int32), P(plan.job_requester, C.c_int32),
         P(fl["sizes"], C.c_int64), P(ex.final_writer, C.c_int32), P(fl["acc_mode"], C.c_int8),
-        P(plan.job_stage_job, C.c_int32), int(bool(ex.p2p)))
+        P(plan.job_stage_job, C.c_int32), int(bool(ex.p2p)), int(bool(getattr(ex, "push", False))))
 
 
 class pinned_host:

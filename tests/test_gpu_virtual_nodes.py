@@ -117,3 +117,34 @@ def test_host_staged_route_p2p_false(fam):
     if fam == "cholesky":
         ref, got = np.tril(ref), np.tril(got)
     assert np.abs(got - ref).max() / np.abs(ref).max() < (1e-12 if fam == "cholesky" else 1e-9)
+
+
+@pytest.mark.parametrize("k,sched", [(4, "dada"), (8, "heft")])
+def test_producer_push_matches_copy_nodes(k, sched):
+    """Producer-push fusion: the peer jobs of POTRF / TRSM / SYRK / GEMM
+    outputs are stored into the consumer nodes' slots by the producing kernels' epilogues.
+    The factor must be bit-identical to the copy-node execution of the same plan, every such
+    job delivered by push (no copy node), and the bytes per (version, destination) the plan's."""
+    import bench
+
+    n, nb = 8192, 512
+    g, plat, plan = _plan("cholesky", n, nb, k, sched)
+    img = bench.make_input(g, n, nb, 4, torch)
+    outs, stats = {}, {}
+    for push in (False, True):
+        out = torch.empty_like(img, pin_memory=True)
+        ex = runtime.Executor(g, plat, plan, img.numpy(), out.numpy(), devices=[0] * k, push=push)
+        stats[push] = ex.run()
+        ex.close()
+        outs[push] = out.numpy().copy()
+    d2d_jobs = int(((plan.job_src >= 1) & (plan.job_dst >= 1)).sum())
+    assert d2d_jobs > 0
+    assert stats[True].n_push_jobs == d2d_jobs and stats[False].n_push_jobs == 0
+    assert stats[True].n_copy_nodes == stats[False].n_copy_nodes - d2d_jobs
+    for st in stats.values():
+        assert st.bytes_d2d == plan.bytes_d2d and st.bytes_h2d == plan.bytes_h2d
+    L_push = np.tril(runtime.from_tile_major(outs[True], g))
+    L_copy = np.tril(runtime.from_tile_major(outs[False], g))
+    assert np.array_equal(L_push, L_copy)
+    res, _ = bench.factor_check(g, img.numpy(), outs[True], nb)
+    assert res < 1e-14

@@ -23,14 +23,17 @@ def _plan(fam, nt, b, k, sched):
     return g, plat, H.make_plan(g, plat, s, H.PerfModel(H.default_timing_table(b, 128)))
 
 
+@pytest.mark.parametrize("push", [False, True])
 @pytest.mark.parametrize("fam,nt,k,sched", [("cholesky", 16, 2, "dada"), ("cholesky", 16, 8, "heft"),
                                             ("lu", 8, 4, "dada"), ("qr", 8, 8, "dada")])
-def test_partition_covers_plan_and_flags_match(fam, nt, k, sched):
+def test_partition_covers_plan_and_flags_match(fam, nt, k, sched, push):
+    """push=True: producer-push jobs make their consumers wait on the producer task's flag
+    instead of a copy job's; the waited and signalled sets must still match exactly."""
     g, plat, plan = _plan(fam, nt, 512, k, sched)
     tasks = jobs = 0
     waited, signalled = set(), set()
     for r in range(1, k + 1):
-        lt, lj, nw, ns, w, sgl = runtime.partition_counts(g, plat, plan, r, with_flags=True)
+        lt, lj, nw, ns, w, sgl = runtime.partition_counts(g, plat, plan, r, with_flags=True, push=push)
         tasks += lt
         jobs += lj
         waited |= set(w.tolist())
