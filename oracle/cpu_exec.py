@@ -150,6 +150,8 @@ class DagPool:
         self.workers = max(1, workers or host_threads())
         self.procs, self.conns = [], []
         self._preds_left = graph.in_degrees()
+        self._running = {}
+        self.stall_seconds = float(os.environ.get("HG_ORACLE_STALL_S", "600"))
 
     def __enter__(self):
         ctx = mp.get_context("fork")
@@ -194,13 +196,21 @@ class DagPool:
         while done < need:
             while ready and idle:
                 w = idle.pop()
-                self.conns[w].send(heapq.heappop(ready))
+                tid = heapq.heappop(ready)
+                self.conns[w].send(tid)
                 busy[self.conns[w]] = w
+                self._running[self.conns[w]] = tid
             if not busy:
                 raise RuntimeError(f"oracle DAG executor: window [{lo}, {hi}) has no runnable task "
                                    "(earlier tasks not done?)")
-            for c in mp_wait(list(busy)):
+            got = mp_wait(list(busy), timeout=self.stall_seconds)
+            if not got:
+                running = sorted(msg for msg in self._running.values())
+                raise RuntimeError(f"oracle DAG executor: no task finished in {self.stall_seconds:.0f} s "
+                                   f"(running: {running[:16]})")
+            for c in got:
                 msg = c.recv()
+                self._running.pop(c, None)
                 if isinstance(msg, tuple):
                     raise RuntimeError(f"oracle task {msg[1]} failed:\n{msg[2]}")
                 done += 1

@@ -12,12 +12,17 @@ B200_LIKE = {"GEMM": 30, "SSSSM": 28, "TSMQR": 26, "SYRK": 25, "UNMQR": 22, "TRS
              "TSQRT": 5, "TSTRF": 4, "POTRF": 3, "GEQRT": 3, "GETRF_INC": 2}
 
 
-def fixtures():
+def fixtures(name="plans.json.gz"):
     global _CACHE
     if _CACHE is None:
-        with gzip.open(os.path.join(HERE, "golden", "plans.json.gz"), "rt", encoding="utf-8") as fh:
-            _CACHE = json.load(fh)["fixtures"]
-    return _CACHE
+        _CACHE = {}
+    if name not in _CACHE:
+        path = os.path.join(HERE, "golden", name)
+        if not os.path.exists(path):
+            return []
+        with gzip.open(path, "rt", encoding="utf-8") as fh:
+            _CACHE[name] = json.load(fh)["fixtures"]
+    return _CACHE[name]
 
 
 def digest(values):
@@ -31,6 +36,8 @@ def digest(values):
 def table_for(fx, H):
     """The timing table a fixture was generated with, built through package ``H``."""
     b, ib = fx["b"], fx["ib"]
+    if fx["table"].startswith("file:"):  # a committed measured table (tests/golden/make_bench_golden.py)
+        return H.load_timing_table(os.path.join(os.path.dirname(HERE), fx["table"][5:]))
     if fx["table"] == "default":
         return H.default_timing_table(b, ib)
     t = {}

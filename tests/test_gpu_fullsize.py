@@ -6,7 +6,8 @@ the bench runs (bench platform, capacity-calibrated B200 cost model,
 DADA(0.5)+CP), against the CPU oracle on the SAME matrix:
 
 * the oracle factor comes from oracle/cpu_exec.py (forked workers on every host
-  core running oracle/tiles*.py; GIL-free, so N=32768 finishes in about a minute);
+  core running oracle/tiles*.py; GIL-free), run as a fresh process
+  (oracle/factor_job.py) so no worker is forked from this CUDA-holding process;
 * every tile of the factor is compared element-wise (max-norm, relative to the
   largest oracle entry); LU pivots must be identical in every tile; the side
   areas (LU: L_uu^-1 per panel against inv(I + dL) of the oracle; QR: T) too;
@@ -22,12 +23,16 @@ differences: two backward-stable evaluations in different summation orders
 differ by ~ c(n) eps kappa of the trailing Schur complements, which stays
 below 1e-12 for these matrices.
 
-Host memory: ~40 GB per family (A, oracle arena, input image, output image).
+Host memory: ~40 GB per family (A, oracle factor, input image, output image).
 ``HG_PARITY_OUT=<file>`` appends the measured numbers as JSON lines.
 """
 import json
 import math
 import os
+import shutil
+import subprocess
+import sys
+import tempfile
 
 import numpy as np
 import pytest
@@ -61,14 +66,42 @@ def _matrix(fam):
     return O.spd_matrix(N, SEED[fam]) if fam == "cholesky" else O.general_matrix(N, SEED[fam])
 
 
+class _OracleFactor:
+    """The oracle's factor read back from oracle/factor_job.py's files (tiles / side like TileArena)."""
+
+    def __init__(self, g, out):
+        lay = g.layout
+        self.ids = sorted(lay.tiles)
+        tl = np.fromfile(os.path.join(out, "tiles.f64"), np.float64)
+        self.tiles = {d: tl[i * NB * NB:(i + 1) * NB * NB].reshape(NB, NB, order="F") for i, d in enumerate(self.ids)}
+        self.aux, self.piv = {}, {}
+        if lay.family != "cholesky":
+            sd = np.fromfile(os.path.join(out, "side.f64"), np.float64)
+            per = IB * NB + NB
+            for i, d in enumerate(self.ids):
+                self.aux[d] = sd[i * per:i * per + IB * NB].reshape(IB, NB, order="F")
+                self.piv[d] = sd[i * per + IB * NB:(i + 1) * per]
+        self.family = lay.family
+
+    side = X.TileArena.side
+
+
 def _oracle(fam):
-    """(A, graph, oracle arena) for ``fam``; one family cached at a time (host memory)."""
+    """(A, graph, oracle factor, seconds) for ``fam``; one family cached at a time (host memory).
+    The oracle runs in a fresh process (oracle/factor_job.py), not forked from this one."""
     if fam not in _cache:
         _cache.clear()
-        A = _matrix(fam)
         g = H.gen_family(fam, N // NB, NB, IB)
-        arena, secs = X.factor(g, A)
-        _cache[fam] = (A, g, arena, secs)
+        tmp = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+        try:
+            res = subprocess.run([sys.executable, "-m", "oracle.factor_job", fam, str(N), str(NB), str(IB),
+                                  str(SEED[fam]), tmp], cwd=ROOT, capture_output=True, text=True, timeout=1800)
+            assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
+            secs = json.loads(res.stdout.strip().splitlines()[-1])["seconds"]
+            fac = _OracleFactor(g, tmp)
+        finally:
+            shutil.rmtree(tmp, ignore_errors=True)
+        _cache[fam] = (_matrix(fam), g, fac, secs)
     return _cache[fam]
 
 
@@ -204,6 +237,10 @@ def test_full_size_elementwise(fam, k):
         row["side_rel"] = side_diff / t_scale
         v = rng.standard_normal(N)
         r_gpu, r_cpu = _qr_residual(A, tiles, gside, lay, v), _qr_residual(A, ref, ora_side, lay, v)
+        # Q^T from the GPU's reflectors and T factors is orthogonal: ||Q^T w|| = ||w||
+        w = rng.standard_normal((N, 1))
+        row["orth_rel"] = abs(float(np.linalg.norm(LQ.qr_apply_qt(tiles, gside, lay, w))) / float(np.linalg.norm(w)) - 1.0)
+        assert row["orth_rel"] < 1e-12, row
     row.update(res_gpu=r_gpu, res_oracle=r_cpu)
     _record(row)
     print(json.dumps(row))

@@ -58,7 +58,7 @@ def _rank_main(rank, world, port, family, q, n=2048, b=512):
 
 
 @pytest.mark.parametrize("family,n,b", [("cholesky", 2048, 512), ("lu", 2048, 512),
-                                        ("cholesky", 8192, 512), ("lu", 4096, 256)])
+                                        ("cholesky", 8192, 512), ("lu", 8192, 512)])
 def test_two_ranks_one_gpu(family, n, b):
     import torch.multiprocessing as mp
 

@@ -86,6 +86,13 @@ for kind in kinds:
         torch.cuda.synchronize()
         reps = 5
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # HG_PROF_RANGE=1: the saturated region is a cudaProfilerStart/Stop range, so
+        # `ncu --replay-mode range --profile-from-start off` measures the concurrent kernel mix
+        # as one workload (DMMA pipe use, L2 / DRAM traffic) instead of serialised launches
+        prof = os.environ.get("HG_PROF_RANGE") == "1" and conc == max(
+            int(c) for c in os.environ.get("HG_CONC", "1,8").split(","))
+        if prof:
+            torch.cuda.profiler.start()
         e0.record()
         for s in streams:
             s.wait_event(e0)
@@ -96,6 +103,8 @@ for kind in kinds:
             torch.cuda.current_stream().wait_event(ev)
         e1.record()
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.profiler.stop()
         ms = e0.elapsed_time(e1)
         tput = conc * reps * flops / (ms * 1e-3) / 1e12
         if conc == 1:
