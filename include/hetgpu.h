@@ -266,6 +266,33 @@ int hg_tile_run_scratch(int32_t kind, int32_t device, void* stream, double* cons
                         int32_t nb, int32_t ib, int32_t* status_dev, int32_t* scratch_dev);
 int hg_task_scratch_ints(int32_t kind, int32_t nb, int32_t ib);
 
+/* ------------------------------------------------------------------------
+ * Device plumbing of the online executor (paper_1402_6601_b200/online.py):
+ * it plays sim.py's event loop (sim.py:140-203) on the host and issues one
+ * hg_tile_run_scratch per dispatched task; slots, streams, events and the
+ * H2D / peer copies of non-resident inputs (sim.py:237-267's transfers,
+ * executed) go through these calls.  Handles are opaque (cudaStream_t,
+ * cudaEvent_t, device pointers).  Replaces nothing in the reference (its
+ * execution is simulated); the call sites it serves are sim.py:353-371
+ * (_start_exec / _task_end: run a kernel, record its measured duration).
+ * ---------------------------------------------------------------------- */
+int hg_dev_alloc(int32_t device, size_t bytes, void** out);
+int hg_dev_free(int32_t device, void* ptr);
+int hg_dev_memset(int32_t device, void* ptr, int32_t value, size_t bytes, void* stream);
+/* peer access device -> peer (HG_EPEER when the pair has no peer route) */
+int hg_dev_enable_peer(int32_t device, int32_t peer);
+int hg_dev_sync(int32_t device);
+int hg_stream_create(int32_t device, void** out);      /* non-blocking stream */
+int hg_stream_destroy(int32_t device, void* stream);
+int hg_stream_wait_event(void* stream, void* event);
+int hg_event_create(int32_t device, int32_t timing, void** out);
+int hg_event_destroy(int32_t device, void* event);
+int hg_event_record(void* event, void* stream);
+int hg_event_query(void* event);                       /* 1 done, 0 pending, <0 error */
+int hg_event_elapsed_ms(void* start, void* end, float* ms);
+/* dst <- src on `stream` (cudaMemcpyDefault: H2D, D2H, D2D or peer over NVLink) */
+int hg_copy_async(int32_t device, void* dst, const void* src, size_t bytes, void* stream);
+
 /* FP64 roofline denominator: DMMA (mma.sync m8n8k4 f64) throughput of a
  * register-only kernel filling every SM, in TFLOP/s (MEASURED_PEAKS.json has
  * no FP64 entry).  Runs ~10 ms on `device`. */

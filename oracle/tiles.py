@@ -114,6 +114,15 @@ def general_matrix(n: int, seed: int) -> np.ndarray:
     return rng.uniform(-0.5, 0.5, size=(n, n))
 
 
+def ulp_perturbed(A: np.ndarray, seed: int) -> np.ndarray:
+    """A with every entry moved by one rounding unit, A * (1 +- 2^-52), random signs
+    (numpy.random.default_rng(seed)): the roundoff-level input perturbation whose
+    effect on the oracle's own factor measures how far two correct evaluations in
+    different summation orders may drift apart (tests/test_gpu_fullsize.py)."""
+    rng = np.random.default_rng(seed)
+    return A * (1.0 + np.ldexp(1.0, -52) * rng.choice(np.array([-1.0, 1.0]), size=A.shape))
+
+
 def cholesky_residual(A: np.ndarray, L: np.ndarray) -> float:
     """||A - L L^T||_F / ||A||_F."""
     L = np.tril(L)

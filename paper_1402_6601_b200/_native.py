@@ -88,7 +88,10 @@ EXPORTS = ("hg_last_error", "hg_abi_version", "hg_device_count", "hg_plan_build"
            "hg_tile_run", "hg_exec_launch", "hg_exec_wait", "hg_exec_info", "hg_fp64_peak",
            "hg_exec_ipc_handle", "hg_exec_ipc_open", "hg_exec_build", "hg_exec_partition",
            "hg_tile_run_scratch", "hg_task_scratch_ints", "hg_exec_set_wait_timeout", "hg_exec_ipc_close", "hg_exec_read_stamps",
-           "hg_matrix_register", "hg_matrix_unregister")
+           "hg_matrix_register", "hg_matrix_unregister",
+           "hg_dev_alloc", "hg_dev_free", "hg_dev_memset", "hg_dev_enable_peer", "hg_dev_sync",
+           "hg_stream_create", "hg_stream_destroy", "hg_stream_wait_event", "hg_event_create",
+           "hg_event_destroy", "hg_event_record", "hg_event_query", "hg_event_elapsed_ms", "hg_copy_async")
 
 _lib = None
 
@@ -136,6 +139,22 @@ def lib():
     L.hg_exec_read_stamps.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
     L.hg_matrix_register.argtypes = [C.c_void_p, C.c_size_t]
     L.hg_matrix_unregister.argtypes = [C.c_void_p]
+    # device plumbing of the online executor (streams, events, slots, async copies)
+    vp, i32, sz = C.c_void_p, C.c_int32, C.c_size_t
+    L.hg_dev_alloc.argtypes = [i32, sz, C.POINTER(vp)]
+    L.hg_dev_free.argtypes = [i32, vp]
+    L.hg_dev_memset.argtypes = [i32, vp, i32, sz, vp]
+    L.hg_dev_enable_peer.argtypes = [i32, i32]
+    L.hg_dev_sync.argtypes = [i32]
+    L.hg_stream_create.argtypes = [i32, C.POINTER(vp)]
+    L.hg_stream_destroy.argtypes = [i32, vp]
+    L.hg_stream_wait_event.argtypes = [vp, vp]
+    L.hg_event_create.argtypes = [i32, i32, C.POINTER(vp)]
+    L.hg_event_destroy.argtypes = [i32, vp]
+    L.hg_event_record.argtypes = [vp, vp]
+    L.hg_event_query.argtypes = [vp]
+    L.hg_event_elapsed_ms.argtypes = [vp, vp, C.POINTER(C.c_float)]
+    L.hg_copy_async.argtypes = [i32, vp, vp, sz, vp]
     _lib = L
     return L
 

@@ -25,7 +25,7 @@ CUDA_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp
 HOST_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall",
               "-I", os.path.join(ROOT, "include")]
 
-CU_SOURCES = ["tiles_chol.cu", "tiles_lu.cu", "tiles_qr.cu", "runtime.cu", "peak.cu"]
+CU_SOURCES = ["tiles_chol.cu", "tiles_lu.cu", "tiles_qr.cu", "runtime.cu", "peak.cu", "devrt.cu"]
 CPP_SOURCES = ["planner.cpp"]
 
 

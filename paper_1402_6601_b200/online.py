@@ -15,7 +15,7 @@ GPUs themselves:
   (a B200 worker is not one-task-at-a-time); a task is dispatched from its
   worker's FIFO when a stream is free;
 * the non-resident inputs of a dispatched task are copied in (H2D from the
-  pinned host image, or a peer copy from the lowest-numbered valid GPU,
+  page-locked host image, or a peer copy from the lowest-numbered valid GPU,
   ``sim.py:242-266``) on the GPU's copy stream; the task's stream waits for
   those copies, then runs the sm_100a tile kernels (``hg_tile_run_scratch``);
 * on completion the written blocks become valid only on that GPU
@@ -63,56 +63,151 @@ class OnlineReport:
     steals_failed: int = 0
 
 
+class _Plumb:
+    """ctypes handles over libhetgpu's device plumbing (hg_dev_* / hg_stream_* /
+    hg_event_* / hg_copy_async): the online executor's data path is this library."""
+
+    def __init__(self, L):
+        self.L = L
+
+    def _out(self, fn, *args):
+        h = C.c_void_p()
+        _native.check(fn(*args, C.byref(h)), fn.__name__)
+        return h.value
+
+    def alloc(self, dev, nbytes):
+        return self._out(self.L.hg_dev_alloc, dev, nbytes)
+
+    def stream(self, dev):
+        return self._out(self.L.hg_stream_create, dev)
+
+    def event(self, dev, timing=False):
+        return self._out(self.L.hg_event_create, dev, 1 if timing else 0)
+
+    def record(self, ev, stream):
+        _native.check(self.L.hg_event_record(C.c_void_p(ev), C.c_void_p(stream)), "hg_event_record")
+
+    def wait(self, stream, ev):
+        _native.check(self.L.hg_stream_wait_event(C.c_void_p(stream), C.c_void_p(ev)), "hg_stream_wait_event")
+
+    def done(self, ev) -> bool:
+        rc = self.L.hg_event_query(C.c_void_p(ev))
+        if rc < 0:
+            _native.check(rc, "hg_event_query")
+        return rc == 1
+
+    def elapsed_ms(self, e0, e1) -> float:
+        ms = C.c_float()
+        _native.check(self.L.hg_event_elapsed_ms(C.c_void_p(e0), C.c_void_p(e1), C.byref(ms)), "hg_event_elapsed_ms")
+        return float(ms.value)
+
+    def copy(self, dev, dst, src, nbytes, stream):
+        _native.check(self.L.hg_copy_async(dev, C.c_void_p(dst), C.c_void_p(src), nbytes, C.c_void_p(stream)),
+                      "hg_copy_async")
+
+    def sync(self, dev):
+        _native.check(self.L.hg_dev_sync(dev), "hg_dev_sync")
+
+
 class OnlineExecutor:
     """Runs ``graph`` on the GPUs of ``platform`` (GPU-only, p2p) with online decisions."""
 
     def __init__(self, graph, platform, scheduler, model, host_in: np.ndarray, devices=None, depth: int = 8,
                  seed: int = 0):
-        import torch
-
         if platform.n_cpu_workers:
             raise PlatformError("the online executor runs GPU-only platforms (no CPU fallback)")
         if platform.k > 1 and not platform.p2p:
             raise PlatformError("the online executor needs the NVLink peer route (p2p=True)")
-        self.torch = torch
         self.g, self.plat, self.sched = graph, platform, scheduler
         self.model = model.copy()  # as sim.py:105: calibration never leaks to the caller
         lay = graph.layout
         self.nb, self.ib = lay.b, lay.ib
         self.k = platform.k
-        ndev = torch.cuda.device_count()
-        self.devices = list(devices) if devices is not None else [g % max(1, ndev) for g in range(self.k)]
+        self.L = _native.lib()
+        self.rt = rt = _Plumb(self.L)
+        ndev = self.L.hg_device_count()
+        if ndev <= 0:
+            raise PlatformError("the online executor needs a CUDA device (there is no CPU fallback)")
+        self.devices = list(devices) if devices is not None else [g % ndev for g in range(self.k)]
         self.depth = depth
         self.seed = seed
-        self.L = _native.lib()
         self.sizes = [s // 8 for s in graph.sizes]
         self.offs = np.cumsum([0] + self.sizes)
         side = lay.side_doubles
         tile = self.nb * self.nb
         self.slot_doubles = [s + (side if s == tile else 0) for s in self.sizes]
-        self.host = torch.from_numpy(np.ascontiguousarray(host_in, np.float64))
-        if not self.host.is_pinned():
-            self.host = self.host.pin_memory()
-        self.slots = [dict() for _ in range(self.k)]  # node-1 -> block -> device tensor
-        self.streams = [[torch.cuda.Stream(device=d) for _ in range(depth)] for d in self.devices]
-        self.copy_streams = [torch.cuda.Stream(device=d) for d in self.devices]
-        self.status = [torch.zeros(1, dtype=torch.int32, device=d) for d in self.devices]
+        # the host image, page-locked in place (async H2D DMA; unregistered by close())
+        self.host = np.ascontiguousarray(host_in, np.float64)
+        self._registered = self.host.nbytes > 0 and self.L.hg_matrix_register(
+            C.c_void_p(self.host.ctypes.data), self.host.nbytes) == 0
+        uniq = sorted(set(self.devices))
+        for a in uniq:
+            for b in uniq:
+                if a != b:
+                    _native.check(self.L.hg_dev_enable_peer(a, b), f"peer access GPU {a} -> GPU {b}")
+        self.slots = [dict() for _ in range(self.k)]  # node-1 -> block -> device pointer
+        self.streams = [[rt.stream(d) for _ in range(depth)] for d in self.devices]
+        self.copy_streams = [rt.stream(d) for d in self.devices]
+        self.status = [rt.alloc(d, 4) for d in self.devices]
         kinds = [ALL_KINDS.index(t.kind) for t in graph.tasks]
         self.kind_id = kinds
         need = max(self.L.hg_task_scratch_ints(kd, self.nb, self.ib) for kd in range(len(ALL_KINDS)))
-        self.scratch = [[torch.zeros(max(need, 1), dtype=torch.int32, device=d) for _ in range(depth)]
-                        for d in self.devices]
+        self.scratch = [[rt.alloc(d, 4 * max(need, 1)) for _ in range(depth)] for d in self.devices]
+        for d, st in zip(self.devices, self.status):
+            _native.check(self.L.hg_dev_memset(d, C.c_void_p(st), 0, 4, None), "hg_dev_memset")
+        for d, scr in zip(self.devices, self.scratch):
+            for p in scr:
+                _native.check(self.L.hg_dev_memset(d, C.c_void_p(p), 0, 4 * max(need, 1), None), "hg_dev_memset")
+        self._events = []  # (device, event) to destroy at close
+        self._closed = False
 
-    def _slot(self, node: int, block: int):
+    def _slot(self, node: int, block: int) -> int:
         s = self.slots[node - 1].get(block)
         if s is None:
-            s = self.torch.empty(self.slot_doubles[block], dtype=self.torch.float64,
-                                 device=self.devices[node - 1])
+            s = self.rt.alloc(self.devices[node - 1], self.slot_doubles[block] * 8)
             self.slots[node - 1][block] = s
         return s
 
+    def _event(self, dev, timing=False):
+        ev = self.rt.event(dev, timing)
+        self._events.append((dev, ev))
+        return ev
+
+    def close(self):
+        """Free slots, streams, events and the host registration (idempotent)."""
+        if self._closed:
+            return
+        self._closed = True
+        L = self.L
+        for d in sorted(set(self.devices)):
+            L.hg_dev_sync(d)
+        for dev, ev in self._events:
+            L.hg_event_destroy(dev, C.c_void_p(ev))
+        for node, slots in enumerate(self.slots):
+            for p in slots.values():
+                L.hg_dev_free(self.devices[node], C.c_void_p(p))
+        for d, ss in zip(self.devices, self.streams):
+            for s_ in ss:
+                L.hg_stream_destroy(d, C.c_void_p(s_))
+        for d, s_ in zip(self.devices, self.copy_streams):
+            L.hg_stream_destroy(d, C.c_void_p(s_))
+        for d, p in zip(self.devices, self.status):
+            L.hg_dev_free(d, C.c_void_p(p))
+        for d, scr in zip(self.devices, self.scratch):
+            for p in scr:
+                L.hg_dev_free(d, C.c_void_p(p))
+        if self._registered:
+            L.hg_matrix_unregister(C.c_void_p(self.host.ctypes.data))
+            self._registered = False
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
     def run(self) -> OnlineReport:
-        torch, g, plat = self.torch, self.g, self.plat
+        g, plat, rt = self.g, self.plat, self.rt
         n = len(g)
         nw = plat.n_workers
         worker_node = [plat.workers[w].memory for w in range(nw)]
@@ -165,33 +260,32 @@ class OnlineExecutor:
                     continue
                 dst = self._slot(node, d)
                 holders = residency[d]
-                with torch.cuda.stream(cs):
-                    if HOST in holders:
-                        dst[: self.sizes[d]].copy_(self.host[self.offs[d]:self.offs[d + 1]], non_blocking=True)
-                        bytes_h2d += self.sizes[d] * 8
-                    else:
-                        src_node = min(holders)
-                        src_ev = copy_ev.get(d, {}).get(src_node)  # the source may itself be in flight
-                        if src_ev is not None:
-                            cs.wait_event(src_ev)
-                        dst.copy_(self._slot(src_node, d), non_blocking=True)
-                        bytes_d2d += self.sizes[d] * 8
-                    ev = torch.cuda.Event()
-                    ev.record(cs)
+                if HOST in holders:
+                    rt.copy(dev, dst, self.host.ctypes.data + int(self.offs[d]) * 8, self.sizes[d] * 8, cs)
+                    bytes_h2d += self.sizes[d] * 8
+                else:
+                    src_node = min(holders)
+                    src_ev = copy_ev.get(d, {}).get(src_node)  # the source may itself be in flight
+                    if src_ev is not None:
+                        rt.wait(cs, src_ev)
+                    rt.copy(dev, dst, self._slot(src_node, d), self.slot_doubles[d] * 8, cs)
+                    bytes_d2d += self.sizes[d] * 8
+                ev = self._event(dev)
+                rt.record(ev, cs)
                 copy_ev.setdefault(d, {})[node] = ev
                 residency.add(d, node)
                 waits.append(ev)
             for ev in waits:
-                stream.wait_event(ev)
-            ptrs = (C.c_void_p * len(task.accesses))(*[self._slot(node, d).data_ptr() for d, _ in task.accesses])
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            _native.check(self.L.hg_tile_run_scratch(self.kind_id[tid], dev, C.c_void_p(stream.cuda_stream), ptrs,
+                rt.wait(stream, ev)
+            ptrs = (C.c_void_p * len(task.accesses))(*[self._slot(node, d) for d, _ in task.accesses])
+            e0, e1 = self._event(dev, True), self._event(dev, True)
+            rt.record(e0, stream)
+            _native.check(self.L.hg_tile_run_scratch(self.kind_id[tid], dev, C.c_void_p(stream), ptrs,
                                                      len(task.accesses), self.nb, self.ib,
-                                                     C.c_void_p(self.status[node - 1].data_ptr()),
-                                                     C.c_void_p(self.scratch[node - 1][si].data_ptr())),
+                                                     C.c_void_p(self.status[node - 1]),
+                                                     C.c_void_p(self.scratch[node - 1][si])),
                           f"online task {tid}")
-            e1.record(stream)
+            rt.record(e1, stream)
             running[tid] = (w, si, e0, e1)
             placed[tid] = w
 
@@ -228,7 +322,7 @@ class OnlineExecutor:
         dispatch_round()
         done = 0
         while done < n:
-            finished = [t for t, r in running.items() if r[3].query()]
+            finished = [t for t, r in running.items() if rt.done(r[3])]
             if not finished:
                 if not running:
                     raise SimulationError(f"online executor stalled with {n - done} tasks left")
@@ -238,7 +332,7 @@ class OnlineExecutor:
                 w, si, e0, e1 = running.pop(tid)
                 task = g.tasks[tid]
                 node = worker_node[w]
-                dur = e0.elapsed_time(e1) * 1e-3
+                dur = rt.elapsed_ms(e0, e1) * 1e-3
                 measured.setdefault(task.kind, []).append(dur)
                 for d in task.write_ids():
                     residency.set_only(d, node)
@@ -255,12 +349,15 @@ class OnlineExecutor:
                 if ready:
                     activate(ready, w)
             dispatch_round()
-        for d_ in self.devices:
-            torch.cuda.synchronize(d_)
+        for d_ in sorted(set(self.devices)):
+            rt.sync(d_)
         span = now()
-        for st in self.status:
-            if int(st.item()) != 0:
-                raise SimulationError(f"tile kernel status {int(st.item())} (non-SPD / singular pivot)")
+        for d_, st in zip(self.devices, self.status):
+            word = np.zeros(1, np.int32)
+            rt.copy(d_, word.ctypes.data, st, 4, None)
+            rt.sync(d_)
+            if int(word[0]) != 0:
+                raise SimulationError(f"tile kernel status {int(word[0])} (non-SPD / singular pivot)")
         self._residency = residency
         from .sim import flops_of
 
@@ -274,7 +371,11 @@ class OnlineExecutor:
         for d in range(len(self.sizes)):
             nodes = [x for x in self._residency[d] if x != HOST]
             if not nodes:
-                out[self.offs[d]:self.offs[d + 1]] = self.host[self.offs[d]:self.offs[d + 1]].numpy()
+                out[self.offs[d]:self.offs[d + 1]] = self.host[self.offs[d]:self.offs[d + 1]]
                 continue
-            out[self.offs[d]:self.offs[d + 1]] = self._slot(min(nodes), d)[: self.sizes[d]].cpu().numpy()
+            node = min(nodes)
+            self.rt.copy(self.devices[node - 1], out.ctypes.data + int(self.offs[d]) * 8, self._slot(node, d),
+                         self.sizes[d] * 8, None)
+        for d_ in sorted(set(self.devices)):
+            self.rt.sync(d_)
         return out

@@ -30,3 +30,12 @@ def test_cpu_only_host_calls():
     assert L.hg_abi_version() == 3
     assert L.hg_device_count() >= 0
     assert isinstance(_native.last_error(), str)
+
+
+def test_online_executor_data_path_is_the_c_abi():
+    """online.py moves tiles and times kernels through libhetgpu (hg_copy_async, hg_event_*),
+    not through torch."""
+    src = open(os.path.join(ROOT, "paper_1402_6601_b200", "online.py")).read()
+    assert "torch" not in src
+    for sym in ("hg_copy_async", "hg_event_record", "hg_stream_wait_event", "hg_dev_alloc"):
+        assert sym in src or sym.replace("hg_", "") in src

@@ -23,6 +23,22 @@ differences: two backward-stable evaluations in different summation orders
 differ by ~ c(n) eps kappa of the trailing Schur complements, which stays
 below 1e-12 for these matrices.
 
+LU-incpiv (configs[2]) is ill-posed at the pivot level for this matrix: the
+oracle on the 1-ulp perturbed input (oracle.tiles.ulp_perturbed, one rounding
+per entry) flips 24 pivots of TSTRF(4, 25) at column 968 (task 4314) and from
+there its own factor moves by O(1) (profiles/r02_lu_sensitivity_32768.json) --
+the GPU flips at exactly that decision.  So for LU the oracle is run twice
+(A and its 1-ulp perturbation) and the test asserts, per the north star:
+* residuals within 1e-12 of the oracle's (independent of any pivot flip);
+* pivots identical to the oracle's in every tile finalized before the first
+  decision the perturbation flips (all tiles if it flips none), and the GPU's
+  first differing decision is not earlier than that;
+* element-wise, on those tiles, within 100x of the perturbed oracle's own
+  difference (one rounding per input entry vs a different summation order in
+  every operation);
+* the k=8 factor is bit-identical to the k=1 factor (same kernels on the same
+  inputs: the virtual-node execution changes placement and copies, not values).
+
 Host memory: ~40 GB per family (A, oracle factor, input image, output image).
 ``HG_PARITY_OUT=<file>`` appends the measured numbers as JSON lines.
 """
@@ -67,16 +83,17 @@ def _matrix(fam):
 
 
 class _OracleFactor:
-    """The oracle's factor read back from oracle/factor_job.py's files (tiles / side like TileArena)."""
+    """The oracle's factor read back from oracle/factor_job.py's files (tiles / side like TileArena),
+    memory-mapped (the files live in /dev/shm until the module ends)."""
 
     def __init__(self, g, out):
         lay = g.layout
         self.ids = sorted(lay.tiles)
-        tl = np.fromfile(os.path.join(out, "tiles.f64"), np.float64)
+        tl = np.memmap(os.path.join(out, "tiles.f64"), np.float64, mode="r")
         self.tiles = {d: tl[i * NB * NB:(i + 1) * NB * NB].reshape(NB, NB, order="F") for i, d in enumerate(self.ids)}
         self.aux, self.piv = {}, {}
         if lay.family != "cholesky":
-            sd = np.fromfile(os.path.join(out, "side.f64"), np.float64)
+            sd = np.memmap(os.path.join(out, "side.f64"), np.float64, mode="r")
             per = IB * NB + NB
             for i, d in enumerate(self.ids):
                 self.aux[d] = sd[i * per:i * per + IB * NB].reshape(IB, NB, order="F")
@@ -86,23 +103,39 @@ class _OracleFactor:
     side = X.TileArena.side
 
 
+_dirs = []
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cleanup():
+    yield
+    _cache.clear()
+    for d in _dirs:
+        shutil.rmtree(d, ignore_errors=True)
+
+
+def _factor_job(fam, perturb=-1):
+    tmp = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    _dirs.append(tmp)
+    res = subprocess.run([sys.executable, "-m", "oracle.factor_job", fam, str(N), str(NB), str(IB),
+                          str(SEED[fam]), tmp, "0", str(perturb)], cwd=ROOT, capture_output=True, text=True,
+                         timeout=1800)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
+    return tmp, json.loads(res.stdout.strip().splitlines()[-1])["seconds"]
+
+
 def _oracle(fam):
-    """(A, graph, oracle factor, seconds) for ``fam``; one family cached at a time (host memory).
-    The oracle runs in a fresh process (oracle/factor_job.py), not forked from this one."""
+    """(A, graph, oracle factor, seconds[, perturbed-input oracle factor for LU]) for ``fam``; one
+    family cached at a time (host memory).  The oracle runs in a fresh process
+    (oracle/factor_job.py), not forked from this one."""
     if fam not in _cache:
         _cache.clear()
         g = H.gen_family(fam, N // NB, NB, IB)
-        tmp = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
-        try:
-            res = subprocess.run([sys.executable, "-m", "oracle.factor_job", fam, str(N), str(NB), str(IB),
-                                  str(SEED[fam]), tmp], cwd=ROOT, capture_output=True, text=True, timeout=1800)
-            assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
-            secs = json.loads(res.stdout.strip().splitlines()[-1])["seconds"]
-            fac = _OracleFactor(g, tmp)
-        finally:
-            shutil.rmtree(tmp, ignore_errors=True)
-        _cache[fam] = (_matrix(fam), g, fac, secs)
-    return _cache[fam]
+        out, secs = _factor_job(fam)
+        fac = _OracleFactor(g, out)
+        pert = _OracleFactor(g, _factor_job(fam, perturb=1)[0]) if fam == "lu" else None
+        _cache[fam] = (_matrix(fam), g, fac, secs, pert)
+    return _cache[fam][:4]
 
 
 def _plan(g, fam, k):
@@ -176,43 +209,107 @@ def _record(row):
             f.write(json.dumps(row) + "\n")
 
 
+_digest = {}  # family -> sha256 of the k=1 GPU factor (tiles + side areas)
+
+
+def _sha(tiles, side, lay):
+    import hashlib
+
+    h = hashlib.sha256()
+    for d in sorted(lay.tiles):
+        h.update(np.ascontiguousarray(tiles[d]).tobytes())
+        if d in side:
+            h.update(np.ascontiguousarray(side[d]).tobytes())
+    return h.hexdigest()
+
+
+def _final_writer_order(g):
+    fw = {}
+    for t in range(len(g)):
+        for d, m in g.tasks[t].accesses:
+            if d in g.layout.tiles and "W" in m.value:
+                fw[d] = t
+    return fw
+
+
+def _gpu_ipiv(side_d):
+    return side_d[IB * NB:].view(np.int32)[:NB].astype(np.int64)
+
+
 @pytest.mark.parametrize("fam,k", [("cholesky", 1), ("cholesky", 8), ("lu", 1), ("lu", 8), ("qr", 1), ("qr", 8)])
 def test_full_size_elementwise(fam, k):
     A, g, arena, oracle_s = _oracle(fam)
+    pert = _cache[fam][4]
     lay = g.layout
     tiles, side, st, plan = _gpu(fam, k)
+    digest = _sha(tiles, side, lay)
+    if k == 1:
+        _digest[fam] = digest
+    elif fam in _digest:
+        # same kernels on the same inputs: placement and copies must not change a single bit
+        assert digest == _digest[fam], "k=8 factor differs from the k=1 factor"
     ref = arena.tiles
+    ora_side = arena.side() if fam != "cholesky" else {}
+    # LU: the tiles finalized before the first pivot decision a 1-ulp input perturbation flips
+    stable = set(lay.tiles)
+    row_extra = {}
+    if fam == "lu":
+        fw = _final_writer_order(g)
+        pside = pert.side()
+        flip_p = flip_g = None
+        for d in sorted(lay.tiles, key=lambda d_: fw[d_]):
+            i, j = lay.tiles[d]
+            if i < j:
+                continue
+            if flip_p is None and not np.array_equal(pside[d]["ipiv"], ora_side[d]["ipiv"]):
+                flip_p = fw[d]
+            if flip_g is None and not np.array_equal(_gpu_ipiv(side[d]), ora_side[d]["ipiv"]):
+                flip_g = fw[d]
+        row_extra = {"first_flip_task_perturbed": flip_p, "first_flip_task_gpu": flip_g}
+        if flip_p is None:
+            assert flip_g is None, ("GPU pivots differ where the problem is stable", flip_g)
+        else:
+            assert flip_g is None or flip_g >= flip_p, ("GPU pivots differ before the first unstable decision",
+                                                        flip_g, flip_p)
+        cut = min(x for x in (flip_p, flip_g, len(g)) if x is not None)
+        stable = {d for d in lay.tiles if fw[d] < cut}
     scale = max(float(np.abs(t).max()) for t in ref.values())
-    diff = 0.0
+    diff = pdiff = 0.0
     for d, (i, j) in lay.tiles.items():
+        if d not in stable:
+            continue
         a, b = tiles[d], ref[d]
         if fam == "cholesky" and i == j:
             a, b = np.tril(a), np.tril(b)  # upper triangle of a diagonal tile is workspace
         if fam == "cholesky" and i < j:
             continue
         diff = max(diff, float(np.abs(a - b).max()))
+        if pert is not None:
+            pdiff = max(pdiff, float(np.abs(pert.tiles[d] - b).max()))
     elem = diff / scale
     row = {"family": fam, "k": k, "n": N, "nb": NB, "elem_rel": elem, "oracle_seconds": oracle_s,
-           "oracle_workers": X.host_threads(), "gpu_ms": st.elapsed_ms, "bytes_d2d": st.bytes_d2d}
+           "oracle_workers": X.host_threads(), "gpu_ms": st.elapsed_ms, "bytes_d2d": st.bytes_d2d,
+           "sha256_16": digest[:16], **row_extra}
+    if pert is not None:
+        row.update(elem_rel_perturbed_oracle=pdiff / scale, stable_tiles=len(stable), tiles=len(lay.tiles))
     rng = np.random.default_rng(9)
     if fam == "cholesky":
         x = rng.standard_normal(N)
         r_gpu, r_cpu = _chol_residual(A, tiles, lay, x), _chol_residual(A, ref, lay, x)
     elif fam == "lu":
         gside, side_diff, inv_scale = {}, 0.0, 0.0
-        ora_side = arena.side()
         for d, (i, j) in lay.tiles.items():
             if i < j:
                 continue  # U tiles carry no side area
             s = side[d]
-            ipiv = s[IB * NB:].view(np.int32)[:NB].astype(np.int64)
-            assert np.array_equal(ipiv, ora_side[d]["ipiv"]), ("pivots differ", i, j)
+            ipiv = _gpu_ipiv(s)
             inv = s[: IB * NB].reshape(IB, NB, order="F")
             dl = np.zeros((IB, NB))
             for ii in range(0, NB, IB):
-                ref_inv = np.linalg.inv(np.eye(IB) + np.tril(ora_side[d]["dl"][:, ii:ii + IB], -1))
-                side_diff = max(side_diff, float(np.abs(inv[:, ii:ii + IB] - ref_inv).max()))
-                inv_scale = max(inv_scale, float(np.abs(ref_inv).max()))
+                if d in stable:
+                    ref_inv = np.linalg.inv(np.eye(IB) + np.tril(ora_side[d]["dl"][:, ii:ii + IB], -1))
+                    side_diff = max(side_diff, float(np.abs(inv[:, ii:ii + IB] - ref_inv).max()))
+                    inv_scale = max(inv_scale, float(np.abs(ref_inv).max()))
                 dl[:, ii:ii + IB] = np.tril(np.linalg.inv(inv[:, ii:ii + IB]), -1)
             gside[d] = {"ipiv": ipiv, "dl": dl}
         row["side_rel"] = side_diff / inv_scale
@@ -225,7 +322,6 @@ def test_full_size_elementwise(fam, k):
 
         r_gpu, r_cpu = res(tiles, gside), res(ref, ora_side)
     else:
-        ora_side = arena.side()
         gside, side_diff, t_scale = {}, 0.0, 0.0
         for d, (i, j) in lay.tiles.items():
             if i < j:
@@ -246,6 +342,10 @@ def test_full_size_elementwise(fam, k):
     print(json.dumps(row))
     assert np.isfinite(r_gpu) and abs(r_gpu - r_cpu) <= RES_TOL, row
     assert r_gpu < 1e-12, row
-    assert elem <= ELEM_TOL[fam], row
-    if "side_rel" in row:
-        assert row["side_rel"] <= ELEM_TOL[fam], row
+    if fam == "lu":
+        # within 100x of one rounding per input entry (the oracle's own sensitivity on these tiles)
+        assert elem <= max(ELEM_TOL[fam], 100 * row["elem_rel_perturbed_oracle"]), row
+    else:
+        assert elem <= ELEM_TOL[fam], row
+        if "side_rel" in row:
+            assert row["side_rel"] <= ELEM_TOL[fam], row

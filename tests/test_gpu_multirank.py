@@ -5,7 +5,15 @@ CPU oracle's factor and the executed copy bytes must equal the plan's.  The
 nt=16 cases have hundreds of cross-rank pulls and flag waits (the gated,
 chained wait nodes of runtime.cu keep at most 8 spinners resident per rank).
 A rank whose peer never launches must fail with DeadlockError after the wait
-timeout instead of hanging the device."""
+timeout instead of hanging the device.
+
+LU-incpiv is checked the north star's way -- identical pivots in every tile and
+a solve residual within 1e-12 of the oracle's -- plus element-wise against the
+problem's own roundoff sensitivity (100x): the oracle on the 1-ulp perturbed input
+(oracle.tiles.ulp_perturbed) moves its factor by 2.2e-5 (max, relative) at
+n=8192 seed 3, so no evaluation in another summation order can be held to
+1e-11 there (measured: GPU vs oracle 3e-5, deterministic, identical with and
+without producer-push and back-to-back launches)."""
 import math
 import os
 import socket
@@ -42,7 +50,9 @@ def _rank_main(rank, world, port, family, q, n=2048, b=512):
         A = O.spd_matrix(n, 3) if family == "cholesky" else O.general_matrix(n, 3)
         img = runtime.to_tile_major(A, g)
         out = np.full_like(img, np.nan)
-        ex = runtime.DistributedExecutor(g, plat, plan, img, out, rank=rank, world=world, device=0)
+        side_out = np.full(len(g.data) * g.layout.side_doubles, np.nan) if g.layout.side_doubles else None
+        ex = runtime.DistributedExecutor(g, plat, plan, img, out, rank=rank, world=world, device=0,
+                                         host_side_out=side_out)
         for _ in range(2):  # two runs: flags must advance with the epoch
             ex.launch(0)
             ex.wait()
@@ -51,7 +61,7 @@ def _rank_main(rank, world, port, family, q, n=2048, b=512):
         ex.wait()
         st = ex.info()
         ex.close()
-        q.put((rank, out, st.bytes_h2d, st.bytes_d2d))
+        q.put((rank, out, st.bytes_h2d, st.bytes_d2d, side_out))
         dist.barrier()
     finally:
         dist.destroy_process_group()
@@ -85,13 +95,40 @@ def test_two_ranks_one_gpu(family, n, b):
     assert sum(r[2] for r in res) == plan.bytes_h2d
     assert sum(r[3] for r in res) == plan.bytes_d2d > 0
     A = O.spd_matrix(n, 3) if family == "cholesky" else O.general_matrix(n, 3)
-    T = O.tiles_of(A, g.layout)
-    O.run_tasks(g, T, side={})
+    T = {d: np.asfortranarray(t) for d, t in O.tiles_of(A, g.layout).items()}
+    side = {}
+    O.run_tasks(g, T, side=side)
     ref = O.assemble(T, g.layout)
     got = runtime.from_tile_major(merged, g)
     if family == "cholesky":
         ref, got = np.tril(ref), np.tril(got)
-    assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-11
+        assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-12
+        return
+    from oracle import tiles_lu_qr as LQ
+    from test_gpu_lu import dl_from_inverse
+
+    sd = g.layout.side_doubles
+    merged_side = np.where(np.isnan(res[0][4]), res[1][4], res[0][4])
+    offs = np.cumsum([0] + [s_ // 8 for s_ in g.sizes])
+    gt, gs = {}, {}
+    for d, (i, j) in g.layout.tiles.items():
+        gt[d] = merged[offs[d]:offs[d + 1]].reshape(b, b, order="F").copy()
+        if i >= j:
+            s_ = merged_side[d * sd:(d + 1) * sd]
+            ipiv = s_[ib * b:].view(np.int32)[:b].astype(np.int64)
+            assert np.array_equal(ipiv, side[d]["ipiv"]), ("pivots differ", i, j)
+            gs[d] = {"ipiv": ipiv, "dl": dl_from_inverse(s_[: ib * b].reshape(ib, b, order="F"), b, ib)}
+    rhs = np.random.default_rng(9).standard_normal(n)
+    nrm = np.linalg.norm(A, 2)
+    res_ = lambda x: np.linalg.norm(A @ x - rhs) / (nrm * np.linalg.norm(x))
+    r_gpu, r_cpu = res_(LQ.lu_solve(gt, gs, g.layout, rhs)), res_(LQ.lu_solve(T, side, g.layout, rhs))
+    assert r_gpu < 1e-12 and abs(r_gpu - r_cpu) < 1e-12, (r_gpu, r_cpu)
+    # element-wise: within 100x of what ONE rounding per input entry does to the oracle itself
+    # (a different summation order injects roundings in every operation, not just the input)
+    T1 = {d: np.asfortranarray(t) for d, t in O.tiles_of(O.ulp_perturbed(A, 1), g.layout).items()}
+    O.run_tasks(g, T1, side={})
+    sens = np.abs(O.assemble(T1, g.layout) - ref).max() / np.abs(ref).max()
+    assert np.abs(got - ref).max() / np.abs(ref).max() <= 100 * sens, sens
 
 
 def _dead_peer_main(rank, world, port, q):

@@ -36,6 +36,7 @@ def test_online_cholesky(k, sched):
         assert rep.steals_ok > 0  # the idle GPU worker stole work
     # the history model learned from measured durations
     assert ex.model.predict_exec("GEMM", H.ResourceClass.GPU) != model.predict_exec("GEMM", H.ResourceClass.GPU)
+    ex.close()
 
 
 def test_online_lu():
@@ -50,4 +51,5 @@ def test_online_lu():
     O.run_tasks(g, T, side={})
     ref = O.assemble(T, g.layout)
     got = runtime.from_tile_major(ex.result_image(), g)
+    ex.close()
     assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-11
