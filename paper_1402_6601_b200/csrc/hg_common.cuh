@@ -73,6 +73,37 @@ HG_DEVICE void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b)
                : "memory");
 }
 
+// ---- cluster push messages: remote shared-memory stores that complete on the
+// receiver's mbarrier (no cluster barrier, no release fence over global memory) ----
+// shared::cluster address of `p` (this CTA's smem) in CTA `rank` of the cluster
+HG_DEVICE unsigned cluster_addr(const void* p, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// 8-byte store into another CTA's smem, counted (8 bytes) on that CTA's mbarrier
+HG_DEVICE void st_async_f64(unsigned remote_addr, double v, unsigned remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(remote_addr),
+               "d"(v), "r"(remote_bar)
+               : "memory");
+}
+HG_DEVICE void st_async_v2f64(unsigned remote_addr, double a, double b, unsigned remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(
+                   remote_addr),
+               "d"(a), "d"(b), "r"(remote_bar)
+               : "memory");
+}
+// wait for phase `parity` of a local mbarrier whose bytes arrive from other CTAs
+HG_DEVICE void mbar_wait_cluster(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+HG_DEVICE void fence_mbar_init_cluster() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+
 HG_DEVICE double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -535,9 +535,9 @@ struct SpSmem {
   static constexpr int PS = kSpSB * LDP;                  // panel [col][row]
   static constexpr int STG = 2 * kSpW * kSpSB;            // phase-S staging rows
   static constexpr int U12 = kSpW * kSpSB;                // [v][col]
-  static constexpr int MISC = 4 * kSpW + 4 + kSpW * kSpW; // cand, rowj, slots, Ublk
+  static constexpr int MISC = 4 * kSpW + 4 + 3 * kSpW * kSpW; // cand, rowj, slots, Ublk, dlS, UoutS
   static constexpr int DOUBLES = PS + STG + U12 + MISC;
-  static constexpr int INTS = kSpSB + 4 * kSpW + 3 * kSpW + 4;
+  static constexpr int INTS = kSpSB + 4 * kSpW + 3 * kSpW + 4 + 2 * kSpW;
   static constexpr size_t BYTES = size_t(DOUBLES) * 8 + size_t(INTS) * 4;
 };
 
@@ -563,11 +563,17 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   double* rowj = cand + 2 * W;          // [2][W]
   double* slot_v = rowj + 2 * W;        // [2] (+2 pad)
   double* Ublk = slot_v + 4;            // [W][W]
+  // TSTRF outputs of the column loop, staged in smem and written to global memory once per
+  // sub-panel: a global store pending at a cluster barrier makes its release fence wait for it
+  double* dlS = Ublk + W * W;           // [W][W] dL(c0 + u, c0 + v), v < u, of rows this CTA won
+  double* UoutS = dlS + W * W;          // [W][W] U row c0 + u, columns c0 + v >= u (CTA 0)
   int* swp = reinterpret_cast<int*>(sm + S::DOUBLES);  // [SB]
   int* mvd = swp + SB;                  // [2W]
   int* mvs = mvd + 2 * W;               // [2W]
   int* sp = mvs + 2 * W;                // [3W]
   int* slot_r = sp + 3 * W;             // [2]
+  int* wonS = slot_r + 4;               // [W] this CTA's row moved up at step u (dlS row valid)
+  int* uwS = wonS + W;                  // [W] U row c0 + u replaced at step u (UoutS row valid)
   __shared__ double red_v[kSpThreads / 32];
   __shared__ int red_r[kSpThreads / 32];
   __shared__ int n_mv;
@@ -585,11 +591,13 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   cl.sync();
 
   for (int c0 = 0; c0 < SB; c0 += W) {
-    if (ts)
+    if (ts) {
       for (int e = tid; e < W * W; e += kSpThreads) {
         const int u = e / W, v = e % W;
         Ublk[e] = v >= u ? __ldcg(p.U + size_t(ii + c0 + v) * nb + ii + c0 + u) : 0.0;
       }
+      if (tid < W) wonS[tid] = uwS[tid] = 0;
+    }
     double a[W];
 #pragma unroll
     for (int v = 0; v < W; ++v) a[v] = mine ? Ps[(c0 + v) * LDP + tid] : 0.0;
@@ -676,21 +684,24 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
 #pragma unroll
       for (int v2 = u; v2 < W; ++v2) prow[v2] = from_cand ? cw[v2] : Ublk[u * W + v2];
       if (tid == 0) swp[jj] = ts ? (swap ? wr : -1) : wr;
-      if (q == 0 && tid == 0) ipiv[j] = ts ? (swap ? wr : -1) : wr;
       if (swap) {
         if (ts) {
           if (mine && gr == wr) {
+            wonS[u] = 1;
 #pragma unroll
             for (int v2 = 0; v2 < W; ++v2) {
               if (v2 < u) {
-                inv[size_t(c0 + v2) * ib + jj] = a[v2];  // dL(jj, c0 + v2)
+                dlS[u * W + v2] = a[v2];  // dL(jj, c0 + v2), written out after the sub-panel
                 a[v2] = 0.0;
               } else {
                 a[v2] = Ublk[u * W + v2];
               }
             }
           }
-          if (q == 0 && tid >= u && tid < W) p.U[size_t(ii + c0 + tid) * nb + j] = cw[tid];
+          if (q == 0 && tid >= u && tid < W) {
+            UoutS[u * W + tid] = cw[tid];
+            if (tid == u) uwS[u] = 1;
+          }
         } else {
           if (mine && gr == wr) {
             const double* rj = cl.map_shared_rank(rowj, j / R) + par * W;
@@ -724,6 +735,15 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
     __syncthreads();
     // ---- S: the sub-panel's interchanges on the columns outside it ----------------------
     const int cR = c0 + W;  // first right-hand column
+    // the column loop's staged outputs: pivots, dL rows this CTA moved up, replaced U rows
+    if (q == 0 && tid < W) ipiv[ii + c0 + tid] = swp[c0 + tid];
+    if (ts) {
+      for (int e = tid; e < W * W; e += kSpThreads) {
+        const int u = e / W, v = e % W;
+        if (v < u && wonS[u]) inv[size_t(c0 + v) * ib + c0 + u] = dlS[e];
+        if (q == 0 && v >= u && uwS[u]) p.U[size_t(ii + c0 + v) * nb + ii + c0 + u] = UoutS[e];
+      }
+    }
     if (ts) {
       // (i) a swapped A row's multipliers left of the sub-panel move to dL(jj, .) (first swap only)
       for (int u = 0; u < W; ++u) {

@@ -108,8 +108,13 @@ def test_two_ranks_one_gpu(family, n, b):
     from test_gpu_lu import dl_from_inverse
 
     sd = g.layout.side_doubles
-    merged_side = np.where(np.isnan(res[0][4]), res[1][4], res[0][4])
     offs = np.cumsum([0] + [s_ // 8 for s_ in g.sizes])
+    # side areas hold int32 pivots (-1 = no swap reads as a NaN double): take each block's side
+    # from the rank whose write-back filled its tile
+    merged_side = np.empty_like(res[0][4])
+    for d in range(len(g.data)):
+        r = 0 if not np.isnan(res[0][1][offs[d]]) else 1
+        merged_side[d * sd:(d + 1) * sd] = res[r][4][d * sd:(d + 1) * sd]
     gt, gs = {}, {}
     for d, (i, j) in g.layout.tiles.items():
         gt[d] = merged[offs[d]:offs[d + 1]].reshape(b, b, order="F").copy()
@@ -122,7 +127,8 @@ def test_two_ranks_one_gpu(family, n, b):
     nrm = np.linalg.norm(A, 2)
     res_ = lambda x: np.linalg.norm(A @ x - rhs) / (nrm * np.linalg.norm(x))
     r_gpu, r_cpu = res_(LQ.lu_solve(gt, gs, g.layout, rhs)), res_(LQ.lu_solve(T, side, g.layout, rhs))
-    assert r_gpu < 1e-12 and abs(r_gpu - r_cpu) < 1e-12, (r_gpu, r_cpu)
+    # LU-incpiv's own backward error grows with n (~1e-12 at n=8192): no worse than the oracle's
+    assert r_gpu <= 1.25 * r_cpu + 1e-13 and abs(r_gpu - r_cpu) <= max(1e-12, 0.25 * r_cpu), (r_gpu, r_cpu)
     # element-wise: within 100x of what ONE rounding per input entry does to the oracle itself
     # (a different summation order injects roundings in every operation, not just the input)
     T1 = {d: np.asfortranarray(t) for d, t in O.tiles_of(O.ulp_perturbed(A, 1), g.layout).items()}
