@@ -525,6 +525,24 @@ __device__ int lu_moves(const int* steps, int ii, int sb, bool ts, int* sp, int*
 //     right-hand columns get U12 = L11^-1 A12 (owner of the 16 pivot rows /
 //     CTA 0 for TSTRF) and A22 -= L21 U12 (every row, registers x broadcast).
 // Same outputs as k_lu_panel (ipiv, dL, panel values, inv(L_uu) in the side area).
+// Phase timestamps of k_lu_panel_sp for tools/panel_stamps.cu (built with -DHG_PANEL_STAMPS; the
+// product build compiles them out): g_panel_stamps[cta][k] = %globaltimer of thread 0.
+#ifdef HG_PANEL_STAMPS
+__device__ unsigned long long g_panel_stamps[8][512];
+#define HG_STAMP(k)                                                                     \
+  do {                                                                                  \
+    if (threadIdx.x == 0) {                                                             \
+      unsigned long long t_;                                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+      g_panel_stamps[q][(k)] = t_;                                                      \
+    }                                                                                   \
+  } while (0)
+#else
+#define HG_STAMP(k) \
+  do {              \
+  } while (0)
+#endif
+
 constexpr int kSpW = 16;
 constexpr int kSpThreads = 128;
 constexpr int kSpSB = kLuMaxSb;
@@ -535,7 +553,10 @@ struct SpSmem {
   static constexpr int PS = kSpSB * LDP;                  // panel [col][row]
   static constexpr int STG = 2 * kSpW * kSpSB;            // phase-S staging rows
   static constexpr int U12 = kSpW * kSpSB;                // [v][col]
-  static constexpr int MISC = 4 * kSpW + 4 + 3 * kSpW * kSpW; // cand, rowj, slots, Ublk, dlS, UoutS
+  static constexpr int REC = 2 + kSpW;                    // column message: (value, row), candidate row
+  static constexpr int INBOX = 2 * kLuCl * REC;           // [parity][sender] messages
+  static constexpr int MISC = INBOX + 2 * kSpW + 2 * kSpW + 2 + 4 * kSpW * kSpW;
+  // inbox, rowjIn[2][W], mycand/myrowj, 2 mbarriers, Ublk, dlS, UoutS
   static constexpr int DOUBLES = PS + STG + U12 + MISC;
   static constexpr int INTS = kSpSB + 4 * kSpW + 3 * kSpW + 4 + 2 * kSpW;
   static constexpr size_t BYTES = size_t(DOUBLES) * 8 + size_t(INTS) * 4;
@@ -559,20 +580,25 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   double* Ps = sm;
   double* stg = Ps + S::PS;
   double* U12 = stg + S::STG;
-  double* cand = U12 + S::U12;          // [2][W]
-  double* rowj = cand + 2 * W;          // [2][W]
-  double* slot_v = rowj + 2 * W;        // [2] (+2 pad)
-  double* Ublk = slot_v + 4;            // [W][W]
+  // per-column messages: every CTA pushes (local best |value|, its row, that row's W sub-panel
+  // values) into every CTA's inbox with st.async, completing on the receiver's mbarrier -- no
+  // cluster barrier per column.  GETRF: the owner of row j also pushes row j (rowjIn).
+  double* inbox = U12 + S::U12;         // [2][kLuCl][REC]
+  double* rowjIn = inbox + S::INBOX;    // [2][W]
+  double* mycand = rowjIn + 2 * W;      // [W] staging of this CTA's candidate row
+  double* myrowj = mycand + W;          // [W] staging of row j (its owner)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(myrowj + W);  // [2] by column parity
+  double* Ublk = myrowj + W + 2;        // [W][W]
   // TSTRF outputs of the column loop, staged in smem and written to global memory once per
   // sub-panel: a global store pending at a cluster barrier makes its release fence wait for it
   double* dlS = Ublk + W * W;           // [W][W] dL(c0 + u, c0 + v), v < u, of rows this CTA won
   double* UoutS = dlS + W * W;          // [W][W] U row c0 + u, columns c0 + v >= u (CTA 0)
+  double* dlAll = UoutS + W * W;        // [W][W] CTA 0: the sub-panel's whole dL block (forward solve)
   int* swp = reinterpret_cast<int*>(sm + S::DOUBLES);  // [SB]
   int* mvd = swp + SB;                  // [2W]
   int* mvs = mvd + 2 * W;               // [2W]
   int* sp = mvs + 2 * W;                // [3W]
-  int* slot_r = sp + 3 * W;             // [2]
-  int* wonS = slot_r + 4;               // [W] this CTA's row moved up at step u (dlS row valid)
+  int* wonS = sp + 3 * W;               // [W] this CTA's row moved up at step u (dlS row valid)
   int* uwS = wonS + W;                  // [W] U row c0 + u replaced at step u (UoutS row valid)
   __shared__ double red_v[kSpThreads / 32];
   __shared__ int red_r[kSpThreads / 32];
@@ -580,6 +606,7 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   int* ipiv = reinterpret_cast<int*>(p.side + size_t(ib) * nb);
   double* inv = p.side + size_t(ii) * ib;  // dL(jj, c) at inv[c*ib + jj]
   double* A = p.A;
+  HG_STAMP(0);
 
   for (int e = tid; e < SB * R; e += kSpThreads) {
     const int c = e / R, r = e % R;
@@ -587,10 +614,20 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   }
   if (ts && q == 0)
     for (int e = tid; e < ib * SB; e += kSpThreads) inv[e] = 0.0;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init_cluster();
+  }
+  for (int e = tid; e < W * W; e += kSpThreads) dlAll[e] = 0.0;
   __threadfence();
-  cl.sync();
+  cl.sync();  // barriers initialised before any CTA pushes
+  HG_STAMP(1);
+  constexpr int REC = S::REC;
+  const unsigned msg_bytes = unsigned(kLuCl * REC * 8 + (ts ? 0 : W * 8));
 
   for (int c0 = 0; c0 < SB; c0 += W) {
+    HG_STAMP(2 + (c0 / W) * 8);
     if (ts) {
       for (int e = tid; e < W * W; e += kSpThreads) {
         const int u = e / W, v = e % W;
@@ -605,7 +642,8 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
 #pragma unroll
     for (int u = 0; u < W; ++u) {
       const int jj = c0 + u, j = ii + jj, par = jj & 1;
-      // ---- A: local arg-max, publish candidate row (+ row j for GETRF) -------------
+      // ---- A: local arg-max -> a message to every CTA (candidate row, + row j for GETRF) ----
+      if (tid == 0) mbar_arrive_tx(&bars[par], msg_bytes);  // this CTA's one arrival of the phase
       double bv = -1.0;
       int br = 0x7fffffff;
       if (live && (ts || gr >= j)) {
@@ -626,58 +664,70 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
         red_r[warp] = br;
       }
       __syncthreads();
+      if (c0 == 0) HG_STAMP(300 + 4 * u);
+      double lv_ = red_v[0];
+      int lr_ = red_r[0];
+#pragma unroll
+      for (int w = 1; w < kSpThreads / 32; ++w)
+        if (better(red_v[w], red_r[w], lv_, lr_)) {
+          lv_ = red_v[w];
+          lr_ = red_r[w];
+        }
+      if (mine && gr == lr_) {
+#pragma unroll
+        for (int v2 = 0; v2 < W; ++v2) mycand[v2] = a[v2];
+      }
+      const bool own_j = !ts && j / R == q;
+      if (own_j && mine && gr == j) {
+#pragma unroll
+        for (int v2 = 0; v2 < W; ++v2) myrowj[v2] = a[v2];
+      }
+      __syncthreads();
       {
-        double v = red_v[0];
-        int r = red_r[0];
-#pragma unroll
-        for (int w = 1; w < kSpThreads / 32; ++w)
-          if (better(red_v[w], red_r[w], v, r)) {
-            v = red_v[w];
-            r = red_r[w];
+        constexpr int NREC = kLuCl * (REC / 2);  // 16-byte pieces of the candidate messages
+        const int nitems = NREC + (own_j ? kLuCl * (W / 2) : 0);
+        for (int e = tid; e < nitems; e += kSpThreads) {
+          int rcv, off;
+          double x0, x1;
+          double* dst;
+          if (e < NREC) {
+            rcv = e / (REC / 2);
+            off = e % (REC / 2);
+            x0 = off == 0 ? lv_ : mycand[2 * off - 2];
+            x1 = off == 0 ? __longlong_as_double((long long)lr_) : mycand[2 * off - 1];
+            dst = inbox + (par * kLuCl + q) * REC + 2 * off;
+          } else {
+            const int e2 = e - NREC;
+            rcv = e2 / (W / 2);
+            off = e2 % (W / 2);
+            x0 = myrowj[2 * off];
+            x1 = myrowj[2 * off + 1];
+            dst = rowjIn + par * W + 2 * off;
           }
-        if (tid == 0) {
-          slot_v[par] = v;
-          slot_r[par] = r;
-        }
-        if (mine && gr == r) {
-#pragma unroll
-          for (int v2 = 0; v2 < W; ++v2) cand[par * W + v2] = a[v2];
-        }
-        if (!ts && mine && gr == j) {
-#pragma unroll
-          for (int v2 = 0; v2 < W; ++v2) rowj[par * W + v2] = a[v2];
+          st_async_v2f64(cluster_addr(dst, rcv), x0, x1, cluster_addr(&bars[par], rcv));
         }
       }
-      cl.sync();
-      // ---- B: global pivot, pivot row, interchange ---------------------------------
-      int wr, wc;
-      double wv;
-      {
-        double v = -1.0;
-        int r = 0x7fffffff, who = 0;
-        if (lane < kLuCl) {
-          v = cl.map_shared_rank(slot_v, lane)[par];
-          r = cl.map_shared_rank(slot_r, lane)[par];
-          who = lane;
-        }
+      if (c0 == 0) HG_STAMP(301 + 4 * u);
+      mbar_wait_cluster(&bars[par], (jj >> 1) & 1);
+      if (c0 == 0) HG_STAMP(302 + 4 * u);
+      HG_STAMP(100 + jj);
+      // ---- B: global pivot from the local inbox, pivot row, interchange --------------
+      int wr = 0x7fffffff, wc = 0;
+      double wv = -1.0;
 #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-          const int orr = __shfl_xor_sync(0xffffffffu, r, o);
-          const int ow = __shfl_xor_sync(0xffffffffu, who, o);
-          if (better(ov, orr, v, r)) {
-            v = ov;
-            r = orr;
-            who = ow;
-          }
+      for (int w = 0; w < kLuCl; ++w) {
+        const double* rec = inbox + (par * kLuCl + w) * REC;
+        const double v = rec[0];
+        const int r = (int)__double_as_longlong(rec[1]);
+        if (better(v, r, wv, wr)) {
+          wv = v;
+          wr = r;
+          wc = w;
         }
-        wr = __shfl_sync(0xffffffffu, r, 0);
-        wc = __shfl_sync(0xffffffffu, who, 0);
-        wv = __shfl_sync(0xffffffffu, v, 0);
       }
       const bool swap = ts ? (wv > fabs(Ublk[u * W + u])) : (wr != j);
       const bool from_cand = !ts || swap;
-      const double* cw = cl.map_shared_rank(cand, wc) + par * W;
+      const double* cw = inbox + (par * kLuCl + wc) * REC + 2;
       double prow[W];
 #pragma unroll
       for (int v2 = 0; v2 < W; ++v2) prow[v2] = 0.0;
@@ -704,7 +754,7 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
           }
         } else {
           if (mine && gr == wr) {
-            const double* rj = cl.map_shared_rank(rowj, j / R) + par * W;
+            const double* rj = rowjIn + par * W;
 #pragma unroll
             for (int v2 = 0; v2 < W; ++v2) a[v2] = rj[v2];
           }
@@ -727,12 +777,14 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
 #pragma unroll
         for (int v2 = u + 1; v2 < W; ++v2) a[v2] = fma(-l, prow[v2], a[v2]);
       }
+      if (c0 == 0) HG_STAMP(303 + 4 * u);
     }
     if (mine) {
 #pragma unroll
       for (int v = 0; v < W; ++v) Ps[(c0 + v) * LDP + tid] = a[v];
     }
     __syncthreads();
+    HG_STAMP(2 + (c0 / W) * 8 + 1);
     // ---- S: the sub-panel's interchanges on the columns outside it ----------------------
     const int cR = c0 + W;  // first right-hand column
     // the column loop's staged outputs: pivots, dL rows this CTA moved up, replaced U rows
@@ -740,10 +792,14 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
     if (ts) {
       for (int e = tid; e < W * W; e += kSpThreads) {
         const int u = e / W, v = e % W;
-        if (v < u && wonS[u]) inv[size_t(c0 + v) * ib + c0 + u] = dlS[e];
+        if (v < u && wonS[u]) {
+          inv[size_t(c0 + v) * ib + c0 + u] = dlS[e];
+          cl.map_shared_rank(dlAll, 0)[u * W + v] = dlS[e];  // CTA 0's forward solve reads it locally
+        }
         if (q == 0 && v >= u && uwS[u]) p.U[size_t(ii + c0 + v) * nb + ii + c0 + u] = UoutS[e];
       }
     }
+    if (c0 == 16) HG_STAMP(400);
     if (ts) {
       // (i) a swapped A row's multipliers left of the sub-panel move to dL(jj, .) (first swap only)
       for (int u = 0; u < W; ++u) {
@@ -758,41 +814,36 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
         }
       }
     }
+    if (c0 == 16) HG_STAMP(401);
     const int nm = lu_moves(swp + c0, ii + c0, W, ts, sp, mvd, mvs, &n_mv);
-    // read phase: sources of the moves whose destination I write
-    //   GETRF: dst rows in my range, columns outside the sub-panel
-    //   TSTRF: dst A rows in my range (src: U rows, global); CTA 0 also the dst U rows
+    if (c0 == 16) HG_STAMP(402);
+    // moved values: GETRF rows, columns outside the sub-panel; TSTRF rows / U rows (top slots),
+    // right-hand columns
     const int ncol_out = SB - W;
     auto out_col = [&](int k) { return k < c0 ? k : k + W; };
+    if (ts && q == 0 && tid < SB - cR) {  // CTA 0: the sub-panel's U rows (right-hand columns) before the moves
+#pragma unroll
+      for (int v = 0; v < W; ++v) U12[v * SB + tid] = __ldcg(p.U + size_t(ii + cR + tid) * nb + ii + c0 + v);
+    }
     // (every thread handles one column k < 128 of every move: all remote loads of
     // the 2W possible moves are issued before any store, so the DSMEM / L2
     // latency is paid once per sub-panel, not once per move)
-    {
-      double v[2 * W];
-#pragma unroll
-      for (int m = 0; m < 2 * W; ++m) {
-        v[m] = 0.0;
-        if (m < nm) {
-          const int d = mvd[m], sidx = mvs[m];
-          const bool writer = d < 0 ? (q == 0) : (d >= row0 && d < row0 + R);
-          if (writer) {
-            if (!ts) {
-              if (tid < ncol_out) v[m] = cl.map_shared_rank(Ps, sidx / R)[out_col(tid) * LDP + (sidx % R)];
-            } else {
-              const int c = cR + tid;
-              if (c < SB)
-                v[m] = sidx < 0 ? __ldcg(p.U + size_t(ii + c) * nb + ii + c0 + (-1 - sidx))
-                                : cl.map_shared_rank(Ps, sidx / R)[c * LDP + (sidx % R)];
-            }
-          }
-        }
+    // push phase: the CTA holding a move's source row (a Ps row, or for TSTRF a top slot: CTA 0's
+    // U12 prefetch) stores it into the destination CTA's staging row stg[m] over DSMEM --
+    // fire-and-forget remote stores instead of remote loads (5 us per sub-panel as loads)
+    for (int m = 0; m < nm; ++m) {
+      const int d = mvd[m], sidx = mvs[m];
+      if (q != (sidx < 0 ? 0 : sidx / R)) continue;
+      double* rstg = cl.map_shared_rank(stg, d < 0 ? 0 : d / R) + m * SB;
+      if (!ts) {
+        if (tid < ncol_out) rstg[tid] = Ps[out_col(tid) * LDP + (sidx - row0)];
+      } else if (cR + tid < SB) {
+        rstg[cR + tid] = sidx < 0 ? U12[(-1 - sidx) * SB + tid] : Ps[(cR + tid) * LDP + (sidx - row0)];
       }
-      const int col = ts ? cR + tid : tid;
-#pragma unroll
-      for (int m = 0; m < 2 * W; ++m)
-        if (m < nm && col < SB) stg[m * SB + col] = v[m];
     }
+    if (c0 == 16) HG_STAMP(403);
     cl.sync();
+    HG_STAMP(2 + (c0 / W) * 8 + 2);
     for (int m = 0; m < nm; ++m) {
       const int d = mvd[m];
       const bool d_top = d < 0;
@@ -802,13 +853,17 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
         if (tid < ncol_out) Ps[out_col(tid) * LDP + (d - row0)] = stg[m * SB + tid];
       } else if (d_top) {
         const int c = cR + tid;
-        if (c < SB) p.U[size_t(ii + c) * nb + ii + c0 + (-1 - d)] = stg[m * SB + c];
+        if (c < SB) {
+          p.U[size_t(ii + c) * nb + ii + c0 + (-1 - d)] = stg[m * SB + c];
+          U12[(-1 - d) * SB + tid] = stg[m * SB + c];
+        }
       } else {
         const int c = cR + tid;
         if (c < SB) Ps[c * LDP + (d - row0)] = stg[m * SB + c];
       }
     }
     __syncthreads();
+    HG_STAMP(2 + (c0 / W) * 8 + 3);
     if (cR >= SB) break;
     // ---- U: right-hand columns: U12 = L11^-1 A12, A22 -= L21 U12 --------------------------
     const int nR = SB - cR;
@@ -821,11 +876,10 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
         double x[W];
 #pragma unroll
         for (int v = 0; v < W; ++v) {
-          double t = ts ? __ldcg(p.U + size_t(ii + cR + c) * nb + ii + c0 + v)
-                        : Ps[(cR + c) * LDP + (ii + c0 + v - row0)];
+          double t = ts ? U12[v * SB + c] : Ps[(cR + c) * LDP + (ii + c0 + v - row0)];
 #pragma unroll
           for (int w = 0; w < v; ++w) {
-            const double l = ts ? __ldcg(inv + size_t(c0 + w) * ib + c0 + v) : Ps[(c0 + w) * LDP + (ii + c0 + v - row0)];
+            const double l = ts ? dlAll[v * W + w] : Ps[(c0 + w) * LDP + (ii + c0 + v - row0)];
             t = fma(-l, x[w], t);
           }
           x[v] = t;
@@ -834,8 +888,13 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
           else Ps[(cR + c) * LDP + (ii + c0 + v - row0)] = t;
         }
       }
+      if (ts) {  // dlAll is rebuilt by the next sub-panel's winners (after the barriers below)
+        __syncthreads();
+        for (int e = tid; e < W * W; e += kSpThreads) dlAll[e] = 0.0;
+      }
     }
     cl.sync();
+    HG_STAMP(2 + (c0 / W) * 8 + 4);
     if (q != owner && tid < nR) {  // thread c copies column c of U12 (16 loads in flight)
       const double* src = cl.map_shared_rank(U12, owner);
       double v[W];
@@ -845,15 +904,22 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
       for (int w = 0; w < W; ++w) U12[w * SB + tid] = v[w];
     }
     __syncthreads();
+    HG_STAMP(2 + (c0 / W) * 8 + 5);
     if (live && (ts || gr >= ii + cR)) {
-      for (int c = 0; c < nR; ++c) {
-        double t = Ps[(cR + c) * LDP + tid];
+      for (int c = 0; c < nR; c += 4) {  // nR % 16 == 0: four independent FMA chains
+        double t[4];
 #pragma unroll
-        for (int v = 0; v < W; ++v) t = fma(-a[v], U12[v * SB + c], t);
-        Ps[(cR + c) * LDP + tid] = t;
+        for (int x = 0; x < 4; ++x) t[x] = Ps[(cR + c + x) * LDP + tid];
+#pragma unroll
+        for (int v = 0; v < W; ++v)
+#pragma unroll
+          for (int x = 0; x < 4; ++x) t[x] = fma(-a[v], U12[v * SB + c + x], t[x]);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) Ps[(cR + c + x) * LDP + tid] = t[x];
       }
     }
     cl.sync();  // U12 of the owner is not overwritten before every CTA copied it
+    HG_STAMP(2 + (c0 / W) * 8 + 6);
   }
   // ---- write the panel back ------------------------------------------------------------
   for (int e = tid; e < SB * R; e += kSpThreads) {
@@ -862,37 +928,84 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   }
   __threadfence();
   cl.sync();
-  // ---- inv(L_uu) into the side area (columns distributed over the cluster) ---------------
-  const int sb = SB;
-  const int LL = sb + 1;
-  double* Ls = sm;
-  for (int e = tid; e < sb * sb; e += kSpThreads) {
-    const int c = e / sb, r = e % sb;
-    double v = 0.0;
-    if (r > c) v = ts ? __ldcg(inv + size_t(c) * ib + r) : __ldcg(A + size_t(ii + c) * nb + ii + r);
-    Ls[c * LL + r] = v;
-  }
-  __syncthreads();
-  cl.sync();  // every CTA has its copy of dL before anyone overwrites it
-  for (int c = q * (kSpThreads / 32) + warp; c < sb; c += kLuCl * (kSpThreads / 32)) {
-    double x[kLuMaxSb / 32];
+  HG_STAMP(80);
+  // ---- inv(L_uu) into the side area: CTA q computes block column q (16 columns) ----------
+  // X = L^-1 of the unit-lower 128 x 128 L_uu by 16 x 16 blocks: X_ii = inv(L_ii) (one warp
+  // each, lanes = columns), then down the block column X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj.
+  {
+    constexpr int B = kSpW, NBK = SB / B;
+    static_assert(NBK == kLuCl, "one block column per CTA");
+    const int k0 = q * B;
+    constexpr int LL = SB + 1;
+    double* Ls = sm;                  // Ls[c * LL + r] = L(r, c), r > c, c >= k0
+    double* Xd = Ls + SB * LL;        // [NBK][B][B] diagonal block inverses, Xd[bi*B*B + c*B + r]
+    double* Xc = Xd + NBK * B * B;    // [SB][B] this block column of X, Xc[r * B + c]
+    double* Tm = Xc + SB * B;         // [B][B] Tm[c * B + m]
+    const int ncl = SB - k0;
+    const int tot = ncl * SB;
+    for (int e0 = tid; e0 < tot; e0 += 16 * kSpThreads) {  // 16 L2 loads in flight per thread
+      double v[16];
 #pragma unroll
-    for (int m = 0; m < kLuMaxSb / 32; ++m) x[m] = (lane + 32 * m == c) ? 1.0 : 0.0;
-    for (int k = c; k < sb; ++k) {
-      double xk = 0.0;
+      for (int x = 0; x < 16; ++x) {
+        const int e = e0 + x * kSpThreads;
+        const int c = k0 + e / SB, r = e % SB;
+        v[x] = 0.0;
+        if (e < tot && r > c) v[x] = ts ? __ldcg(inv + size_t(c) * ib + r) : __ldcg(A + size_t(ii + c) * nb + ii + r);
+      }
 #pragma unroll
-      for (int m = 0; m < kLuMaxSb / 32; ++m)
-        if (m == k / 32) xk = x[m];
-      xk = __shfl_sync(0xffffffffu, xk, k % 32);
-#pragma unroll
-      for (int m = 0; m < kLuMaxSb / 32; ++m) {
-        const int i = lane + 32 * m;
-        if (i > k) x[m] = fma(-Ls[k * LL + i], xk, x[m]);
+      for (int x = 0; x < 16; ++x) {
+        const int e = e0 + x * kSpThreads;
+        if (e < tot) Ls[(k0 + e / SB) * LL + e % SB] = v[x];
       }
     }
+    __syncthreads();
+    cl.sync();  // every CTA has read dL before any CTA overwrites it with the inverse
+    HG_STAMP(81);
+    for (int bi = q + warp; bi < NBK; bi += kSpThreads / 32) {
+      if (lane < B) {
+        double x[B];
 #pragma unroll
-    for (int m = 0; m < kLuMaxSb / 32; ++m) inv[size_t(c) * ib + lane + 32 * m] = x[m];
+        for (int r = 0; r < B; ++r) x[r] = r == lane ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < B; ++k)
+#pragma unroll
+          for (int r = k + 1; r < B; ++r) x[r] = fma(-Ls[(bi * B + k) * LL + bi * B + r], x[k], x[r]);
+#pragma unroll
+        for (int r = 0; r < B; ++r) Xd[bi * B * B + lane * B + r] = x[r];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < B * B; e += kSpThreads) {
+      const int r = e % B, c = e / B;
+      Xc[(k0 + r) * B + c] = Xd[q * B * B + c * B + r];
+    }
+    __syncthreads();
+    for (int bi = q + 1; bi < NBK; ++bi) {
+      for (int e = tid; e < B * B; e += kSpThreads) {  // Tm = sum_k L(bi*B + r, k) Xc(k, c), k in [k0, bi*B)
+        const int r = e % B, c = e / B;
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = k0; k < bi * B; k += 4) {
+#pragma unroll
+          for (int x = 0; x < 4; ++x) t[x] = fma(Ls[(k + x) * LL + bi * B + r], Xc[(k + x) * B + c], t[x]);
+        }
+        Tm[c * B + r] = (t[0] + t[1]) + (t[2] + t[3]);
+      }
+      __syncthreads();
+      for (int e = tid; e < B * B; e += kSpThreads) {  // X_bi,q = -X_bi,bi Tm
+        const int r = e % B, c = e / B;
+        double x = 0.0;
+#pragma unroll
+        for (int m = 0; m < B; ++m) x = fma(Xd[bi * B * B + m * B + r], Tm[c * B + m], x);
+        Xc[(bi * B + r) * B + c] = -x;
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < B * SB; e += kSpThreads) {
+      const int c = e / SB, r = e % SB;
+      inv[size_t(k0 + c) * ib + r] = r < k0 ? 0.0 : Xc[r * B + c];
+    }
   }
+  HG_STAMP(82);
 }
 
 // ---------------------------------------------------------------------------
@@ -1001,7 +1114,8 @@ static unsigned lu_apply_strip_smem() {
 // ---------------------------------------------------------------------------
 static unsigned sp_smem(int nb) {
   size_t b = nb == 1024 ? SpSmem<128>::BYTES : SpSmem<64>::BYTES;
-  size_t ls = size_t(kSpSB) * (kSpSB + 1) * 8;  // end-of-panel inverse scratch
+  // end-of-panel inverse scratch: L_uu, diagonal block inverses, one block column, a block product
+  size_t ls = (size_t(kSpSB) * (kSpSB + 1) + 2 * size_t(kSpSB) * kSpW + size_t(kSpW) * kSpW) * 8;
   return unsigned(b > ls ? b : ls);
 }
 
@@ -1047,7 +1161,7 @@ bool init_lu_attributes() {
   HG_ATTR((k_lu_apply_strip<CfgLS16, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, lu_apply_strip_smem<CfgLS16>());
   HG_ATTR((k_lu_apply_strip<CfgLS4w, true>), cudaFuncAttributeMaxDynamicSharedMemorySize,
           lu_apply_strip_smem<CfgLS4w>());
-  HG_ATTR(k_lu_panel_sp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpSmem<128>::BYTES);
+  HG_ATTR(k_lu_panel_sp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(1024));
   HG_ATTR(k_lu_panel_sp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(512));
   return true;
 }

@@ -142,5 +142,5 @@ def test_lu_planned_factorization(k, devices):
     x_gpu = LQ.lu_solve(gpu_tiles, gpu_side, lay, rhs)
     x_cpu = LQ.lu_solve(T, side, lay, rhs)
     res = lambda x: np.linalg.norm(A @ x - rhs) / (np.linalg.norm(A, 2) * np.linalg.norm(x))
-    assert res(x_gpu) < 1e-13
+    assert res(x_gpu) <= 1.25 * res(x_cpu) + 1e-14  # no worse than the oracle's backward error
     assert abs(res(x_gpu) - res(x_cpu)) < TOL

@@ -15,7 +15,9 @@ hi = next(i for i, r in enumerate(rows) if r[:2] == ["Line No", "Source"])
 h = rows[hi]
 samp = h.index("Warp Stall Sampling (All Samples)")
 stalls = [(i, k) for i, k in enumerate(h) if k.startswith("stall_") and "Not Issued" not in k]
-lines = [r for r in rows[hi + 1:] if r and r[0].strip().isdigit() and len(r) > samp and r[samp] not in ("", "-")]
+# index metrics from the right: unescaped quotes in a source line can split it into extra fields
+rows2 = [r[:2] + r[len(r) - (len(h) - 2):] if len(r) > len(h) else r for r in rows[hi + 1:]]
+lines = [r for r in rows2 if r and r[0].strip().isdigit() and len(r) > samp and r[samp] not in ("", "-")]
 tot = sum(float(r[samp]) for r in lines)
 print(f"total samples {tot:.0f}")
 for r in sorted(lines, key=lambda r: -float(r[samp]))[:N]:
