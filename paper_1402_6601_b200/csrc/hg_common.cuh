@@ -104,6 +104,24 @@ HG_DEVICE void mbar_wait_cluster(uint64_t* b, unsigned parity) {
 }
 HG_DEVICE void fence_mbar_init_cluster() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
+// Phase timestamps of the panel kernels for tools/panel_stamps.cu (built with -DHG_PANEL_STAMPS;
+// the product build compiles them out): g_panel_stamps[cta][k] = %globaltimer of thread 0 of CTA q.
+#ifdef HG_PANEL_STAMPS
+__device__ unsigned long long g_panel_stamps[8][512];
+#define HG_STAMP(k)                                                  \
+  do {                                                               \
+    if (threadIdx.x == 0) {                                          \
+      unsigned long long t_;                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));         \
+      ::hg::g_panel_stamps[q][(k)] = t_;                             \
+    }                                                                \
+  } while (0)
+#else
+#define HG_STAMP(k) \
+  do {              \
+  } while (0)
+#endif
+
 HG_DEVICE double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -525,24 +525,6 @@ __device__ int lu_moves(const int* steps, int ii, int sb, bool ts, int* sp, int*
 //     right-hand columns get U12 = L11^-1 A12 (owner of the 16 pivot rows /
 //     CTA 0 for TSTRF) and A22 -= L21 U12 (every row, registers x broadcast).
 // Same outputs as k_lu_panel (ipiv, dL, panel values, inv(L_uu) in the side area).
-// Phase timestamps of k_lu_panel_sp for tools/panel_stamps.cu (built with -DHG_PANEL_STAMPS; the
-// product build compiles them out): g_panel_stamps[cta][k] = %globaltimer of thread 0.
-#ifdef HG_PANEL_STAMPS
-__device__ unsigned long long g_panel_stamps[8][512];
-#define HG_STAMP(k)                                                                     \
-  do {                                                                                  \
-    if (threadIdx.x == 0) {                                                             \
-      unsigned long long t_;                                                            \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
-      g_panel_stamps[q][(k)] = t_;                                                      \
-    }                                                                                   \
-  } while (0)
-#else
-#define HG_STAMP(k) \
-  do {              \
-  } while (0)
-#endif
-
 constexpr int kSpW = 16;
 constexpr int kSpThreads = 128;
 constexpr int kSpSB = kLuMaxSb;

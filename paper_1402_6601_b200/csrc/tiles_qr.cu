@@ -130,6 +130,14 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
   double* slot = wv + kQrMaxSb;            // [2][2]: partial norm^2, alpha (owner of row j)
   double* vv = slot + 4;                   // [R]  reflector entries of my rows for column jj
   double* ph = vv + kQrMaxSb;              // [2][sb] half-row partial sums
+  // column jj's outputs (T column, TSQRT R row) staged in CTA jj % 8 and written at the end: a
+  // global store pending at a cluster barrier makes its release fence wait for it
+  double* Tst = ph + 2 * kQrMaxSb;         // [sb / 8][ib]
+  double* Rst = Tst + (kQrMaxSb / kQrCl) * kQrMaxSb;  // [sb / 8][sb]
+  // cross-CTA partials are PUSHED (remote stores before the barrier) into every CTA's local copy,
+  // so nothing is loaded over DSMEM after a barrier (remote loads there cost ~1.5 us per column)
+  double* slotAll = Rst + (kQrMaxSb / kQrCl) * kQrMaxSb;  // [2][kQrCl][2] norm^2 partial, alpha
+  double* pwAll = slotAll + 2 * kQrCl * 2;                // [2][kQrCl][sb] partial x^T [V | A]
   __shared__ double s_red[kQrThreads / 32];
   __shared__ double s_tau, s_beta, s_scal;
   double* T = p.side + size_t(ii) * ib;    // this panel's ib x sb T block (ld = ib)
@@ -143,7 +151,7 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
   __syncthreads();
 
   // partial ||x||^2 of column jj over my rows strictly below the diagonal row
-  auto publish_norm = [&](int jj, int par) {
+  auto publish_norm = [&](int jj, int par, double rpre) {
     const int j = ii + jj;
     double acc = 0.0;
     for (int r = tid; r < R; r += kQrThreads) {
@@ -155,26 +163,29 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     }
     acc = warp_sum(acc);
     if (lane == 0) s_red[warp] = acc;
-    if (ts)
-      for (int c = tid; c < sb; c += kQrThreads) rrow[par * kQrMaxSb + c] = c >= jj ? p.R[size_t(ii + c) * nb + j] : 0.0;
+    if (ts && tid < kQrMaxSb) rrow[par * kQrMaxSb + tid] = rpre;  // R row j, loaded a phase ahead
     __syncthreads();
-    if (tid == 0) {
+    if (tid < kQrCl) {  // thread d sends this CTA's (norm^2 partial, alpha) to CTA d
       double t = 0.0;
       for (int w = 0; w < kQrThreads / 32; ++w) t += s_red[w];
-      slot[par * 2 + 0] = t;
-      slot[par * 2 + 1] = (!ts && j >= row0 && j < row0 + R) ? s[jj * LD + (j - row0)] : 0.0;
+      double* dst = cl.map_shared_rank(slotAll, tid) + (par * kQrCl + q) * 2;
+      dst[0] = t;
+      dst[1] = (!ts && j >= row0 && j < row0 + R) ? s[jj * LD + (j - row0)] : 0.0;
     }
   };
 
-  publish_norm(0, 0);
+  HG_STAMP(0);
+  publish_norm(0, 0, (ts && tid < sb) ? p.R[size_t(ii + tid) * nb + ii] : 0.0);
   for (int jj = 0; jj < sb; ++jj) {
     const int j = ii + jj;
     const int par = jj & 1;
+    if (jj < 16) HG_STAMP(300 + 8 * jj);
     cl.sync();  // barrier 1: norms + alpha of column jj
+    if (jj < 16) HG_STAMP(301 + 8 * jj);
     if (tid < 32) {
       double xn2 = 0.0, al = 0.0;
       if (tid < kQrCl) {
-        const double* sl = cl.map_shared_rank(slot, tid) + par * 2;
+        const double* sl = slotAll + (par * kQrCl + tid) * 2;
         xn2 = sl[0];
         al = sl[1];  // only the owner of row j publishes a non-zero alpha
       }
@@ -183,22 +194,25 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
         xn2 += __shfl_xor_sync(0xffffffffu, xn2, o);
         al += __shfl_xor_sync(0xffffffffu, al, o);
       }
-      if (tid == 0) {
-        double alpha = ts ? rrow[par * kQrMaxSb + jj] : al;
-        double tau = 0.0, beta = alpha, scal = 1.0;
-        if (xn2 != 0.0) {
-          const double xnorm = sqrt(xn2);
-          beta = -copysign(hypot(alpha, xnorm), alpha);
-          tau = (beta - alpha) / beta;
-          scal = 1.0 / (alpha - beta);
-        }
-        s_tau = tau;
-        s_beta = beta;
-        s_scal = scal;
+      // dlarfg: beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha) / beta, x *= 1 / (alpha - beta).
+      // Lanes 0..7 hold the reduced (xn2, alpha); the two divisions run on different lanes, and
+      // sqrt(alpha^2 + xn2) replaces dlapy2's overflow-safe hypot (xn2 is already a sum of squares;
+      // the single-thread hypot + 2 divisions chain cost ~1.5 us per column)
+      const double alpha = ts ? rrow[par * kQrMaxSb + jj] : al;
+      if (xn2 != 0.0) {
+        const double beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+        if (tid == 0) s_tau = (beta - alpha) / beta;
+        if (tid == 1) s_scal = 1.0 / (alpha - beta);
+        if (tid == 2) s_beta = beta;
+      } else if (tid == 0) {
+        s_tau = 0.0;
+        s_beta = alpha;
+        s_scal = 1.0;
       }
     }
     __syncthreads();
     const double tau = s_tau, beta = s_beta, scal = s_scal;
+    if (jj < 16) HG_STAMP(302 + 8 * jj);
     // scale my part of x (the owner of row j stores beta) and stage v for the products
     for (int r = tid; r < R; r += kQrThreads) {
       int gr = row0 + r;
@@ -231,14 +245,27 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
       }
     }
     __syncthreads();
-    for (int c = tid; c < sb; c += kQrThreads) pw[par * kQrMaxSb + c] = ph[c] + ph[kQrMaxSb + c];
+    if (jj < 16) HG_STAMP(303 + 8 * jj);
+    {  // this CTA's partial of column c goes to every CTA: thread (c, half) covers 4 destinations
+      const int c = tid % kQrMaxSb, h = tid / kQrMaxSb;
+      if (c < sb) {
+        const double v = ph[c] + ph[kQrMaxSb + c];
+#pragma unroll
+        for (int d = 0; d < kQrCl / 2; ++d)
+          cl.map_shared_rank(pwAll, h * (kQrCl / 2) + d)[(par * kQrCl + q) * kQrMaxSb + c] = v;
+      }
+    }
     cl.sync();  // barrier 2: partial products
+    if (jj < 16) HG_STAMP(304 + 8 * jj);
+    // R row j+1 for the next column's norm phase, issued now so it lands before barrier 1
+    double rnext = 0.0;
+    if (ts && tid < sb && jj + 1 < sb && tid >= jj + 1) rnext = p.R[size_t(ii + tid) * nb + j + 1];
     for (int c = tid; c < sb; c += kQrThreads) {
       double t = 0.0;
       if (c != jj) {
         double part[kQrCl];
 #pragma unroll
-        for (int c2 = 0; c2 < kQrCl; ++c2) part[c2] = cl.map_shared_rank(pw, c2)[par * kQrMaxSb + c];
+        for (int c2 = 0; c2 < kQrCl; ++c2) part[c2] = pwAll[(par * kQrCl + c2) * kQrMaxSb + c];
 #pragma unroll
         for (int c2 = 0; c2 < kQrCl; ++c2) t += part[c2];
       }
@@ -246,12 +273,14 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
       wv[c] = t;
     }
     __syncthreads();
-    // T column jj (y above the diagonal, tau on it) and the R row (TSQRT)
-    if (q == 0) {
-      for (int c = tid; c < ib; c += kQrThreads) T[size_t(jj) * ib + c] = c < jj ? wv[c] : (c == jj ? tau : 0.0);
+    if (jj < 16) HG_STAMP(305 + 8 * jj);
+    // T column jj (y above the diagonal, tau on it) and the R row (TSQRT), staged in CTA jj % 8
+    if (q == jj % kQrCl) {
+      const int slot = jj / kQrCl;
+      for (int c = tid; c < ib; c += kQrThreads) Tst[slot * kQrMaxSb + c] = c < jj ? wv[c] : (c == jj ? tau : 0.0);
       if (ts)
-        for (int c = jj + tid; c < sb; c += kQrThreads)
-          p.R[size_t(ii + c) * nb + j] = (c == jj) ? beta : rrow[par * kQrMaxSb + c] - tau * wv[c];
+        for (int c = tid; c < sb; c += kQrThreads)
+          Rst[slot * kQrMaxSb + c] = c < jj ? 0.0 : ((c == jj) ? beta : rrow[par * kQrMaxSb + c] - tau * wv[c]);
     }
     // apply H_j to columns (jj, sb) of my rows
     {
@@ -283,9 +312,17 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
       }
     }
     __syncthreads();
-    if (jj + 1 < sb) publish_norm(jj + 1, par ^ 1);
+    if (jj < 16) HG_STAMP(306 + 8 * jj);
+    if (jj + 1 < sb) publish_norm(jj + 1, par ^ 1, rnext);
   }
   __syncthreads();
+  // the staged T columns / R rows of this CTA's columns jj = q, q + 8, ...
+  for (int e = tid; e < (sb / kQrCl) * kQrMaxSb; e += kQrThreads) {
+    const int slot = e / kQrMaxSb, c = e % kQrMaxSb, jj = slot * kQrCl + q;
+    if (jj >= sb) continue;
+    if (c < ib) T[size_t(jj) * ib + c] = Tst[slot * kQrMaxSb + c];
+    if (ts && c >= jj && c < sb) p.R[size_t(ii + c) * nb + ii + jj] = Rst[slot * kQrMaxSb + c];
+  }
   for (int e = tid; e < sb * R; e += kQrThreads) {
     int c = e / R, r = e % R;
     int gr = row0 + r;
@@ -293,8 +330,10 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
   }
   __threadfence();
   cl.sync();
+  HG_STAMP(80);
   if (q != 0) return;
   qr_t_from_y(T, ib, sb, s);
+  HG_STAMP(82);
 }
 
 // ---------------------------------------------------------------------------
@@ -423,7 +462,7 @@ static unsigned qr_panel_smem(int nb, int sb) {
   size_t d = size_t(sb) * (R + 1);
   size_t t = size_t(sb) * (sb + 1) + sb + 7 * 256;
   if (t > d) d = t;
-  d += 8 * kQrMaxSb + 8;
+  d += 8 * kQrMaxSb + 8 + 2 * (kQrMaxSb / kQrCl) * kQrMaxSb + 2 * kQrCl * 2 + 2 * kQrCl * kQrMaxSb;
   return unsigned(d * sizeof(double));
 }
 
