@@ -40,7 +40,11 @@ HG_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(
 // the SM).  fl(c + (-a)) == fl(c - a), so "red(-acc)" is bit-identical to the
 // read-modify-write "c = c - acc" when one thread owns the element.
 HG_DEVICE void red_add_f64(double* p, double v) {
+#ifdef HG_EXP_RED_AS_STORE  // tools/ssssm_ab.cu timing experiment only (wrong results)
+  asm volatile("st.global.cg.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+#else
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+#endif
 }
 
 // ---- mbarrier + bulk-copy (TMA engine, no tensor map) helpers --------------

@@ -1008,10 +1008,10 @@ k_lu_apply_strip(LuApplyParams p) {
   constexpr int RING_T = G::STAGES * G::slab_mmaj(G::BM);  // only A streams (B is resident)
   constexpr int RING_U = GU::STAGES * GU::slab_mmaj(GU::BM);
   constexpr int RING = RING_T > RING_U ? RING_T : RING_U;
-  constexpr int AREA = (RING + BN * kLcLd > kLcMaxMoves * BN) ? RING + BN * kLcLd : kLcMaxMoves * BN;
+  constexpr int AREA = RING + BN * kLcLd;
+  static_assert(RING >= BN * kLcLd, "the pristine top rows fit in the ring");
   extern __shared__ double sm[];
   double* ring = sm;
-  double* mvv = sm;                       // interchange staging (ring and Ts are idle then)
   double* Ts = sm + RING;                 // [BN][kLcLd] top rows after the moves, then top'
   double* Wt = Ts;                        // top' overwrites Ts once the product has read it
   int* mv_dst = reinterpret_cast<int*>(sm + AREA);
@@ -1027,35 +1027,70 @@ k_lu_apply_strip(LuApplyParams p) {
   double* bot = ts ? p.bot : p.top;
   for (int P = p.p0; P < p.p1; ++P) {
     const int ii = P * ib;
+#ifdef HG_EXP_NO_MOVES  // tools/ssssm_ab.cu timing experiment only (wrong results)
+    const int nm = 0;
+#else
     const int nm = lu_moves(ipiv + ii, ii, sb, ts, sp, mv_dst, mv_src, &n_moves);
-    auto at = [&](int code, int c) -> double* {
-      return code >= 0 ? bot + size_t(c) * nb + code : top + size_t(c) * nb + ii + (-1 - code);
-    };
-    // gather every moved value before any is written; 8 loads in flight per thread
-    constexpr int GU_ = 4096 / G::THREADS;  // loads in flight per thread
-    for (int e0 = tid; e0 < nm * BN; e0 += GU_ * G::THREADS) {
-      double v[GU_];
-#pragma unroll
-      for (int u = 0; u < GU_; ++u) {
-        const int e = e0 + u * G::THREADS;
-        v[u] = e < nm * BN ? __ldcg(at(mv_src[e / BN], n0 + e % BN)) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < GU_; ++u) {
-        const int e = e0 + u * G::THREADS;
-        if (e < nm * BN) mvv[e] = v[u];
+#endif
+    // ---- the panel's row interchanges -------------------------------------------------
+    // Each top slot jj (row ii + jj) takes its value from a bot row, another top slot or itself;
+    // each bot row that receives a value receives a (pristine) top slot.  Only the bot side
+    // touches global memory: bot-sourced slots are gathered straight into Ts (L2 loads), the top
+    // rows' final values reach global memory through the top' epilogue below, and the bot rows
+    // that received top slots are stored from a pristine smem copy (Pt) of the top rows.
+    static_assert(G::THREADS == kLuMaxSb, "one thread per top slot");
+    int* slot_src = sp + 3 * kLuMaxSb;      // [sb] >= 0: bot row; < 0: top slot -1-k
+    int* bd_row = slot_src + kLuMaxSb;      // [sb] bot rows that receive a top slot
+    int* bd_slot = bd_row + kLuMaxSb;       // [sb] ... namely this one
+    __shared__ int n_bd;
+    slot_src[tid] = -1 - tid;
+    if (tid == 0) n_bd = 0;
+    __syncthreads();
+    for (int m = tid; m < nm; m += G::THREADS) {
+      const int d = mv_dst[m], s = mv_src[m];
+      // GETRF: rows inside the panel are its top slots; TSTRF: codes are already (bot row | -1-slot)
+      const int dslot = ts ? (d < 0 ? -1 - d : -1) : (d >= ii && d < ii + sb ? d - ii : -1);
+      const int scode = ts ? s : (s >= ii && s < ii + sb ? -1 - (s - ii) : s);
+      if (dslot >= 0) {
+        slot_src[dslot] = scode;
+      } else {
+        const int k = atomicAdd(&n_bd, 1);
+        bd_row[k] = d;
+        bd_slot[k] = -1 - scode;  // a bot row only ever receives a top slot
       }
     }
     __syncthreads();
-    for (int e = tid; e < nm * BN; e += G::THREADS) __stcg(at(mv_dst[e / BN], n0 + e % BN), mvv[e]);
-    __syncthreads();
-    // top rows -> smem with cp.async (16-byte chunks along the contiguous rows)
+    const int nbd = n_bd;
+    double* Pt = ring;  // [BN][kLcLd] pristine top rows (the ring is idle until the top' product)
     for (int e = tid; e < (sb / 2) * BN; e += G::THREADS) {
       const int c = e / (sb / 2), r = (e % (sb / 2)) * 2;
-      cp_async16(Ts + c * kLcLd + r, top + size_t(n0 + c) * nb + ii + r);
+      cp_async16(Pt + c * kLcLd + r, top + size_t(n0 + c) * nb + ii + r);
     }
     cp_async_commit();
+    {
+      const int sc = slot_src[tid];
+      if (sc >= 0) {  // BN loads in flight, one bot row across the strip's columns
+        double v[BN];
+#pragma unroll
+        for (int c = 0; c < BN; ++c) v[c] = __ldcg(bot + size_t(n0 + c) * nb + sc);
+#pragma unroll
+        for (int c = 0; c < BN; ++c) Ts[c * kLcLd + tid] = v[c];
+      }
+    }
     cp_async_wait<0>();
+    __syncthreads();
+    {
+      const int sc = slot_src[tid];
+      if (sc < 0) {
+#pragma unroll 8
+        for (int c = 0; c < BN; ++c) Ts[c * kLcLd + tid] = Pt[c * kLcLd + (-1 - sc)];
+      }
+      if (tid < nbd) {
+        const int r = bd_row[tid], k = bd_slot[tid];
+#pragma unroll 8
+        for (int c = 0; c < BN; ++c) __stcg(bot + size_t(n0 + c) * nb + r, Pt[c * kLcLd + k]);
+      }
+    }
     __syncthreads();
     {  // top' = inv(L_uu) top
       double acc[G::FM][G::FN][2];
@@ -1088,8 +1123,7 @@ static unsigned lu_apply_strip_smem() {
   const size_t ru = size_t(GU::STAGES) * GU::slab_mmaj(GU::BM);
   if (ru > ring) ring = ru;
   size_t d = ring + G::BN * kLcLd;
-  if (d < size_t(kLcMaxMoves) * G::BN) d = size_t(kLcMaxMoves) * G::BN;
-  size_t ints = 2 * kLcMaxMoves + 3 * kLuMaxSb;
+  size_t ints = 2 * kLcMaxMoves + 3 * kLuMaxSb + 3 * kLuMaxSb;  // moves, lu_moves scratch, slot sources
   return unsigned(d * sizeof(double) + ints * sizeof(int));
 }
 

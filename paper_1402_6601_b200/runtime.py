@@ -92,7 +92,8 @@ class ExecReport(SimReport):
     ``transfer_start`` / ``transfer_end`` TraceEvents (sim.py:145-147, 169-188) sorted by
     time.  Extras: ``planned`` (the plan's own SimReport, for planned-vs-measured),
     ``task_seconds[w]`` (sum of task durations on ``w``), ``jobs[j] = (worker, start, end,
-    block, nbytes)`` and ``elapsed_ms`` (CUDA-event time of the graph)."""
+    block, nbytes)`` (a producer-pushed job reports its producer task's window: the tile reached the
+    consumer's slot through that task's epilogue stores) and ``elapsed_ms`` (CUDA-event time of the graph)."""
 
     planned: SimReport = None
     task_seconds: tuple = ()
@@ -255,6 +256,13 @@ class Executor:
         jobs = {}
         for j in range(plan.n_jobs):
             if st[n + j, 0] == 0:
+                # producer-push: no copy node; the tile reached the consumer GPU's slot through the
+                # epilogue stores of the task that wrote the version (its window is the transfer's)
+                v = int(plan.job_version[j])
+                if v < 0 or st[v, 0] == 0 or int(plan.job_src[j]) < 1 or int(plan.job_dst[j]) < 1:
+                    continue
+                jobs[j] = (ncpu + int(plan.job_dst[j]) - 1, float(sec[v, 0]), float(sec[v, 1]),
+                           int(plan.job_block[j]), int(plan.job_bytes[j]))
                 continue
             jobs[j] = (ncpu + int(plan.job_dst[j]) - 1, float(sec[n + j, 0]), float(sec[n + j, 1]),
                        int(plan.job_block[j]), int(plan.job_bytes[j]))
