@@ -124,19 +124,15 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool ts = p.mode == QR_TSQRT;
   double* s = sm;                          // s[c*LD + r]
-  double* pw = s + sb * LD;                // [2][sb] partial x^T [V | A]
-  double* rrow = pw + 2 * kQrMaxSb;        // [2][sb] TSQRT: R row j
+  double* rrow = s + sb * LD;              // [2][sb] TSQRT: R row j
   double* wv = rrow + 2 * kQrMaxSb;        // [sb] reduced w / y
-  double* slot = wv + kQrMaxSb;            // [2][2]: partial norm^2, alpha (owner of row j)
-  double* vv = slot + 4;                   // [R]  reflector entries of my rows for column jj
+  double* vv = wv + kQrMaxSb;              // [R]  reflector entries of my rows for column jj
   double* ph = vv + kQrMaxSb;              // [2][sb] half-row partial sums
-  // column jj's outputs (T column, TSQRT R row) staged in CTA jj % 8 and written at the end: a
-  // global store pending at a cluster barrier makes its release fence wait for it
-  double* Tst = ph + 2 * kQrMaxSb;         // [sb / 8][ib]
-  double* Rst = Tst + (kQrMaxSb / kQrCl) * kQrMaxSb;  // [sb / 8][sb]
   // cross-CTA partials are PUSHED (remote stores before the barrier) into every CTA's local copy,
-  // so nothing is loaded over DSMEM after a barrier (remote loads there cost ~1.5 us per column)
-  double* slotAll = Rst + (kQrMaxSb / kQrCl) * kQrMaxSb;  // [2][kQrCl][2] norm^2 partial, alpha
+  // so nothing is loaded over DSMEM after a barrier (remote loads there cost ~1.5 us per column).
+  // (The footprint stays <= 157 KB so that one 68 KB trailing-update strip CTA co-resides on each
+  // of the cluster's SMs inside the DAG: staging the T columns / R rows too cost 5% of QR C4.)
+  double* slotAll = ph + 2 * kQrMaxSb;    // [2][kQrCl][2] norm^2 partial, alpha
   double* pwAll = slotAll + 2 * kQrCl * 2;                // [2][kQrCl][sb] partial x^T [V | A]
   __shared__ double s_red[kQrThreads / 32];
   __shared__ double s_tau, s_beta, s_scal;
@@ -274,13 +270,12 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     }
     __syncthreads();
     if (jj < 16) HG_STAMP(305 + 8 * jj);
-    // T column jj (y above the diagonal, tau on it) and the R row (TSQRT), staged in CTA jj % 8
+    // T column jj (y above the diagonal, tau on it) and the R row (TSQRT), by CTA jj % 8
     if (q == jj % kQrCl) {
-      const int slot = jj / kQrCl;
-      for (int c = tid; c < ib; c += kQrThreads) Tst[slot * kQrMaxSb + c] = c < jj ? wv[c] : (c == jj ? tau : 0.0);
+      for (int c = tid; c < ib; c += kQrThreads) T[size_t(jj) * ib + c] = c < jj ? wv[c] : (c == jj ? tau : 0.0);
       if (ts)
-        for (int c = tid; c < sb; c += kQrThreads)
-          Rst[slot * kQrMaxSb + c] = c < jj ? 0.0 : ((c == jj) ? beta : rrow[par * kQrMaxSb + c] - tau * wv[c]);
+        for (int c = jj + tid; c < sb; c += kQrThreads)
+          p.R[size_t(ii + c) * nb + j] = (c == jj) ? beta : rrow[par * kQrMaxSb + c] - tau * wv[c];
     }
     // apply H_j to columns (jj, sb) of my rows
     {
@@ -316,13 +311,6 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     if (jj + 1 < sb) publish_norm(jj + 1, par ^ 1, rnext);
   }
   __syncthreads();
-  // the staged T columns / R rows of this CTA's columns jj = q, q + 8, ...
-  for (int e = tid; e < (sb / kQrCl) * kQrMaxSb; e += kQrThreads) {
-    const int slot = e / kQrMaxSb, c = e % kQrMaxSb, jj = slot * kQrCl + q;
-    if (jj >= sb) continue;
-    if (c < ib) T[size_t(jj) * ib + c] = Tst[slot * kQrMaxSb + c];
-    if (ts && c >= jj && c < sb) p.R[size_t(ii + c) * nb + ii + jj] = Rst[slot * kQrMaxSb + c];
-  }
   for (int e = tid; e < sb * R; e += kQrThreads) {
     int c = e / R, r = e % R;
     int gr = row0 + r;
@@ -458,12 +446,12 @@ __global__ void __launch_bounds__(CfgQ::THREADS, CfgQ::THREADS == 128 ? 3 : 2) k
 
 // ---------------------------------------------------------------------------
 static unsigned qr_panel_smem(int nb, int sb) {
+  // the column loop's buffers follow the panel s[sb][R+1]; the end-of-panel T scratch
+  // (qr_t_from_y, CTA 0) reuses the same region once they are dead
   const int R = nb / kQrCl;
-  size_t d = size_t(sb) * (R + 1);
-  size_t t = size_t(sb) * (sb + 1) + sb + 7 * 256;
-  if (t > d) d = t;
-  d += 8 * kQrMaxSb + 8 + 2 * (kQrMaxSb / kQrCl) * kQrMaxSb + 2 * kQrCl * 2 + 2 * kQrCl * kQrMaxSb;
-  return unsigned(d * sizeof(double));
+  const size_t loop = size_t(sb) * (R + 1) + 6 * kQrMaxSb + 2 * kQrCl * 2 + 2 * kQrCl * kQrMaxSb;
+  const size_t t = size_t(sb) * (sb + 1) + sb + 7 * 256;
+  return unsigned((loop > t ? loop : t) * sizeof(double));
 }
 
 template <class CfgQ, class C1 = CfgQ>
