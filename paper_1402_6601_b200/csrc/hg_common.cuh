@@ -111,10 +111,10 @@ HG_DEVICE void fence_mbar_init_cluster() { asm volatile("fence.mbarrier_init.rel
 // Phase timestamps of the panel kernels for tools/panel_stamps.cu (built with -DHG_PANEL_STAMPS;
 // the product build compiles them out): g_panel_stamps[cta][k] = %globaltimer of thread 0 of CTA q.
 #ifdef HG_PANEL_STAMPS
-__device__ unsigned long long g_panel_stamps[8][512];
+__device__ unsigned long long g_panel_stamps[16][512];
 #define HG_STAMP(k)                                                  \
   do {                                                               \
-    if (threadIdx.x == 0) {                                          \
+    if (threadIdx.x == 0 && (q) >= 0) {                              \
       unsigned long long t_;                                         \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));         \
       ::hg::g_panel_stamps[q][(k)] = t_;                             \

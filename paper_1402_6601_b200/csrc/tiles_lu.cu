@@ -295,6 +295,9 @@ struct LuApplyParams {
   double* bot;          // GETRF-type: == top; TSTRF-type: the other tile
   int nb, ib, p0, p1, col0, mode;
   int swap_only;        // 1: row interchanges + inv(L_uu)*top only (the bot update is a separate wide GEMM)
+#ifdef HG_PANEL_STAMPS
+  int stamp;            // tools/ssssm_ab.cu: this task's CTA 0 records phase stamps
+#endif
 };
 
 template <int SB>
@@ -1025,7 +1028,11 @@ k_lu_apply_strip(LuApplyParams p) {
   const int* ipiv = reinterpret_cast<const int*>(p.side + size_t(ib) * nb);
   double* top = p.top;
   double* bot = ts ? p.bot : p.top;
+#ifdef HG_PANEL_STAMPS
+  const int q = blockIdx.x == 0 && p.stamp ? 0 : -1;  // tools/ssssm_ab.cu phase stamps (CTA 0 of one task)
+#endif
   for (int P = p.p0; P < p.p1; ++P) {
+    HG_STAMP(20 + 4 * (P - p.p0));
     const int ii = P * ib;
 #ifdef HG_EXP_NO_MOVES  // tools/ssssm_ab.cu timing experiment only (wrong results)
     const int nm = 0;
@@ -1092,6 +1099,7 @@ k_lu_apply_strip(LuApplyParams p) {
       }
     }
     __syncthreads();
+    HG_STAMP(20 + 4 * (P - p.p0) + 1);
     {  // top' = inv(L_uu) top
       double acc[G::FM][G::FN][2];
       zero_acc<G>(acc);
@@ -1103,6 +1111,7 @@ k_lu_apply_strip(LuApplyParams p) {
       });
     }
     __syncthreads();
+    HG_STAMP(20 + 4 * (P - p.p0) + 2);
     if (!p.swap_only) {
       TileLoader<GU, M_MAJOR, GU::BM> la{p.L + size_t(ii) * nb, nb, 0};
       const int m_mask = ts ? 0 : ii + sb;
@@ -1111,6 +1120,7 @@ k_lu_apply_strip(LuApplyParams p) {
                                                               m_mask);
     }
     __syncthreads();
+    HG_STAMP(20 + 4 * (P - p.p0) + 3);
   }
 }
 

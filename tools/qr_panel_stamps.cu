@@ -48,7 +48,7 @@ int main(int argc, char** argv) {
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
   }
-  unsigned long long st[8][512];
+  unsigned long long st[16][512];
   CK(cudaMemcpyFromSymbol(st, hg::g_panel_stamps, sizeof(st)));
   auto ns = [&](int q, int k) { return (long long)(st[q][k] - st[0][0]); };
   printf("{\"mode\": \"%s\", \"total_us\": %.1f, \"loop_us\": %.1f, \"t_factor_us\": %.1f, \"phases_ns\": [",

@@ -62,6 +62,9 @@ int main() {
         ld.clear();
         if (!hg::build_lu_launches(hg::K_SSSSM, o, ld)) exit(1);
         for (auto& d : ld) {
+#ifdef HG_PANEL_STAMPS
+          reinterpret_cast<hg::LuApplyParams*>(d.params)->stamp = (i == conc / 2 && rep == r - 1);
+#endif
           void* args[1] = {d.params};
           CK(cudaLaunchKernel(d.func, d.grid, d.block, args, d.smem, st[i]));
         }
@@ -86,6 +89,19 @@ int main() {
   float ms;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   const double fl = 2.0 * nb * double(nb) * nb;
-  printf("{\"ssssm_tflops\": %.2f, \"ms\": %.2f}\n", conc * reps * fl / (ms * 1e-3) / 1e12, ms);
+  printf("{\"ssssm_tflops\": %.2f, \"ms\": %.2f", conc * reps * fl / (ms * 1e-3) / 1e12, ms);
+#ifdef HG_PANEL_STAMPS
+  unsigned long long stp[16][512];
+  CK(cudaMemcpyFromSymbol(stp, hg::g_panel_stamps, sizeof(stp)));
+  double mv = 0, tr = 0, up = 0;
+  for (int P = 0; P < 8; ++P) {
+    const int b = 20 + 4 * P;
+    mv += (stp[0][b + 1] - stp[0][b]) * 1e-3;
+    tr += (stp[0][b + 2] - stp[0][b + 1]) * 1e-3;
+    up += ((P < 7 ? stp[0][b + 4] : stp[0][b + 3]) - stp[0][b + 2]) * 1e-3;
+  }
+  printf(", \"cta0_us\": {\"moves\": %.1f, \"trsm\": %.1f, \"update\": %.1f}", mv, tr, up);
+#endif
+  printf("}\n");
   return 0;
 }
