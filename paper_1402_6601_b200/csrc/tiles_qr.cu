@@ -136,6 +136,9 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
   double* pwAll = slotAll + 2 * kQrCl * 2;                // [2][kQrCl][sb] partial x^T [V | A]
   __shared__ double s_red[kQrThreads / 32];
   __shared__ double s_tau, s_beta, s_scal;
+  // the two per-column exchanges are st.async messages completing on the receiver's mbarriers
+  // (by column parity): bars[par] the (norm^2, alpha) messages, bars[2 + par] the partials
+  __shared__ __align__(8) uint64_t bars[4];
   double* T = p.side + size_t(ii) * ib;    // this panel's ib x sb T block (ld = ib)
   double* A = p.A;
 
@@ -144,7 +147,11 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     int gr = row0 + r;
     s[c * LD + r] = (ts || gr >= ii) ? A[size_t(ii + c) * nb + gr] : 0.0;
   }
-  __syncthreads();
+  if (tid == 0) {
+    for (int b = 0; b < 4; ++b) mbar_init(&bars[b], 1);
+    fence_mbar_init_cluster();
+  }
+  cl.sync();  // every CTA's barriers exist before the first message
 
   // partial ||x||^2 of column jj over my rows strictly below the diagonal row
   auto publish_norm = [&](int jj, int par, double rpre) {
@@ -160,13 +167,13 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     acc = warp_sum(acc);
     if (lane == 0) s_red[warp] = acc;
     if (ts && tid < kQrMaxSb) rrow[par * kQrMaxSb + tid] = rpre;  // R row j, loaded a phase ahead
+    if (tid == 0) mbar_arrive_tx(&bars[par], kQrCl * 16);     // this CTA's arrival for column jj
     __syncthreads();
     if (tid < kQrCl) {  // thread d sends this CTA's (norm^2 partial, alpha) to CTA d
       double t = 0.0;
       for (int w = 0; w < kQrThreads / 32; ++w) t += s_red[w];
-      double* dst = cl.map_shared_rank(slotAll, tid) + (par * kQrCl + q) * 2;
-      dst[0] = t;
-      dst[1] = (!ts && j >= row0 && j < row0 + R) ? s[jj * LD + (j - row0)] : 0.0;
+      const double al = (!ts && j >= row0 && j < row0 + R) ? s[jj * LD + (j - row0)] : 0.0;
+      st_async_v2f64(cluster_addr(slotAll + (par * kQrCl + q) * 2, tid), t, al, cluster_addr(&bars[par], tid));
     }
   };
 
@@ -176,9 +183,9 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     const int j = ii + jj;
     const int par = jj & 1;
     if (jj < 16) HG_STAMP(300 + 8 * jj);
-    cl.sync();  // barrier 1: norms + alpha of column jj
     if (jj < 16) HG_STAMP(301 + 8 * jj);
     if (tid < 32) {
+      mbar_wait_cluster(&bars[par], (jj >> 1) & 1);  // the 8 (norm^2, alpha) messages of column jj
       double xn2 = 0.0, al = 0.0;
       if (tid < kQrCl) {
         const double* sl = slotAll + (par * kQrCl + tid) * 2;
@@ -242,16 +249,20 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     }
     __syncthreads();
     if (jj < 16) HG_STAMP(303 + 8 * jj);
+    if (tid == 0) mbar_arrive_tx(&bars[2 + par], unsigned(kQrCl * sb * 8));
     {  // this CTA's partial of column c goes to every CTA: thread (c, half) covers 4 destinations
       const int c = tid % kQrMaxSb, h = tid / kQrMaxSb;
       if (c < sb) {
         const double v = ph[c] + ph[kQrMaxSb + c];
 #pragma unroll
-        for (int d = 0; d < kQrCl / 2; ++d)
-          cl.map_shared_rank(pwAll, h * (kQrCl / 2) + d)[(par * kQrCl + q) * kQrMaxSb + c] = v;
+        for (int d = 0; d < kQrCl / 2; ++d) {
+          const int dst = h * (kQrCl / 2) + d;
+          st_async_f64(cluster_addr(pwAll + (par * kQrCl + q) * kQrMaxSb + c, dst), v,
+                       cluster_addr(&bars[2 + par], dst));
+        }
       }
     }
-    cl.sync();  // barrier 2: partial products
+    mbar_wait_cluster(&bars[2 + par], (jj >> 1) & 1);  // the 8 partials of every column
     if (jj < 16) HG_STAMP(304 + 8 * jj);
     // R row j+1 for the next column's norm phase, issued now so it lands before barrier 1
     double rnext = 0.0;
