@@ -177,15 +177,17 @@ class Executor:
         priority_levels = int(os.environ.get("HG_PRIORITY_LEVELS", priority_levels))
         self.task_weight = np.ascontiguousarray(np.asarray(plan.end, np.float64) - np.asarray(plan.start, np.float64))
         # host-staged routes (p2p=False, platform.py:117): GPU->host->GPU moves stage through
-        # a pinned image with the host image's layout
+        # a page-locked image with the host image's layout (hg_matrix_register, released by close)
         self.p2p = bool(platform.p2p) or k == 1
         self.host_stage = None
+        self._stage_registered = False
         if not self.p2p:
-            import torch
-
             tile = lay.b * lay.b
             n_stage = sum(sz // 8 + (lay.side_doubles if sz // 8 == tile else 0) for sz in graph.sizes)
-            self.host_stage = torch.empty(n_stage, dtype=torch.float64).pin_memory().numpy()
+            self.host_stage = np.zeros(n_stage, np.float64)
+            _native.check(L.hg_matrix_register(C.c_void_p(self.host_stage.ctypes.data), self.host_stage.nbytes),
+                          "hg_matrix_register (staging image)")
+            self._stage_registered = True
         self._keep = [fl, kind_map]
         ep = ExecPlan_from(plan, n, len(graph.data), k, lay, self, fl)
         opts = _native.ExecOpts(
@@ -297,6 +299,9 @@ class Executor:
         if getattr(self, "_h", None):
             _native.lib().hg_exec_destroy(self._h)
             self._h = None
+        if getattr(self, "_stage_registered", False):
+            _native.lib().hg_matrix_unregister(C.c_void_p(self.host_stage.ctypes.data))
+            self._stage_registered = False
 
     def __del__(self):
         try:
