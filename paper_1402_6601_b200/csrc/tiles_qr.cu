@@ -379,6 +379,9 @@ struct QrApplyParams {
   double* top;         // UNMQR: the tile C (rows [ii, nb)); TSMQR: A_kj (rows [ii, ii+sb))
   double* bot;         // TSMQR: A_ij; UNMQR: unused
   int nb, ib, p0, p1, col0, mode;
+#ifdef HG_PANEL_STAMPS
+  int stamp;           // tools/ssssm_ab.cu (q mode): this task's CTA 0 records phase stamps
+#endif
 };
 
 // Column-strip variant: one CTA per BN-column strip (no cluster, all rows),
@@ -405,9 +408,13 @@ __global__ void __launch_bounds__(CfgQ::THREADS, CfgQ::THREADS == 128 ? 3 : 2) k
   const int nb = p.nb, ib = p.ib;
   const int n0 = p.col0 + blockIdx.x * kQrBN;
   const bool ts = p.mode == QR_TSQRT;
+#ifdef HG_PANEL_STAMPS
+  const int q = blockIdx.x == 0 && p.stamp ? 0 : -1;
+#endif
   for (int P = p.p0; P < p.p1; ++P) {
     const int ii = P * ib;
     const double* Vp = p.V + size_t(ii) * nb;  // V(tr, pc) at Vp[pc*nb + tr]
+    HG_STAMP(20 + 4 * (P - p.p0));
     // ---- W = V^T C   (UNMQR, K over tile rows [ii, nb))  |  top + V_B^T bot (TSMQR)
     {
       double acc[C1::FM][C1::FN][2];
@@ -435,6 +442,7 @@ __global__ void __launch_bounds__(CfgQ::THREADS, CfgQ::THREADS == 128 ? 3 : 2) k
       for_each_acc<C1>(acc, [&](int r, int c, double v) { W[c * kWld + r] = v; });
     }
     __syncthreads();
+    HG_STAMP(20 + 4 * (P - p.p0) + 1);
     // ---- W <- T^T W  (T^T(r, k) = T(k, r) at side[(ii + r)*ib + k])
     {
       double acc[C1::FM][C1::FN][2];
@@ -445,6 +453,7 @@ __global__ void __launch_bounds__(CfgQ::THREADS, CfgQ::THREADS == 128 ? 3 : 2) k
       if (ts) sub_store<C1>(acc, p.top + ii, nb, 0, n0);  // top -= W (all loads first)
     }
     __syncthreads();
+    HG_STAMP(20 + 4 * (P - p.p0) + 2);
     // ---- C -= V W  (UNMQR rows [ii, nb))  |  bot -= V_B W (TSMQR)
     {
       VLoader<CfgQ, M_MAJOR, 128> la{Vp, nb, 0, ii, ts ? 0 : 1};
@@ -452,6 +461,7 @@ __global__ void __launch_bounds__(CfgQ::THREADS, CfgQ::THREADS == 128 ? 3 : 2) k
                                                                   ts ? p.bot : p.top, nb, n0);
     }
     __syncthreads();
+    HG_STAMP(20 + 4 * (P - p.p0) + 3);
   }
 }
 

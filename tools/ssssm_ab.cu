@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../paper_1402_6601_b200/csrc/tiles_lu.cu"
+#include "../paper_1402_6601_b200/csrc/tiles_qr.cu"
 
 namespace hg {
 void set_error(const char* fmt, ...) {
@@ -26,10 +27,11 @@ void set_error(const char* fmt, ...) {
     }                                                                            \
   } while (0)
 
-int main() {
+int main(int argc, char** argv) {
+  const bool qr = argc > 1 && argv[1][0] == 'q';  // TSMQR instead of SSSSM
   const int nb = 1024, ib = 128, conc = 32, reps = 5;
   const size_t tile = size_t(nb) * nb, slot = tile + size_t(ib) * nb + nb;
-  if (!hg::init_lu_attributes()) return 1;
+  if (!hg::init_lu_attributes() || !hg::init_qr_attributes()) return 1;
   std::vector<double> h(slot);
   srand(3);
   std::vector<double*> L(conc), T(conc), B(conc);
@@ -60,10 +62,11 @@ int main() {
         o.t[2] = B[i];
         o.n_t = 3;
         ld.clear();
-        if (!hg::build_lu_launches(hg::K_SSSSM, o, ld)) exit(1);
+        if (!(qr ? hg::build_qr_launches(hg::K_TSMQR, o, ld) : hg::build_lu_launches(hg::K_SSSSM, o, ld))) exit(1);
         for (auto& d : ld) {
 #ifdef HG_PANEL_STAMPS
-          reinterpret_cast<hg::LuApplyParams*>(d.params)->stamp = (i == conc / 2 && rep == r - 1);
+          if (qr) reinterpret_cast<hg::QrApplyParams*>(d.params)->stamp = (i == conc / 2 && rep == r - 1);
+          else reinterpret_cast<hg::LuApplyParams*>(d.params)->stamp = (i == conc / 2 && rep == r - 1);
 #endif
           void* args[1] = {d.params};
           CK(cudaLaunchKernel(d.func, d.grid, d.block, args, d.smem, st[i]));
@@ -88,8 +91,8 @@ int main() {
   CK(cudaEventSynchronize(e1));
   float ms;
   CK(cudaEventElapsedTime(&ms, e0, e1));
-  const double fl = 2.0 * nb * double(nb) * nb;
-  printf("{\"ssssm_tflops\": %.2f, \"ms\": %.2f", conc * reps * fl / (ms * 1e-3) / 1e12, ms);
+  const double fl = (qr ? 4.0 : 2.0) * nb * double(nb) * nb;
+  printf("{\"kind\": \"%s\", \"tflops\": %.2f, \"ms\": %.2f", qr ? "TSMQR" : "SSSSM", conc * reps * fl / (ms * 1e-3) / 1e12, ms);
 #ifdef HG_PANEL_STAMPS
   unsigned long long stp[16][512];
   CK(cudaMemcpyFromSymbol(stp, hg::g_panel_stamps, sizeof(stp)));
@@ -100,7 +103,8 @@ int main() {
     tr += (stp[0][b + 2] - stp[0][b + 1]) * 1e-3;
     up += ((P < 7 ? stp[0][b + 4] : stp[0][b + 3]) - stp[0][b + 2]) * 1e-3;
   }
-  printf(", \"cta0_us\": {\"moves\": %.1f, \"trsm\": %.1f, \"update\": %.1f}", mv, tr, up);
+  printf(qr ? ", \"cta0_us\": {\"W=top+VtB\": %.1f, \"TtW\": %.1f, \"update\": %.1f}"
+            : ", \"cta0_us\": {\"moves\": %.1f, \"trsm\": %.1f, \"update\": %.1f}", mv, tr, up);
 #endif
   printf("}\n");
   return 0;
