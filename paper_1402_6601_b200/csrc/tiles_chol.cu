@@ -901,8 +901,13 @@ static unsigned trsm_smem() { return (unsigned)GemmSmem<CfgG, M_MAJOR, K_MAJOR>:
 bool init_chol_attributes() {
   HG_ATTR((k_gemm_nt<CfgG4, 3>), cudaFuncAttributeMaxDynamicSharedMemorySize,
           (int)(GemmSmem<CfgG4, M_MAJOR, M_MAJOR>::BYTES));
+  HG_ATTR(k_trsm_inv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
   HG_ATTR(k_trsm_inv<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
+  HG_ATTR(k_trsm_inv<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
   HG_ATTR(k_trsm_inv<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
+  HG_ATTR(k_trsm_inv<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
+  HG_ATTR(k_trsm_inv<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
+  HG_ATTR(k_trsm_inv<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
   HG_ATTR(k_trsm_inv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem());
   HG_ATTR(k_potrf_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPotrfDynDoubles * sizeof(double)));
   HG_ATTR(k_potrf_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -941,14 +946,19 @@ bool build_chol_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc
       return true;
     }
     case K_TRSM: {
-      const int P = nJ / 2;  // CTAs per row strip = cluster size
-      if (nJ % 2 || (P != 2 && P != 4 && P != 8)) {
-        set_error("TRSM needs nb in {256, 512, 1024} (nb=%d)", nb);
+      const int P = nJ / 2;  // CTAs per row strip = cluster size (portable: <= 8)
+      if (nJ % 2 || P < 1 || P > 8) {
+        set_error("TRSM needs nb a multiple of %d up to 1024 (nb=%d)", 2 * kR, nb);
         return false;
       }
       LaunchDesc d;
       TrsmInvParams tp{o.t[0], o.t[1], o.scratch, nb, o.push};
-      const void* f = P == 8 ? (const void*)k_trsm_inv<8> : (P == 4 ? (const void*)k_trsm_inv<4> : (const void*)k_trsm_inv<2>);
+      static const void* const kTrsm[9] = {nullptr,
+                                           (const void*)k_trsm_inv<1>, (const void*)k_trsm_inv<2>,
+                                           (const void*)k_trsm_inv<3>, (const void*)k_trsm_inv<4>,
+                                           (const void*)k_trsm_inv<5>, (const void*)k_trsm_inv<6>,
+                                           (const void*)k_trsm_inv<7>, (const void*)k_trsm_inv<8>};
+      const void* f = kTrsm[P];
       d.set(f, dim3(nJ * P), dim3(CfgG::THREADS), trsm_smem(), tp);
       out.push_back(d);
       return true;

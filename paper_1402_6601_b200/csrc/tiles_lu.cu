@@ -1139,7 +1139,10 @@ static unsigned lu_apply_strip_smem() {
 
 // ---------------------------------------------------------------------------
 static unsigned sp_smem(int nb) {
-  size_t b = nb == 1024 ? SpSmem<128>::BYTES : SpSmem<64>::BYTES;
+  size_t b = nb == 1024 ? SpSmem<128>::BYTES
+             : nb == 768 ? SpSmem<96>::BYTES
+             : nb == 512 ? SpSmem<64>::BYTES
+                         : SpSmem<32>::BYTES;
   // end-of-panel inverse scratch: L_uu, diagonal block inverses, one block column, a block product
   size_t ls = (size_t(kSpSB) * (kSpSB + 1) + 2 * size_t(kSpSB) * kSpW + size_t(kSpW) * kSpW) * 8;
   return unsigned(b > ls ? b : ls);
@@ -1152,11 +1155,16 @@ static unsigned panel_smem(int nb, int sb) {
   return unsigned((bufs > inv ? bufs : inv) * sizeof(double));
 }
 
-// ib = 128: the sub-panel kernel; ib = 64: the register-resident full-width panel kernel
-static bool use_sp_panel(int nb, int ib) { return ib == kSpSB && (nb == 1024 || nb == 512); }
+// ib = 128: the sub-panel kernel (nb in {256, 512, 768, 1024}: nb / 8 rows per CTA); ib = 64: the
+// register-resident full-width panel kernel (nb in {512, 1024})
+static bool use_sp_panel(int nb, int ib) { return ib == kSpSB && (nb == 1024 || nb == 768 || nb == 512 || nb == 256); }
 
 static const void* panel_kernel(int nb, int ib) {
-  if (use_sp_panel(nb, ib)) return nb == 1024 ? (const void*)k_lu_panel_sp<128> : (const void*)k_lu_panel_sp<64>;
+  if (use_sp_panel(nb, ib))
+    return nb == 1024 ? (const void*)k_lu_panel_sp<128>
+           : nb == 768 ? (const void*)k_lu_panel_sp<96>
+           : nb == 512 ? (const void*)k_lu_panel_sp<64>
+                       : (const void*)k_lu_panel_sp<32>;
   if (nb == 1024 && ib == 64) return (const void*)k_lu_panel<128, 64>;
   if (nb == 512 && ib == 64) return (const void*)k_lu_panel<64, 64>;
   return nullptr;
@@ -1189,6 +1197,8 @@ bool init_lu_attributes() {
           lu_apply_strip_smem<CfgLS4w>());
   HG_ATTR(k_lu_panel_sp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(1024));
   HG_ATTR(k_lu_panel_sp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(512));
+  HG_ATTR(k_lu_panel_sp<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(768));
+  HG_ATTR(k_lu_panel_sp<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_smem(256));
   return true;
 }
 
@@ -1202,7 +1212,7 @@ static void push_apply(std::vector<LaunchDesc>& out, const LuApplyParams& ap) { 
 
 // ib = 128: every panel application is the strip kernel (one CTA per 16 / 32-column strip,
 // L2-reduction update).  ib = 64: narrow swap + inv(L_uu) kernel, then a wide GEMM.
-static bool use_strip_apply(int nb, int ib) { return ib == kLuMaxSb && nb % 512 == 0; }
+static bool use_strip_apply(int nb, int ib) { return ib == kLuMaxSb && nb % 128 == 0; }
 
 // Panels [P0, P1) applied to columns [col0, nb) by the strip kernel.
 static void push_apply_strip(std::vector<LaunchDesc>& out, const double* L, const double* side, double* top,
@@ -1240,8 +1250,9 @@ static void push_panel_apply(std::vector<LaunchDesc>& out, int ib, const double*
 
 bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out) {
   const int nb = o.nb, ib = o.ib;
-  if ((nb != 512 && nb != 1024) || (ib != 64 && ib != 128)) {
-    set_error("LU tile kernels need nb in {512, 1024} and ib in {64, 128}; got nb=%d ib=%d", nb, ib);
+  if (!(ib == 128 && use_sp_panel(nb, ib)) && !(ib == 64 && (nb == 512 || nb == 1024))) {
+    set_error("LU tile kernels need ib = 128 with nb in {256, 512, 768, 1024}, or ib = 64 with nb in {512, 1024}; "
+              "got nb=%d ib=%d", nb, ib);
     return false;
   }
   const size_t tile = size_t(nb) * nb;
