@@ -536,14 +536,13 @@ template <int R>
 struct SpSmem {
   static constexpr int LDP = R + 1;
   static constexpr int PS = kSpSB * LDP;                  // panel [col][row]
-  static constexpr int STG = 2 * kSpW * kSpSB;            // phase-S staging rows
-  static constexpr int U12 = kSpW * kSpSB;                // [v][col]
+  static constexpr int U12 = kSpW * kSpSB;                // [v][col] (the sub-panel's U block Ublk in the column loop)
   static constexpr int REC = 2 + kSpW;                    // column message: (value, row), candidate row
   static constexpr int INBOX = 2 * kLuCl * REC;           // [parity][sender] messages
-  static constexpr int MISC = INBOX + 2 * kSpW + 2 * kSpW + 2 + 4 * kSpW * kSpW;
-  // inbox, rowjIn[2][W], mycand/myrowj, 2 mbarriers, Ublk, dlS, UoutS
-  static constexpr int DOUBLES = PS + STG + U12 + MISC;
-  static constexpr int INTS = kSpSB + 4 * kSpW + 3 * kSpW + 4 + 2 * kSpW;
+  static constexpr int MISC = INBOX + 2 * kSpW + 2 * kSpW + 2 + kSpW * kSpW;
+  // inbox, rowjIn[2][W], mycand/myrowj, 2 mbarriers, dlAll
+  static constexpr int DOUBLES = PS + U12 + MISC;
+  static constexpr int INTS = kSpSB + 4 * kSpW + 3 * kSpW;
   static constexpr size_t BYTES = size_t(DOUBLES) * 8 + size_t(INTS) * 4;
 };
 
@@ -562,9 +561,11 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   const bool mine = tid < R;
   const int gr = row0 + tid;
   const bool live = mine && (ts || gr >= ii);
+  // Footprint <= 151 KB (nb = 1024) so that one 71 KB trailing-update strip CTA co-resides on each
+  // of the cluster's SMs inside the DAG: no phase-S staging rows (moves go register -> remote Ps),
+  // the sub-panel's U block lives in U12's space during the column loop.
   double* Ps = sm;
-  double* stg = Ps + S::PS;
-  double* U12 = stg + S::STG;
+  double* U12 = Ps + S::PS;
   // per-column messages: every CTA pushes (local best |value|, its row, that row's W sub-panel
   // values) into every CTA's inbox with st.async, completing on the receiver's mbarrier -- no
   // cluster barrier per column.  GETRF: the owner of row j also pushes row j (rowjIn).
@@ -573,18 +574,12 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   double* mycand = rowjIn + 2 * W;      // [W] staging of this CTA's candidate row
   double* myrowj = mycand + W;          // [W] staging of row j (its owner)
   uint64_t* bars = reinterpret_cast<uint64_t*>(myrowj + W);  // [2] by column parity
-  double* Ublk = myrowj + W + 2;        // [W][W]
-  // TSTRF outputs of the column loop, staged in smem and written to global memory once per
-  // sub-panel: a global store pending at a cluster barrier makes its release fence wait for it
-  double* dlS = Ublk + W * W;           // [W][W] dL(c0 + u, c0 + v), v < u, of rows this CTA won
-  double* UoutS = dlS + W * W;          // [W][W] U row c0 + u, columns c0 + v >= u (CTA 0)
-  double* dlAll = UoutS + W * W;        // [W][W] CTA 0: the sub-panel's whole dL block (forward solve)
+  double* Ublk = U12;                   // [W][W] during the column loop (U12 is idle then)
+  double* dlAll = myrowj + W + 2;       // [W][W] CTA 0: the sub-panel's whole dL block (forward solve)
   int* swp = reinterpret_cast<int*>(sm + S::DOUBLES);  // [SB]
   int* mvd = swp + SB;                  // [2W]
   int* mvs = mvd + 2 * W;               // [2W]
   int* sp = mvs + 2 * W;                // [3W]
-  int* wonS = sp + 3 * W;               // [W] this CTA's row moved up at step u (dlS row valid)
-  int* uwS = wonS + W;                  // [W] U row c0 + u replaced at step u (UoutS row valid)
   __shared__ double red_v[kSpThreads / 32];
   __shared__ int red_r[kSpThreads / 32];
   __shared__ int n_mv;
@@ -613,12 +608,19 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
 
   for (int c0 = 0; c0 < SB; c0 += W) {
     HG_STAMP(2 + (c0 / W) * 8);
+    // TSTRF, CTA 0: the sub-panel's U rows right of it, loaded now (the column loop never touches
+    // them) and parked in U12 for the moves -- the L2 latency hides behind the column loop
+    double upre[W];
+    const bool pre = ts && q == 0 && tid < SB - (c0 + W);
+    if (pre) {
+#pragma unroll
+      for (int v = 0; v < W; ++v) upre[v] = __ldcg(p.U + size_t(ii + c0 + W + tid) * nb + ii + c0 + v);
+    }
     if (ts) {
       for (int e = tid; e < W * W; e += kSpThreads) {
         const int u = e / W, v = e % W;
         Ublk[e] = v >= u ? __ldcg(p.U + size_t(ii + c0 + v) * nb + ii + c0 + u) : 0.0;
       }
-      if (tid < W) wonS[tid] = uwS[tid] = 0;
     }
     double a[W];
 #pragma unroll
@@ -722,21 +724,20 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
       if (swap) {
         if (ts) {
           if (mine && gr == wr) {
-            wonS[u] = 1;
+            double* dl0 = cl.map_shared_rank(dlAll, 0) + u * W;  // CTA 0's forward solve reads it locally
 #pragma unroll
             for (int v2 = 0; v2 < W; ++v2) {
               if (v2 < u) {
-                dlS[u * W + v2] = a[v2];  // dL(jj, c0 + v2), written out after the sub-panel
+                inv[size_t(c0 + v2) * ib + jj] = a[v2];  // dL(jj, c0 + v2)
+                dl0[v2] = a[v2];
                 a[v2] = 0.0;
               } else {
                 a[v2] = Ublk[u * W + v2];
               }
             }
           }
-          if (q == 0 && tid >= u && tid < W) {
-            UoutS[u * W + tid] = cw[tid];
-            if (tid == u) uwS[u] = 1;
-          }
+          // (no cluster barrier in the column loop: these global stores delay nothing)
+          if (q == 0 && tid >= u && tid < W) p.U[size_t(ii + c0 + tid) * nb + j] = cw[tid];
         } else {
           if (mine && gr == wr) {
             const double* rj = rowjIn + par * W;
@@ -772,18 +773,7 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
     HG_STAMP(2 + (c0 / W) * 8 + 1);
     // ---- S: the sub-panel's interchanges on the columns outside it ----------------------
     const int cR = c0 + W;  // first right-hand column
-    // the column loop's staged outputs: pivots, dL rows this CTA moved up, replaced U rows
     if (q == 0 && tid < W) ipiv[ii + c0 + tid] = swp[c0 + tid];
-    if (ts) {
-      for (int e = tid; e < W * W; e += kSpThreads) {
-        const int u = e / W, v = e % W;
-        if (v < u && wonS[u]) {
-          inv[size_t(c0 + v) * ib + c0 + u] = dlS[e];
-          cl.map_shared_rank(dlAll, 0)[u * W + v] = dlS[e];  // CTA 0's forward solve reads it locally
-        }
-        if (q == 0 && v >= u && uwS[u]) p.U[size_t(ii + c0 + v) * nb + ii + c0 + u] = UoutS[e];
-      }
-    }
     if (c0 == 16) HG_STAMP(400);
     if (ts) {
       // (i) a swapped A row's multipliers left of the sub-panel move to dL(jj, .) (first swap only)
@@ -806,47 +796,42 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
     // right-hand columns
     const int ncol_out = SB - W;
     auto out_col = [&](int k) { return k < c0 ? k : k + W; };
-    if (ts && q == 0 && tid < SB - cR) {  // CTA 0: the sub-panel's U rows (right-hand columns) before the moves
+    if (pre) {  // CTA 0: the sub-panel's U rows (right-hand columns) before the moves
 #pragma unroll
-      for (int v = 0; v < W; ++v) U12[v * SB + tid] = __ldcg(p.U + size_t(ii + cR + tid) * nb + ii + c0 + v);
+      for (int v = 0; v < W; ++v) U12[v * SB + tid] = upre[v];
     }
-    // (every thread handles one column k < 128 of every move: all remote loads of
-    // the 2W possible moves are issued before any store, so the DSMEM / L2
-    // latency is paid once per sub-panel, not once per move)
-    // push phase: the CTA holding a move's source row (a Ps row, or for TSTRF a top slot: CTA 0's
-    // U12 prefetch) stores it into the destination CTA's staging row stg[m] over DSMEM --
-    // fire-and-forget remote stores instead of remote loads (5 us per sub-panel as loads)
-    for (int m = 0; m < nm; ++m) {
-      const int d = mvd[m], sidx = mvs[m];
-      if (q != (sidx < 0 ? 0 : sidx / R)) continue;
-      double* rstg = cl.map_shared_rank(stg, d < 0 ? 0 : d / R) + m * SB;
-      if (!ts) {
-        if (tid < ncol_out) rstg[tid] = Ps[out_col(tid) * LDP + (sidx - row0)];
-      } else if (cR + tid < SB) {
-        rstg[cR + tid] = sidx < 0 ? U12[(-1 - sidx) * SB + tid] : Ps[(cR + tid) * LDP + (sidx - row0)];
+    // Moves in two steps separated by a cluster barrier: the CTA holding a move's source (a Ps
+    // row, or for TSTRF a top slot: CTA 0's U12 prefetch) reads it into registers; after the
+    // barrier it stores it straight into the destination (a Ps row of its owner over DSMEM, or a
+    // U row: CTA 0's U12).  Remote stores, no remote loads, no staging rows.
+    const int mcol = ts ? cR + tid : (tid < ncol_out ? out_col(tid) : -1);  // this thread's column
+    const bool colok = ts ? (cR + tid < SB) : (tid < ncol_out);
+    double mv[2 * W];
+#pragma unroll
+    for (int m = 0; m < 2 * W; ++m) {
+      mv[m] = 0.0;
+      if (m < nm && colok) {
+        const int sidx = mvs[m];
+        if (q == (sidx < 0 ? 0 : sidx / R)) mv[m] = sidx < 0 ? U12[(-1 - sidx) * SB + tid] : Ps[mcol * LDP + (sidx - row0)];
       }
     }
     if (c0 == 16) HG_STAMP(403);
-    cl.sync();
+    cl.sync();  // every source read before any destination is overwritten
     HG_STAMP(2 + (c0 / W) * 8 + 2);
-    for (int m = 0; m < nm; ++m) {
-      const int d = mvd[m];
-      const bool d_top = d < 0;
-      const bool writer = d_top ? (q == 0) : (d >= row0 && d < row0 + R);
-      if (!writer) continue;
-      if (!ts) {
-        if (tid < ncol_out) Ps[out_col(tid) * LDP + (d - row0)] = stg[m * SB + tid];
-      } else if (d_top) {
-        const int c = cR + tid;
-        if (c < SB) {
-          p.U[size_t(ii + c) * nb + ii + c0 + (-1 - d)] = stg[m * SB + c];
-          U12[(-1 - d) * SB + tid] = stg[m * SB + c];
+#pragma unroll
+    for (int m = 0; m < 2 * W; ++m) {
+      if (m < nm && colok) {
+        const int d = mvd[m], sidx = mvs[m];
+        if (q == (sidx < 0 ? 0 : sidx / R)) {
+          if (ts && d < 0) {  // a U row (right-hand columns): the forward solve writes it to global memory
+            cl.map_shared_rank(U12, 0)[(-1 - d) * SB + tid] = mv[m];
+          } else {
+            cl.map_shared_rank(Ps, d / R)[mcol * LDP + (d % R)] = mv[m];
+          }
         }
-      } else {
-        const int c = cR + tid;
-        if (c < SB) Ps[c * LDP + (d - row0)] = stg[m * SB + c];
       }
     }
+    cl.sync();  // every destination written
     __syncthreads();
     HG_STAMP(2 + (c0 / W) * 8 + 3);
     if (cR >= SB) break;
@@ -917,17 +902,17 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   // ---- inv(L_uu) into the side area: CTA q computes block column q (16 columns) ----------
   // X = L^-1 of the unit-lower 128 x 128 L_uu by 16 x 16 blocks: X_ii = inv(L_ii) (one warp
   // each, lanes = columns), then down the block column X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj.
+  // L is kept packed (lower triangle by columns) so the scratch fits the panel's footprint.
   {
     constexpr int B = kSpW, NBK = SB / B;
     static_assert(NBK == kLuCl, "one block column per CTA");
     const int k0 = q * B;
-    constexpr int LL = SB + 1;
-    double* Ls = sm;                  // Ls[c * LL + r] = L(r, c), r > c, c >= k0
-    double* Xd = Ls + SB * LL;        // [NBK][B][B] diagonal block inverses, Xd[bi*B*B + c*B + r]
-    double* Xc = Xd + NBK * B * B;    // [SB][B] this block column of X, Xc[r * B + c]
-    double* Tm = Xc + SB * B;         // [B][B] Tm[c * B + m]
-    const int ncl = SB - k0;
-    const int tot = ncl * SB;
+    auto pk = [](int r, int c) { return c * SB - (c * (c - 1)) / 2 + (r - c); };  // r >= c
+    double* Ls = sm;                          // packed lower L_uu (diagonal slot unused)
+    double* Xd = Ls + SB * (SB + 1) / 2;      // [NBK][B][B] diagonal block inverses, Xd[bi*B*B + c*B + r]
+    double* Xc = Xd + NBK * B * B;            // [SB][B] this block column of X, Xc[r * B + c]
+    double* Tm = Xc + SB * B;                 // [B][B] Tm[c * B + m]
+    const int tot = (SB - k0) * SB;
     for (int e0 = tid; e0 < tot; e0 += 16 * kSpThreads) {  // 16 L2 loads in flight per thread
       double v[16];
 #pragma unroll
@@ -940,7 +925,8 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
 #pragma unroll
       for (int x = 0; x < 16; ++x) {
         const int e = e0 + x * kSpThreads;
-        if (e < tot) Ls[(k0 + e / SB) * LL + e % SB] = v[x];
+        const int c = k0 + e / SB, r = e % SB;
+        if (e < tot && r >= c) Ls[pk(r, c)] = v[x];
       }
     }
     __syncthreads();
@@ -954,7 +940,7 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
 #pragma unroll
         for (int k = 0; k < B; ++k)
 #pragma unroll
-          for (int r = k + 1; r < B; ++r) x[r] = fma(-Ls[(bi * B + k) * LL + bi * B + r], x[k], x[r]);
+          for (int r = k + 1; r < B; ++r) x[r] = fma(-Ls[pk(bi * B + r, bi * B + k)], x[k], x[r]);
 #pragma unroll
         for (int r = 0; r < B; ++r) Xd[bi * B * B + lane * B + r] = x[r];
       }
@@ -971,7 +957,7 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
         double t[4] = {0.0, 0.0, 0.0, 0.0};
         for (int k = k0; k < bi * B; k += 4) {
 #pragma unroll
-          for (int x = 0; x < 4; ++x) t[x] = fma(Ls[(k + x) * LL + bi * B + r], Xc[(k + x) * B + c], t[x]);
+          for (int x = 0; x < 4; ++x) t[x] = fma(Ls[pk(bi * B + r, k + x)], Xc[(k + x) * B + c], t[x]);
         }
         Tm[c * B + r] = (t[0] + t[1]) + (t[2] + t[3]);
       }
@@ -1046,7 +1032,7 @@ k_lu_apply_strip(LuApplyParams p) {
     // rows' final values reach global memory through the top' epilogue below, and the bot rows
     // that received top slots are stored from a pristine smem copy (Pt) of the top rows.
     static_assert(G::THREADS == kLuMaxSb, "one thread per top slot");
-    int* slot_src = sp + 3 * kLuMaxSb;      // [sb] >= 0: bot row; < 0: top slot -1-k
+    int* slot_src = sp;                     // [sb] >= 0: bot row; < 0: top slot -1-k (lu_moves' scratch is dead)
     int* bd_row = slot_src + kLuMaxSb;      // [sb] bot rows that receive a top slot
     int* bd_slot = bd_row + kLuMaxSb;       // [sb] ... namely this one
     __shared__ int n_bd;
@@ -1133,7 +1119,7 @@ static unsigned lu_apply_strip_smem() {
   const size_t ru = size_t(GU::STAGES) * GU::slab_mmaj(GU::BM);
   if (ru > ring) ring = ru;
   size_t d = ring + G::BN * kLcLd;
-  size_t ints = 2 * kLcMaxMoves + 3 * kLuMaxSb + 3 * kLuMaxSb;  // moves, lu_moves scratch, slot sources
+  size_t ints = 2 * kLcMaxMoves + 3 * kLuMaxSb;  // moves, lu_moves scratch (then the slot sources)
   return unsigned(d * sizeof(double) + ints * sizeof(int));
 }
 
@@ -1143,8 +1129,8 @@ static unsigned sp_smem(int nb) {
              : nb == 768 ? SpSmem<96>::BYTES
              : nb == 512 ? SpSmem<64>::BYTES
                          : SpSmem<32>::BYTES;
-  // end-of-panel inverse scratch: L_uu, diagonal block inverses, one block column, a block product
-  size_t ls = (size_t(kSpSB) * (kSpSB + 1) + 2 * size_t(kSpSB) * kSpW + size_t(kSpW) * kSpW) * 8;
+  // end-of-panel inverse scratch: packed L_uu, diagonal block inverses, one block column, a block product
+  size_t ls = (size_t(kSpSB) * (kSpSB + 1) / 2 + 2 * size_t(kSpSB) * kSpW + size_t(kSpW) * kSpW) * 8;
   return unsigned(b > ls ? b : ls);
 }
 
