@@ -583,6 +583,7 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   __shared__ double red_v[kSpThreads / 32];
   __shared__ int red_r[kSpThreads / 32];
   __shared__ int n_mv;
+  __shared__ __align__(8) uint64_t sbar;  // phase S: the moved values land with st.async (one phase per sub-panel)
   int* ipiv = reinterpret_cast<int*>(p.side + size_t(ib) * nb);
   double* inv = p.side + size_t(ii) * ib;  // dL(jj, c) at inv[c*ib + jj]
   double* A = p.A;
@@ -597,6 +598,7 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&sbar, 1);
     fence_mbar_init_cluster();
   }
   for (int e = tid; e < W * W; e += kSpThreads) dlAll[e] = 0.0;
@@ -608,14 +610,6 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
 
   for (int c0 = 0; c0 < SB; c0 += W) {
     HG_STAMP(2 + (c0 / W) * 8);
-    // TSTRF, CTA 0: the sub-panel's U rows right of it, loaded now (the column loop never touches
-    // them) and parked in U12 for the moves -- the L2 latency hides behind the column loop
-    double upre[W];
-    const bool pre = ts && q == 0 && tid < SB - (c0 + W);
-    if (pre) {
-#pragma unroll
-      for (int v = 0; v < W; ++v) upre[v] = __ldcg(p.U + size_t(ii + c0 + W + tid) * nb + ii + c0 + v);
-    }
     if (ts) {
       for (int e = tid; e < W * W; e += kSpThreads) {
         const int u = e / W, v = e % W;
@@ -796,9 +790,9 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
     // right-hand columns
     const int ncol_out = SB - W;
     auto out_col = [&](int k) { return k < c0 ? k : k + W; };
-    if (pre) {  // CTA 0: the sub-panel's U rows (right-hand columns) before the moves
+    if (ts && q == 0 && tid < SB - cR) {  // CTA 0: the sub-panel's U rows (right-hand columns) before the moves
 #pragma unroll
-      for (int v = 0; v < W; ++v) U12[v * SB + tid] = upre[v];
+      for (int v = 0; v < W; ++v) U12[v * SB + tid] = __ldcg(p.U + size_t(ii + cR + tid) * nb + ii + c0 + v);
     }
     // Moves in two steps separated by a cluster barrier: the CTA holding a move's source (a Ps
     // row, or for TSTRF a top slot: CTA 0's U12 prefetch) reads it into registers; after the
@@ -818,20 +812,28 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
     if (c0 == 16) HG_STAMP(403);
     cl.sync();  // every source read before any destination is overwritten
     HG_STAMP(2 + (c0 / W) * 8 + 2);
+    if (tid == 0) {  // this CTA's arrival: the bytes the moves will deliver into it
+      const int ncv = ts ? SB - cR : ncol_out;
+      int cnt = 0;
+      for (int m = 0; m < nm; ++m) {
+        const int d = mvd[m];
+        cnt += (ts && d < 0) ? (q == 0) : (d / R == q);
+      }
+      mbar_arrive_tx(&sbar, unsigned(cnt * ncv * 8));
+    }
 #pragma unroll
     for (int m = 0; m < 2 * W; ++m) {
       if (m < nm && colok) {
         const int d = mvd[m], sidx = mvs[m];
         if (q == (sidx < 0 ? 0 : sidx / R)) {
-          if (ts && d < 0) {  // a U row (right-hand columns): the forward solve writes it to global memory
-            cl.map_shared_rank(U12, 0)[(-1 - d) * SB + tid] = mv[m];
-          } else {
-            cl.map_shared_rank(Ps, d / R)[mcol * LDP + (d % R)] = mv[m];
-          }
+          const bool top = ts && d < 0;  // a U row (right-hand columns): the forward solve writes it out
+          const unsigned dst = top ? 0u : unsigned(d / R);
+          double* loc = top ? U12 + (-1 - d) * SB + tid : Ps + mcol * LDP + (d % R);
+          st_async_f64(cluster_addr(loc, dst), mv[m], cluster_addr(&sbar, dst));
         }
       }
     }
-    cl.sync();  // every destination written
+    mbar_wait_cluster(&sbar, (c0 / W) & 1);  // every move into this CTA has landed
     __syncthreads();
     HG_STAMP(2 + (c0 / W) * 8 + 3);
     if (cR >= SB) break;
