@@ -90,6 +90,21 @@ HG_DEVICE void load_slab(double* s, const double* __restrict__ g, int ld, int r0
   }
 }
 
+// One warp's 32 rows [w0, w0 + 32) of an M_MAJOR (ROWS x BK) slab: per k 256 contiguous
+// bytes (16 chunks), BK / 2 chunks per lane.
+template <class Cfg, int ROWS>
+HG_DEVICE void load_slab_warp(double* s, const double* __restrict__ g, int ld, int r0, int k0, int w0, int lane) {
+  constexpr int BK = Cfg::BK, PAD = Cfg::PAD;
+  static_assert((BK * 16) % 32 == 0, "whole chunks per lane");
+  const double* gb = g + size_t(k0) * ld + r0 + w0;
+#pragma unroll
+  for (int i = 0; i < BK * 16 / 32; ++i) {
+    const int c = lane + i * 32;
+    const int kk = c / 16, rr = (c % 16) * 2;
+    cp_async16(s + kk * (ROWS + PAD) + w0 + rr, gb + size_t(kk) * ld + rr);
+  }
+}
+
 template <class Cfg, int L, int ROWS>
 HG_DEVICE double frag_at(const double* s, int r, int k) {
   if constexpr (L == M_MAJOR) return s[k * (ROWS + Cfg::PAD) + r];
@@ -105,6 +120,11 @@ struct TileLoader {
   int ld;
   int r0;
   HG_DEVICE void load(double* s, int k0) const { load_slab<Cfg, L, ROWS>(s, p, ld, r0, k0); }
+  // M_MAJOR only: the 32 slab rows [w0, w0 + 32) of one warp (warp-private rings)
+  HG_DEVICE void load_warp(double* s, int k0, int w0, int lane) const {
+    static_assert(L == M_MAJOR, "warp-row loads are M_MAJOR");
+    load_slab_warp<Cfg, ROWS>(s, p, ld, r0, k0, w0, lane);
+  }
 };
 
 // Main loop over k in [k_begin, k_end) (multiples of BK). acc[FM][FN][2].
@@ -548,7 +568,80 @@ HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int
     if (s < total) load(s);
     cp_async_commit();
   }
-  if constexpr (RED && STAGES >= 3) {
+  if constexpr (RED && STAGES >= 3 && Cfg::WARPS_N == 1 && LA == M_MAJOR) {
+    // Warp-private A stream: with one warp column every warp reads only its own 32 rows of
+    // each A slab (B is resident), so each warp loads exactly those rows with its own cp.async
+    // groups and synchronises with __syncwarp -- no CTA barrier in the stream.  The warps
+    // drift apart, so one warp's chunk epilogue (the red.global.add drain) overlaps the other
+    // warps' DMMAs instead of all four draining in lockstep.  Same k order per accumulator as
+    // the CTA-barrier variant below: bit-identical results.
+    static_assert(BK % 8 == 0, "slabs start on fragment buffer 0");
+    __syncthreads();  // the ring may still be read by the caller's previous (CTA-wide) phase
+    auto load_w = [&](int s) {
+      LdA l = la;
+      l.r0 = m_begin + (s / NK) * Cfg::BM;
+      l.load_warp(ring + (s % STAGES) * A_SLAB, (s % NK) * BK, wm, lane);
+    };
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < total) load_w(s);
+      cp_async_commit();
+    }
+    double acc[Cfg::FM][Cfg::FN][2];
+    zero_acc<Cfg>(acc);
+    double af[2][Cfg::FM], bf[2][Cfg::FN];
+    cp_async_wait<STAGES - 2>();
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i) af[0][i] = frag_at<Cfg, LA, Cfg::BM>(ring, wm + i * 8 + g, t);
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) bf[0][j] = sB[(wn + j * 8 + g) * ldsb + t];
+    for (int it = 0; it < total; ++it) {
+      const int kslab = it % NK;
+      cp_async_wait<STAGES - 3>();
+      __syncwarp();
+      if (it + STAGES - 1 < total) load_w(it + STAGES - 1);
+      cp_async_commit();
+      const double* a_s = ring + (it % STAGES) * A_SLAB;
+      const double* a_n = ring + ((it + 1) % STAGES) * A_SLAB;
+      const int kb = kslab * BK;
+      const int kb_n = ((it + 1) % NK) * BK;
+      const bool more = it + 1 < total;
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        const int cur = (kk >> 2) & 1, nxt = cur ^ 1;
+        if (kk + 4 < BK) {
+#pragma unroll
+          for (int i = 0; i < Cfg::FM; ++i) af[nxt][i] = frag_at<Cfg, LA, Cfg::BM>(a_s, wm + i * 8 + g, kk + 4 + t);
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) bf[nxt][j] = sB[(wn + j * 8 + g) * ldsb + kb + kk + 4 + t];
+        } else if (more) {
+#pragma unroll
+          for (int i = 0; i < Cfg::FM; ++i) af[nxt][i] = frag_at<Cfg, LA, Cfg::BM>(a_n, wm + i * 8 + g, t);
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) bf[nxt][j] = sB[(wn + j * 8 + g) * ldsb + kb_n + t];
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
+      }
+      if (kslab == NK - 1) {
+        const int m0 = m_begin + (it / NK) * Cfg::BM;
+        for_each_acc_ij<Cfg>([&](int i, int j, int r, int c) {
+          if (m0 + r >= m_mask) {
+            red_add_f64(C + size_t(n0 + c) * ldc + m0 + r, -acc[i][j][0]);
+            red_add_f64(C + size_t(n0 + c + 1) * ldc + m0 + r, -acc[i][j][1]);
+          }
+        });
+        zero_acc<Cfg>(acc);
+      }
+    }
+    __threadfence();
+    cp_async_wait<0>();
+    __syncthreads();
+    return;
+  } else if constexpr (RED && STAGES >= 3) {
     static_assert(BK % 8 == 0, "slabs start on fragment buffer 0");
     // Fragment pipeline that never drains at slab boundaries: the barrier at the
     // top of iteration `it` publishes slab it+1 as well (wait_group STAGES-3), so
@@ -661,6 +754,52 @@ HG_DEVICE void gemm_sub_chunks_bsmem(double* ring, LdA la, const double* sB, int
   if constexpr (RED) __threadfence();
   cp_async_wait<0>();
   __syncthreads();
+}
+
+
+// ---------------------------------------------------------------------------
+// Producer-push helpers: the producing kernel stores the final values of a
+// task's output block into the consumer GPUs' slots of that block (peer / IPC pointers), so the
+// plan's copy job needs no copy node.  Callers fence + synchronise first (the values are read
+// back through L2: the trailing updates end in L2 reductions).
+
+// Whole slots (tile + side area), the threads of `nrank` CTAs of a cluster cooperating.
+HG_DEVICE void push_slots(const PushList& pl, int rank, int nrank) {
+  const long long n2 = pl.len / 2;
+  const long long step = (long long)nrank * blockDim.x;
+  for (int q = 0; q < pl.n; ++q) {
+    const double2* s = reinterpret_cast<const double2*>(pl.src[q]);
+    double2* d = reinterpret_cast<double2*>(pl.dst[q]);
+    long long e = (long long)rank * blockDim.x + threadIdx.x;
+    for (; e + 3 * step < n2; e += 4 * step) {  // 4 L2 loads in flight per thread
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcg(s + e + u * step);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) __stcg(d + e + u * step, v[u]);
+    }
+    for (; e < n2; e += step) __stcg(d + e, __ldcg(s + e));
+    if ((pl.len & 1) && rank == 0 && threadIdx.x == 0) pl.dst[q][pl.len - 1] = __ldcg(pl.src[q] + pl.len - 1);
+  }
+}
+
+// Columns [n0, n0 + BN) of every pushed tile (all nb rows, column-major ld = nb): one CTA's strip.
+template <int BN, int THREADS>
+HG_DEVICE void push_strip(const PushList& pl, int n0, int nb) {
+  const int h = nb / 2;  // double2 per column
+  for (int q = 0; q < pl.n; ++q) {
+    const double2* s = reinterpret_cast<const double2*>(pl.src[q] + size_t(n0) * nb);
+    double2* d = reinterpret_cast<double2*>(pl.dst[q] + size_t(n0) * nb);
+    for (int e = threadIdx.x; e < BN * h; e += 4 * THREADS) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (e + u * THREADS < BN * h) v[u] = __ldcg(s + e + u * THREADS);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (e + u * THREADS < BN * h) __stcg(d + e + u * THREADS, v[u]);
+    }
+  }
 }
 
 }  // namespace hg

@@ -321,7 +321,7 @@ struct hg_exec {
   int p2p = 1;
   int push = 0;                          // producer-push fusion requested (hg_exec_plan.push)
   std::vector<char> job_push;            // job delivered by its version's producer kernel (no copy node)
-  std::vector<std::vector<int>> push_to; // per task: destination nodes its kernels push the output to
+  std::vector<std::vector<std::pair<int, int>>> push_to;  // per task: (destination node, block) its kernels push
   double* host_stage = nullptr;          // p2p = 0: pinned staging image, slot-sized regions
   std::vector<int64_t> stage_off;
   // options
@@ -438,10 +438,12 @@ static void plan_layout(hg_exec* ex) {
   for (int j = 0; j < ex->n_jobs; ++j) need(ex->job_dst[j], ex->job_block[j]);
 }
 
-// Producer-push fusion: a peer job that moves version v (written by task v)
-// to GPU node D is delivered by task v's own kernels -- their epilogue stores the final tile to
-// D's slot as well (peer / IPC pointers) -- when v's kind supports it (tiles.h kind_can_push)
-// and v has at most kMaxPush such destinations.  Bytes per (version, destination) equal the
+// Producer-push fusion: a peer job that moves version v of block b (written
+// by task v) to GPU node D is delivered by task v's own kernels -- their epilogue stores the final
+// tile to D's slot of b as well (peer / IPC pointers) -- when v's kind supports it (tiles.h
+// kind_can_push: the Cholesky kinds, the LU / QR trailing updates and panels) and b is a tile
+// (materialised T blocks travel by copy node).  At most kMaxPush (D, b) pairs per task are
+// pushed; further jobs keep their copy nodes.  Bytes per (version, destination) equal the
 // plan's; the copy node disappears and the consumer depends on task v itself.  WAR-safe: every
 // reader of any older version of the block precedes v in the DAG (graph.py:58-84), and the
 // step fence orders runs across ranks.  Deterministic from the plan, so every rank agrees.
@@ -449,19 +451,20 @@ static void plan_push(hg_exec* ex) {
   ex->job_push.assign(ex->n_jobs, 0);
   ex->push_to.assign(ex->n_tasks, {});
   if (!ex->push || !ex->p2p || ex->k < 2) return;
+  const int64_t tile_d = int64_t(ex->nb) * ex->nb;
   for (int j = 0; j < ex->n_jobs; ++j) {
-    const int v = ex->job_version[j], dst = ex->job_dst[j];
-    if (v < 0 || dst < 1 || ex->job_src[j] < 1 || !kind_can_push(ex->task_kind[v])) continue;
+    const int v = ex->job_version[j], dst = ex->job_dst[j], b = ex->job_block[j];
+    if (v < 0 || dst < 1 || ex->job_src[j] < 1 || !kind_can_push(ex->task_kind[v], ex->nb, ex->ib)) continue;
+    if (ex->blk_doubles[b] != tile_d) continue;
     auto& d = ex->push_to[v];
-    if (std::find(d.begin(), d.end(), dst) == d.end()) d.push_back(dst);
+    const std::pair<int, int> e{dst, b};
+    if ((int)d.size() < kMaxPush && std::find(d.begin(), d.end(), e) == d.end()) d.push_back(e);
   }
-  for (auto& d : ex->push_to)
-    if ((int)d.size() > kMaxPush) d.clear();
   for (int j = 0; j < ex->n_jobs; ++j) {
     const int v = ex->job_version[j];
     if (v < 0) continue;
     const auto& d = ex->push_to[v];
-    ex->job_push[j] = std::find(d.begin(), d.end(), ex->job_dst[j]) != d.end();
+    ex->job_push[j] = std::find(d.begin(), d.end(), std::make_pair(ex->job_dst[j], ex->job_block[j])) != d.end();
   }
 }
 
@@ -739,6 +742,11 @@ static int build_graph(hg_exec* ex) {
         job_node[j] = deps[0];
         st.bytes_d2d += size_t(ex->blk_doubles[b]) * 8;
         st.n_push_jobs++;
+        {  // the LU / QR panel kinds push whole slots: the side area rides along as with a copy node
+          const int pk = ex->task_kind[ex->job_version[j]];
+          if (pk == K_GETRF_INC || pk == K_TSTRF || pk == K_GEQRT || pk == K_TSQRT)
+            side_bytes += int64_t(ex->slot_doubles[b] - ex->blk_doubles[b]) * 8;
+        }
         continue;
       }
       const bool staged_in = src == 0 && (ex->job_version[j] >= 0 || ex->job_src_job[j] >= 0 ||
@@ -850,18 +858,19 @@ static int build_graph(hg_exec* ex) {
       return HG_EINVAL;
     }
     for (int64_t a = a0; a < a1; ++a) ops.t[ops.n_t++] = ex->slot_ptr(node, ex->acc_block[a]);
-    if (!ex->push_to[t].empty()) {
-      int wb = -1;  // the block this task writes (last written access)
+    ops.side = ex->side;
+    for (const auto& e : ex->push_to[t]) {
+      const int d = e.first, b = e.second;
+      int op = -1;  // the written operand holding block b
       for (int64_t a = a0; a < a1; ++a)
-        if (ex->acc_mode.empty() || (ex->acc_mode[a] & HG_ACCESS_W)) wb = ex->acc_block[a];
-      for (int d : ex->push_to[t]) {
-        double* q = ex->slot_ptr(d, wb);
-        if (wb < 0 || !q) {
-          set_error("task %d: no slot of its output block on push destination node %d", t, d);
-          return HG_EINVAL;
-        }
-        ops.push.dst[ops.push.n++] = q;
+        if (ex->acc_block[a] == b && (ex->acc_mode.empty() || (ex->acc_mode[a] & HG_ACCESS_W))) op = int(a - a0);
+      double* q = ex->slot_ptr(d, b);
+      if (op < 0 || !q) {
+        set_error("task %d: block %d is not an output with a slot on push destination node %d", t, b, d);
+        return HG_EINVAL;
       }
+      ops.push.dst[ops.push.n] = q;
+      ops.push.op[ops.push.n++] = (unsigned char)op;
     }
     launches.clear();
     if (!build_task_launches(ex->task_kind[t], ops, launches)) return HG_EINVAL;
@@ -1218,6 +1227,12 @@ extern "C" int hg_exec_partition(const hg_exec_plan* P, int32_t rank_node, int32
   ex.job_src_job = vcopy(P->job_src_job, nj);
   ex.job_src = vcopy(P->job_src, nj);
   ex.task_kind = vcopy(P->task_kind, n);
+  ex.job_block = vcopy(P->job_block, nj);
+  ex.nb = P->nb;
+  ex.ib = P->ib;
+  ex.n_blocks = P->n_blocks;
+  ex.blk_doubles.resize(P->n_blocks);
+  for (int b = 0; b < P->n_blocks; ++b) ex.blk_doubles[b] = P->block_bytes[b] / 8;
   ex.p2p = P->p2p;
   ex.push = P->push;
   plan_push(&ex);

@@ -13,17 +13,23 @@
 
 namespace hg {
 
-constexpr int kParamBytes = 160;
+constexpr int kParamBytes = 256;
 
-// Producer-push fusion: at most this many consumer GPUs receive a task's output tile
-// straight from the producing kernel (peer stores), see PushList / runtime.cu.
-constexpr int kMaxPush = 7;
+// Producer-push fusion: at most this many (consumer GPU, output block) pairs receive a
+// task's output straight from the producing kernel (peer stores), see PushList / runtime.cu.
+constexpr int kMaxPush = 8;
 
-// Destinations of a pushed output tile: the same block's slot on up to kMaxPush other GPUs
-// (peer / IPC-mapped pointers; same nb x nb column-major layout as the local tile).
+// Destinations of a pushed output: the same block's slot on up to kMaxPush other GPUs
+// (peer / IPC-mapped pointers; same layout as the local slot).  The runtime fills dst and op
+// (index of the written operand in TaskOperands::t); the kind's launch builder resolves src
+// (the local slot of that operand) and len (doubles per slot: the tile, plus the side area for
+// the LU / QR panel kinds, whose consumers read the dL / IPIV / T factors from it).
 struct PushList {
   double* dst[kMaxPush];
+  const double* src[kMaxPush];
+  unsigned char op[kMaxPush];
   int n;
+  int len;
 };
 
 struct LaunchDesc {
@@ -52,10 +58,27 @@ struct TaskOperands {
   int* scratch = nullptr; // per-task device ints (task_scratch_ints), zero-initialised once;
                           // kernels keep them self-consistent across runs
   PushList push{};        // producer-push: where the written tile also goes (kinds with push support)
+  int side = 0;           // doubles of a tile's side area (LU / QR), the slot is nb*nb + side
 };
 
-// Kinds whose kernels can push their output tile to consumer GPUs in the epilogue.
-inline bool kind_can_push(int kind) { return kind >= 0 && kind <= 3; }  // POTRF, TRSM, SYRK, GEMM
+// Kinds whose kernels can push their output tiles to consumer GPUs in the epilogue: the
+// Cholesky kinds (the store epilogue), the LU / QR trailing updates (each strip CTA pushes its
+// columns once its last L2 reduction landed) and the LU / QR panels (the task's last panel
+// kernel pushes the whole slots after its final cluster barrier).  LU only on the ib = 128
+// kernels (the sub-panel cluster and the strip apply).
+inline bool kind_can_push(int kind, int nb, int ib) {
+  if (kind >= 0 && kind <= 3) return true;                          // POTRF, TRSM, SYRK, GEMM
+  if (kind >= 4 && kind <= 7) return ib == 128 && nb % 128 == 0;    // GETRF_INC, GESSM, TSTRF, SSSSM
+  return kind >= 8 && kind <= 11;                                   // GEQRT, UNMQR, TSQRT, TSMQR
+}
+
+// The task's push list with src / len resolved: whole slots (tile + side) or tiles only.
+inline PushList resolve_push(const TaskOperands& o, bool whole_slots) {
+  PushList pl = o.push;
+  for (int q = 0; q < pl.n; ++q) pl.src[q] = o.t[pl.op[q]];
+  pl.len = o.nb * o.nb + (whole_slots ? o.side : 0);
+  return pl;
+}
 
 // Device ints of per-task scratch a kind needs (0 for most kinds).
 int task_scratch_ints(int kind, int nb, int ib);

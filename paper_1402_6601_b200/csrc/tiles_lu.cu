@@ -49,6 +49,7 @@ struct LuPanelParams {
   double* side;   // side area of A: inverse blocks (ib x nb), then ipiv
   int nb, ib, ii, sb, mode;
   int* status;
+  PushList push;  // the task's last panel: producer-push of its output slots (tile + side)
 };
 
 __device__ __forceinline__ bool better(double v, int r, double bv, int br) {
@@ -298,6 +299,7 @@ struct LuApplyParams {
 #ifdef HG_PANEL_STAMPS
   int stamp;            // tools/ssssm_ab.cu: this task's CTA 0 records phase stamps
 #endif
+  PushList push;        // task-level launch: producer-push of the written tiles' columns of each strip
 };
 
 template <int SB>
@@ -978,7 +980,11 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
       inv[size_t(k0 + c) * ib + r] = r < k0 ? 0.0 : Xc[r * B + c];
     }
   }
-  HG_STAMP(82);
+  HG_STAMP(82);  if (p.push.n) {  // producer-push: every kernel of the task is done once the whole cluster is here
+    __threadfence();
+    cl.sync();
+    push_slots(p.push, q, kLuCl);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1110,6 +1116,11 @@ k_lu_apply_strip(LuApplyParams p) {
     __syncthreads();
     HG_STAMP(20 + 4 * (P - p.p0) + 3);
   }
+  if (p.push.n) {  // this strip's columns are final once its own L2 reductions landed
+    __threadfence();
+    __syncthreads();
+    push_strip<BN, G::THREADS>(p.push, n0, nb);
+  }
 }
 
 using CfgLS16 = GemmCfg<128, 16, 16, 32, 16, 3>;  // 4 warps, 16-column strips: the in-panel trailing columns
@@ -1204,8 +1215,10 @@ static bool use_strip_apply(int nb, int ib) { return ib == kLuMaxSb && nb % 128 
 
 // Panels [P0, P1) applied to columns [col0, nb) by the strip kernel.
 static void push_apply_strip(std::vector<LaunchDesc>& out, const double* L, const double* side, double* top,
-                             double* bot, int nb, int ib, int P0, int P1, int col0, int mode, int bn) {
+                             double* bot, int nb, int ib, int P0, int P1, int col0, int mode, int bn,
+                             const PushList* push = nullptr) {
   LuApplyParams ap{L, side, top, bot, nb, ib, P0, P1, col0, mode, 0};
+  if (push) ap.push = *push;
   LaunchDesc d;
   const int ncols = nb - col0;
   if (bn == 16)
@@ -1254,6 +1267,7 @@ bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
       for (int P = 0; P < np; ++P) {
         LuPanelParams pp{A, ts ? o.t[0] : nullptr, ts ? side(1) : side(0), nb, ib, P * ib, ib,
                          ts ? LU_TSTRF : LU_GETRF, o.status};
+        if (P + 1 == np && use_sp_panel(nb, ib)) pp.push = resolve_push(o, true);  // tile + side (dL, IPIV)
         LaunchDesc d;
         if (use_sp_panel(nb, ib))
           d.set(panel_kernel(nb, ib), dim3(kLuCl), dim3(kSpThreads), sp_smem(nb), pp);
@@ -1268,14 +1282,16 @@ bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
     }
     case K_GESSM:
       if (use_strip_apply(nb, ib)) {
-        push_apply_strip(out, o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF, 32);
+        const PushList pl = resolve_push(o, false);
+        push_apply_strip(out, o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF, 32, &pl);
         return true;
       }
       for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[1], nb, P, 0, LU_GETRF);
       return true;
     case K_SSSSM:
       if (use_strip_apply(nb, ib)) {
-        push_apply_strip(out, o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF, 32);
+        const PushList pl = resolve_push(o, false);
+        push_apply_strip(out, o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF, 32, &pl);
         return true;
       }
       for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[2], nb, P, 0, LU_TSTRF);

@@ -38,6 +38,7 @@ struct QrPanelParams {
   double* R;     // TSQRT: A_kk (R rows); GEQRT: unused
   double* side;  // side area of A: T factors (ib x nb)
   int nb, ib, ii, sb, mode;
+  PushList push;  // the task's last panel: producer-push of its output slots (tile + side)
 };
 
 // T (ib x sb block at T, ld ib, upper triangular) from y = striu(V^T V) stored above
@@ -330,9 +331,15 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
   __threadfence();
   cl.sync();
   HG_STAMP(80);
-  if (q != 0) return;
-  qr_t_from_y(T, ib, sb, s);
-  HG_STAMP(82);
+  if (q == 0) {
+    qr_t_from_y(T, ib, sb, s);
+    HG_STAMP(82);
+  }
+  if (p.push.n) {  // producer-push: every kernel of the task is done once CTA 0's T is written
+    __threadfence();
+    cl.sync();
+    push_slots(p.push, q, kQrCl);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -371,6 +378,20 @@ struct VLoader {
       else s[kk * (ROWS + PAD) + rr] = val(r0 + rr, k0 + kk);
     }
   }
+  // M_MAJOR only: one warp's 32 slab rows [w0, w0 + 32) (warp-private rings of the C -= V W stream)
+  HG_DEVICE void load_warp(double* s, int k0, int w0, int lane) const {
+    static_assert(L == M_MAJOR, "warp-row loads are M_MAJOR");
+    constexpr int BK = Cfg::BK, PAD = Cfg::PAD;
+    const int rw = r0 + w0;
+    // element-wise unless every row of the warp lies strictly below the slab's diagonal band
+    // (rows entirely ABOVE it are zeros of the unit-lower V, not the stored R)
+    if (!(masked && rw < ii + k0 + BK)) {
+      load_slab_warp<Cfg, ROWS>(s, v, ld, r0, k0, w0, lane);
+      return;
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) s[kk * (ROWS + PAD) + w0 + lane] = val(rw + lane, k0 + kk);
+  }
 };
 
 struct QrApplyParams {
@@ -382,6 +403,7 @@ struct QrApplyParams {
 #ifdef HG_PANEL_STAMPS
   int stamp;           // tools/ssssm_ab.cu (q mode): this task's CTA 0 records phase stamps
 #endif
+  PushList push;       // task-level launch: producer-push of the written tiles' columns of each strip
 };
 
 // Column-strip variant: one CTA per BN-column strip (no cluster, all rows),
@@ -463,6 +485,11 @@ __global__ void __launch_bounds__(CfgQ::THREADS, CfgQ::THREADS == 128 ? 3 : 2) k
     __syncthreads();
     HG_STAMP(20 + 4 * (P - p.p0) + 3);
   }
+  if (p.push.n) {  // this strip's columns are final once its own L2 reductions landed
+    __threadfence();
+    __syncthreads();
+    push_strip<kQrBN, CfgQ::THREADS>(p.push, n0, nb);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -521,7 +548,8 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
   auto side = [&](int i) { return o.t[i] + tile; };
   // block-reflector applications: 16-column strips inside a panel task (few trailing columns),
   // 32-column strips of 4 warps at 3 CTAs / SM for UNMQR / TSMQR; C -= V W as L2 reductions
-  auto push_apply = [&](const QrApplyParams& ap, int bn) {
+  auto push_apply = [&](QrApplyParams ap, int bn, bool push = false) {
+    if (push) ap.push = resolve_push(o, false);  // the task-level strip launch pushes its columns
     LaunchDesc d;
     const int ncols = nb - ap.col0;
     if (bn == 16)
@@ -540,6 +568,7 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
       for (int P = 0; P < np; ++P) {
         QrPanelParams pp{A, ts ? o.t[0] : nullptr, ts ? side(1) : side(0), nb, ib, P * ib, ib,
                          ts ? QR_TSQRT : QR_GEQRT};
+        if (P + 1 == np) pp.push = resolve_push(o, true);  // tile + side (T factors)
         LaunchDesc d;
         d.set((const void*)k_qr_panel, dim3(kQrCl), dim3(kQrThreads), qr_panel_smem(nb, ib), pp);
         out.push_back(d);
@@ -557,10 +586,10 @@ bool build_qr_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
       return true;
     }
     case K_UNMQR:
-      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], nullptr, nb, ib, 0, np, 0, QR_GEQRT}, 32);
+      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], nullptr, nb, ib, 0, np, 0, QR_GEQRT}, 32, true);
       return true;
     case K_TSMQR:
-      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, QR_TSQRT}, 32);
+      push_apply(QrApplyParams{o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, QR_TSQRT}, 32, true);
       return true;
     default:
       set_error("kind %d is not a QR kind", kind);

