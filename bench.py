@@ -296,12 +296,36 @@ def cpu_baseline_sample(fam, n, nb, ib):
 
     workers = cpu_exec.host_threads()
     g = H.gen_family(fam, n // nb, nb, ib)
-    arena, secs = cpu_exec.factor(g, oracle_matrix(fam, n, 0), workers)
+    A = oracle_matrix(fam, n, 0)
+    arena, secs = cpu_exec.factor(g, A, workers)
     flops = H.flops_of(fam, n)
     return {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": workers, "kind": "port",
             "sample": f"tiled {fam} N={n} nb={nb} ib={ib} factored once ({secs:.2f} s): oracle SciPy/OpenBLAS/"
                       f"NumPy tile kernels (oracle/tiles*.py) on {workers} forked worker processes, one BLAS "
-                      f"thread each, dynamic DAG list scheduling"}
+                      f"thread each, dynamic DAG list scheduling",
+            "monolithic": monolithic_lapack(fam, A, flops, workers)}
+
+
+def monolithic_lapack(fam, A, flops, threads):
+    """the monolithic LAPACK factorization of the same matrix (scipy.linalg
+    cholesky / lu_factor / qr(mode='r')) on `threads` OpenBLAS threads -- a CPU reference point
+    beside the tile DAG, not the reference's algorithm."""
+    import scipy.linalg as sl
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=threads, user_api="blas"):
+        sl.cholesky(np.eye(512) * 2.0, lower=True)  # spin the BLAS thread pool up outside the timing
+        t0 = time.perf_counter()
+        if fam == "cholesky":
+            sl.cholesky(A, lower=True, overwrite_a=False, check_finite=False)
+        elif fam == "lu":
+            sl.lu_factor(A, overwrite_a=False, check_finite=False)
+        else:
+            sl.qr(A, mode="r", overwrite_a=False, check_finite=False)
+        secs = time.perf_counter() - t0
+    return {"value": flops / secs / 1e9, "unit": "GFLOP/s", "threads": threads,
+            "sample": f"scipy.linalg {'cholesky' if fam == 'cholesky' else 'lu_factor' if fam == 'lu' else 'qr'} "
+                      f"N={A.shape[0]} ({secs:.2f} s, OpenBLAS)"}
 
 
 def reference_planner(g, plat, sched_name, alpha, model_path, nb, ib, ours):
