@@ -77,6 +77,19 @@ HG_DEVICE void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b)
                : "memory");
 }
 
+// 2-D tensor-map TMA load (cp.async.bulk.tensor, SASS UTMALDG) of the box at coordinates
+// (c0 = inner / row, c1 = outer / column) into dense shared memory; `tmap` is the generic
+// address of a CUtensorMap in parameter (__grid_constant__) or global memory.
+HG_DEVICE void tma_load_2d(void* dst, const void* tmap, int c0, int c1, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(b))
+      : "memory");
+}
+// generic-proxy accesses of shared memory before this are ordered before later async-proxy ones (TMA writes)
+HG_DEVICE void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 // ---- cluster push messages: remote shared-memory stores that complete on the
 // receiver's mbarrier (no cluster barrier, no release fence over global memory) ----
 // shared::cluster address of `p` (this CTA's smem) in CTA `rank` of the cluster

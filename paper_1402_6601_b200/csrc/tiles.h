@@ -13,7 +13,7 @@
 
 namespace hg {
 
-constexpr int kParamBytes = 256;
+constexpr int kParamBytes = 512;
 
 // Producer-push fusion: at most this many (consumer GPU, output block) pairs receive a
 // task's output straight from the producing kernel (peer stores), see PushList / runtime.cu.
@@ -36,7 +36,7 @@ struct LaunchDesc {
   const void* func = nullptr;
   dim3 grid, block;
   unsigned smem = 0;
-  alignas(16) unsigned char params[kParamBytes];
+  alignas(64) unsigned char params[kParamBytes];
   template <class P>
   void set(const void* f, dim3 g, dim3 b, unsigned sm, const P& p) {
     static_assert(sizeof(P) <= kParamBytes, "param struct too large");

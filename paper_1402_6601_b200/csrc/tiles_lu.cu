@@ -28,6 +28,8 @@
 // (GETRF: absolute row swapped with row j; TSTRF: A row swapped with U row j,
 // or -1).
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cstdlib>
 
 #include "dgemm_dmma.cuh"
@@ -300,6 +302,7 @@ struct LuApplyParams {
   int stamp;            // tools/ssssm_ab.cu: this task's CTA 0 records phase stamps
 #endif
   PushList push;        // task-level launch: producer-push of the written tiles' columns of each strip
+  alignas(64) CUtensorMap top_map;  // strip kernel: 2-D tensor map of `top` (128-row x BN-column boxes, TMA)
 };
 
 template <int SB>
@@ -999,7 +1002,7 @@ __global__ void __cluster_dims__(kLuCl, 1, 1) __launch_bounds__(kSpThreads) k_lu
 // BM = 256 starts its first row chunk early and masks the rows above it.
 template <class G, bool RED = false, class GU = G>
 __global__ void __launch_bounds__(G::THREADS, G::THREADS == 128 ? 3 : (GU::BM == 256 ? 2 : 1))
-k_lu_apply_strip(LuApplyParams p) {
+k_lu_apply_strip(const __grid_constant__ LuApplyParams p) {
   static_assert(GU::THREADS == G::THREADS && GU::BN == G::BN, "update config");
   constexpr int BN = G::BN;
   constexpr int RING_T = G::STAGES * G::slab_mmaj(G::BM);  // only A streams (B is resident)
@@ -1007,7 +1010,7 @@ k_lu_apply_strip(LuApplyParams p) {
   constexpr int RING = RING_T > RING_U ? RING_T : RING_U;
   constexpr int AREA = RING + BN * kLcLd;
   static_assert(RING >= BN * kLcLd, "the pristine top rows fit in the ring");
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];  // the ring's first slot is a TMA destination
   double* ring = sm;
   double* Ts = sm + RING;                 // [BN][kLcLd] top rows after the moves, then top'
   double* Wt = Ts;                        // top' overwrites Ts once the product has read it
@@ -1022,6 +1025,12 @@ k_lu_apply_strip(LuApplyParams p) {
   const int* ipiv = reinterpret_cast<const int*>(p.side + size_t(ib) * nb);
   double* top = p.top;
   double* bot = ts ? p.bot : p.top;
+  __shared__ __align__(8) uint64_t tbar;  // the pristine top rows land by TMA (one phase per panel)
+  if (tid == 0) {
+    mbar_init(&tbar, 1);
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
 #ifdef HG_PANEL_STAMPS
   const int q = blockIdx.x == 0 && p.stamp ? 0 : -1;  // tools/ssssm_ab.cu phase stamps (CTA 0 of one task)
 #endif
@@ -1062,12 +1071,15 @@ k_lu_apply_strip(LuApplyParams p) {
     }
     __syncthreads();
     const int nbd = n_bd;
-    double* Pt = ring;  // [BN][kLcLd] pristine top rows (the ring is idle until the top' product)
-    for (int e = tid; e < (sb / 2) * BN; e += G::THREADS) {
-      const int c = e / (sb / 2), r = (e % (sb / 2)) * 2;
-      cp_async16(Pt + c * kLcLd + r, top + size_t(n0 + c) * nb + ii + r);
+    // pristine top rows [ii, ii + 128) x [n0, n0 + BN): ONE tensor-map TMA box into the idle ring
+    // (dense [BN][128]); it lands while the bot-sourced slots are gathered below
+    constexpr int kPt = kLuMaxSb;
+    double* Pt = ring;
+    if (tid == 0) {
+      fence_proxy_async_smem();  // the ring's generic-proxy reads of the previous panel come first
+      mbar_arrive_tx(&tbar, unsigned(BN * kPt * sizeof(double)));
+      tma_load_2d(Pt, &p.top_map, ii, n0, &tbar);
     }
-    cp_async_commit();
     {
       const int sc = slot_src[tid];
       if (sc >= 0) {  // BN loads in flight, one bot row across the strip's columns
@@ -1078,18 +1090,18 @@ k_lu_apply_strip(LuApplyParams p) {
         for (int c = 0; c < BN; ++c) Ts[c * kLcLd + tid] = v[c];
       }
     }
-    cp_async_wait<0>();
+    mbar_wait(&tbar, unsigned(P - p.p0) & 1u);
     __syncthreads();
     {
       const int sc = slot_src[tid];
       if (sc < 0) {
 #pragma unroll 8
-        for (int c = 0; c < BN; ++c) Ts[c * kLcLd + tid] = Pt[c * kLcLd + (-1 - sc)];
+        for (int c = 0; c < BN; ++c) Ts[c * kLcLd + tid] = Pt[c * kPt + (-1 - sc)];
       }
       if (tid < nbd) {
         const int r = bd_row[tid], k = bd_slot[tid];
 #pragma unroll 8
-        for (int c = 0; c < BN; ++c) __stcg(bot + size_t(n0 + c) * nb + r, Pt[c * kLcLd + k]);
+        for (int c = 0; c < BN; ++c) __stcg(bot + size_t(n0 + c) * nb + r, Pt[c * kPt + k]);
       }
     }
     __syncthreads();
@@ -1214,11 +1226,41 @@ static void push_apply(std::vector<LaunchDesc>& out, const LuApplyParams& ap) { 
 static bool use_strip_apply(int nb, int ib) { return ib == kLuMaxSb && nb % 128 == 0; }
 
 // Panels [P0, P1) applied to columns [col0, nb) by the strip kernel.
-static void push_apply_strip(std::vector<LaunchDesc>& out, const double* L, const double* side, double* top,
+// The TMA tensor map of a tile's top rows: nb x nb column-major doubles, boxes of 128 rows x bn columns
+// (cuTensorMapEncodeTiled through the runtime's driver entry point: no -lcuda link).
+static bool top_rows_map(CUtensorMap* m, const double* tile, int nb, int bn) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) {
+    set_error("cuTensorMapEncodeTiled is not available from the driver");
+    return false;
+  }
+  const cuuint64_t dims[2] = {cuuint64_t(nb), cuuint64_t(nb)};
+  const cuuint64_t strides[1] = {cuuint64_t(nb) * sizeof(double)};
+  const cuuint32_t box[2] = {cuuint32_t(kLuMaxSb), cuuint32_t(bn)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(tile), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(top rows, nb=%d, bn=%d) failed: %d", nb, bn, int(r));
+    return false;
+  }
+  return true;
+}
+
+static bool push_apply_strip(std::vector<LaunchDesc>& out, const double* L, const double* side, double* top,
                              double* bot, int nb, int ib, int P0, int P1, int col0, int mode, int bn,
                              const PushList* push = nullptr) {
   LuApplyParams ap{L, side, top, bot, nb, ib, P0, P1, col0, mode, 0};
   if (push) ap.push = *push;
+  if (!top_rows_map(&ap.top_map, top, nb, bn)) return false;
   LaunchDesc d;
   const int ncols = nb - col0;
   if (bn == 16)
@@ -1228,25 +1270,24 @@ static void push_apply_strip(std::vector<LaunchDesc>& out, const double* L, cons
     d.set((const void*)k_lu_apply_strip<CfgLS4w, true>, dim3(ncols / 32), dim3(CfgLS4w::THREADS),
           lu_apply_strip_smem<CfgLS4w>(), ap);
   out.push_back(d);
+  return true;
 }
 
-static void push_panel_apply(std::vector<LaunchDesc>& out, int ib, const double* L, const double* side,
+static bool push_panel_apply(std::vector<LaunchDesc>& out, int ib, const double* L, const double* side,
                              double* top, double* bot, int nb, int P, int col0, int mode) {
-  if (use_strip_apply(nb, ib)) {
-    push_apply_strip(out, L, side, top, bot, nb, ib, P, P + 1, col0, mode, 16);
-    return;
-  }
+  if (use_strip_apply(nb, ib)) return push_apply_strip(out, L, side, top, bot, nb, ib, P, P + 1, col0, mode, 16);
   LuApplyParams ap{L, side, top, bot, nb, ib, P, P + 1, col0, mode, 1};
   push_apply(out, ap);
   const int ii = P * ib;
   const bool ts = mode == LU_TSTRF;
   const int m0 = ts ? 0 : ii + ib;
   const int M = nb - m0, N = nb - col0;
-  if (M <= 0 || N <= 0) return;
+  if (M <= 0 || N <= 0) return true;
   GemmNNParams gp{L + size_t(ii) * nb + m0, top + size_t(col0) * nb + ii, bot + size_t(col0) * nb + m0, nb, nb, nb, ib};
   LaunchDesc d;
   d.set((const void*)k_gemm_nn, dim3(M / CfgN::BM, N / CfgN::BN), dim3(CfgN::THREADS), nn_smem(), gp);
   out.push_back(d);
+  return true;
 }
 
 bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>& out) {
@@ -1274,27 +1315,27 @@ bool build_lu_launches(int kind, const TaskOperands& o, std::vector<LaunchDesc>&
         else
           d.set(panel_kernel(nb, ib), dim3(kLuCl), dim3(kLuThreads), panel_smem(nb, ib), pp);
         out.push_back(d);
-        if (P + 1 < np)
-          push_panel_apply(out, ib, A, ts ? side(1) : side(0), ts ? o.t[0] : A, A, nb, P, (P + 1) * ib,
-                           ts ? LU_TSTRF : LU_GETRF);
+        if (P + 1 < np && !push_panel_apply(out, ib, A, ts ? side(1) : side(0), ts ? o.t[0] : A, A, nb, P,
+                                            (P + 1) * ib, ts ? LU_TSTRF : LU_GETRF))
+          return false;
       }
       return true;
     }
     case K_GESSM:
       if (use_strip_apply(nb, ib)) {
         const PushList pl = resolve_push(o, false);
-        push_apply_strip(out, o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF, 32, &pl);
-        return true;
+        return push_apply_strip(out, o.t[0], side(0), o.t[1], o.t[1], nb, ib, 0, np, 0, LU_GETRF, 32, &pl);
       }
-      for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[1], nb, P, 0, LU_GETRF);
+      for (int P = 0; P < np; ++P)
+        if (!push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[1], nb, P, 0, LU_GETRF)) return false;
       return true;
     case K_SSSSM:
       if (use_strip_apply(nb, ib)) {
         const PushList pl = resolve_push(o, false);
-        push_apply_strip(out, o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF, 32, &pl);
-        return true;
+        return push_apply_strip(out, o.t[0], side(0), o.t[1], o.t[2], nb, ib, 0, np, 0, LU_TSTRF, 32, &pl);
       }
-      for (int P = 0; P < np; ++P) push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[2], nb, P, 0, LU_TSTRF);
+      for (int P = 0; P < np; ++P)
+        if (!push_panel_apply(out, ib, o.t[0], side(0), o.t[1], o.t[2], nb, P, 0, LU_TSTRF)) return false;
       return true;
     default:
       set_error("kind %d is not an LU kind", kind);
