@@ -56,6 +56,27 @@ def test_geqrt_unmqr_tiles(nb):
     assert _rel(host_tile(tc, nb), rc) < TOL
 
 
+@pytest.mark.parametrize("scale", [1e-9, 1e-4])
+def test_tsqrt_norm_downdate_fallback(scale):
+    """TSQRT downdates ||B(:, c)||^2 through each reflector instead of exchanging it per column;
+    a B that is tiny against R makes every downdate cancel, so each column must take the exact
+    (message) path: the factor still matches LAPACK dtpqrt at 1e-12."""
+    from gpu_util import dev_tile, host_tile, tile_run
+
+    nb, ib = 512, 128
+    rng = np.random.default_rng(17)
+    r = np.asfortranarray(np.triu(rng.uniform(-0.5, 0.5, (nb, nb))) + np.eye(nb))
+    a = np.asfortranarray(scale * rng.uniform(-0.5, 0.5, (nb, nb)))
+    sd = side_doubles(nb, ib)
+    tr, ta = dev_tile(r, sd), dev_tile(a, sd)
+    tile_run(KIND["TSQRT"], [tr, ta], nb, ib)
+    rr, ra = r.copy(order="F"), a.copy(order="F")
+    t_ref = LQ.tsqrt(rr, ra, ib)
+    assert _rel(np.triu(host_tile(tr, nb)), np.triu(rr)) < TOL
+    assert _rel(host_tile(ta, nb), ra) < TOL
+    assert _rel(t_of(ta, nb, ib), np.triu(t_ref) if t_ref.shape == (ib, nb) else t_ref) < 1e-11
+
+
 @pytest.mark.parametrize("nb", [512, 1024])
 def test_tsqrt_tsmqr_tiles(nb):
     from gpu_util import dev_tile, host_tile, tile_run

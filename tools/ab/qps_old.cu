@@ -7,7 +7,7 @@
 #include <cstdlib>
 #include <vector>
 
-#include "../paper_1402_6601_b200/csrc/tiles_qr.cu"
+#include "tiles_qr_old.cu"
 
 namespace hg {
 void set_error(const char* fmt, ...) {

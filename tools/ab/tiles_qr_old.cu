@@ -30,9 +30,6 @@ namespace hg {
 constexpr int kQrCl = 8;
 constexpr int kQrThreads = 256;
 constexpr int kQrMaxSb = 128;
-// TSQRT column norms are downdated through each reflector (||[R(j,c); B(:,c)]|| is invariant);
-// a downdate that cancels more than this fraction is redone exactly (the message exchange)
-constexpr double kQrDowndateTol = 0.25;
 
 enum { QR_GEQRT = 0, QR_TSQRT = 1 };
 
@@ -138,9 +135,6 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
   // of the cluster's SMs inside the DAG: staging the T columns / R rows too cost 5% of QR C4.)
   double* slotAll = ph + 2 * kQrMaxSb;    // [2][kQrCl][2] norm^2 partial, alpha
   double* pwAll = slotAll + 2 * kQrCl * 2;                // [2][kQrCl][sb] partial x^T [V | A]
-  double* npart = pwAll + 2 * kQrCl * kQrMaxSb;           // [sb] TSQRT: this CTA's ||B(:, c)||^2 at panel start
-  double* xn2all = npart + kQrMaxSb;                      // [sb] TSQRT: ||B(:, c)||^2, downdated per column
-  int* stale = reinterpret_cast<int*>(xn2all + kQrMaxSb); // [sb] TSQRT: downdate cancelled, recompute exactly
   __shared__ double s_red[kQrThreads / 32];
   __shared__ double s_tau, s_beta, s_scal;
   // the two per-column exchanges are st.async messages completing on the receiver's mbarriers
@@ -154,34 +148,11 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     int gr = row0 + r;
     s[c * LD + r] = (ts || gr >= ii) ? A[size_t(ii + c) * nb + gr] : 0.0;
   }
-  if (ts) {  // TSQRT: every column's ||B(:, c)||^2 once (this CTA's rows); the column loop downdates them
-    __syncthreads();
-    const int c = tid % kQrMaxSb, half = tid / kQrMaxSb;
-    if (c < sb) {
-      const int rb = half * (R / 2), re = rb + R / 2;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* sc = s + c * LD;
-      for (int r = rb; r < re; r += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] = fma(sc[r + u], sc[r + u], acc[u]);
-      }
-      ph[half * kQrMaxSb + c] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-    }
-    __syncthreads();
-    if (tid < sb) npart[tid] = ph[tid] + ph[kQrMaxSb + tid];
-  }
   if (tid == 0) {
     for (int b = 0; b < 4; ++b) mbar_init(&bars[b], 1);
     fence_mbar_init_cluster();
   }
-  cl.sync();  // every CTA's barriers exist before the first message (and its norm partials are written)
-  if (ts && tid < sb) {  // the same sum, in the same order, in every CTA: the downdates stay cluster-uniform
-    double t = 0.0;
-#pragma unroll
-    for (int q2 = 0; q2 < kQrCl; ++q2) t += cl.map_shared_rank(npart, q2)[tid];
-    xn2all[tid] = t;
-    stale[tid] = 0;
-  }
+  cl.sync();  // every CTA's barriers exist before the first message
 
   // partial ||x||^2 of column jj over my rows strictly below the diagonal row
   auto publish_norm = [&](int jj, int par, double rpre) {
@@ -207,41 +178,25 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     }
   };
 
-  // TSQRT without a norm message: only R row j is staged (the norm comes from xn2all)
-  auto stage_rrow = [&](int par, double rpre) {
-    if (tid < kQrMaxSb) rrow[par * kQrMaxSb + tid] = rpre;
-    __syncthreads();
-  };
   HG_STAMP(0);
-  const double rpre0 = (ts && tid < sb) ? p.R[size_t(ii + tid) * nb + ii] : 0.0;
-  if (ts) stage_rrow(0, rpre0);
-  else publish_norm(0, 0, rpre0);
-  int nph0 = 0, nph1 = 0;  // completed phases of the two norm-message barriers (columns that exchanged)
+  publish_norm(0, 0, (ts && tid < sb) ? p.R[size_t(ii + tid) * nb + ii] : 0.0);
   for (int jj = 0; jj < sb; ++jj) {
     const int j = ii + jj;
     const int par = jj & 1;
-    const bool exact = !ts || stale[jj];  // cluster-uniform
-#ifdef HG_PANEL_STAMPS  // tools/qr_panel_stamps.cu: how many TSQRT columns took the exact (message) norm
-    if (exact && ts && tid == 0 && q == 0) atomicAdd(&g_panel_stamps[0][500], 1ull);
-#endif
     if (jj < 16) HG_STAMP(300 + 8 * jj);
     if (jj < 16) HG_STAMP(301 + 8 * jj);
     if (tid < 32) {
+      mbar_wait_cluster(&bars[par], (jj >> 1) & 1);  // the 8 (norm^2, alpha) messages of column jj
       double xn2 = 0.0, al = 0.0;
-      if (exact) {
-        mbar_wait_cluster(&bars[par], (par ? nph1 : nph0) & 1);  // the 8 (norm^2, alpha) messages of column jj
-        if (tid < kQrCl) {
-          const double* sl = slotAll + (par * kQrCl + tid) * 2;
-          xn2 = sl[0];
-          al = sl[1];  // only the owner of row j publishes a non-zero alpha
-        }
+      if (tid < kQrCl) {
+        const double* sl = slotAll + (par * kQrCl + tid) * 2;
+        xn2 = sl[0];
+        al = sl[1];  // only the owner of row j publishes a non-zero alpha
+      }
 #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-          xn2 += __shfl_xor_sync(0xffffffffu, xn2, o);
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-        }
-      } else {
-        xn2 = xn2all[jj];
+      for (int o = 4; o > 0; o >>= 1) {
+        xn2 += __shfl_xor_sync(0xffffffffu, xn2, o);
+        al += __shfl_xor_sync(0xffffffffu, al, o);
       }
       // dlarfg: beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha) / beta, x *= 1 / (alpha - beta).
       // Lanes 0..7 hold the reduced (xn2, alpha); the two divisions run on different lanes, and
@@ -259,7 +214,6 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
         s_scal = 1.0;
       }
     }
-    if (exact) (par ? nph1 : nph0) += 1;
     __syncthreads();
     const double tau = s_tau, beta = s_beta, scal = s_scal;
     if (jj < 16) HG_STAMP(302 + 8 * jj);
@@ -325,13 +279,6 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
       }
       if (ts && c > jj) t += rrow[par * kQrMaxSb + c];  // the unit of v_j sits in R row j
       wv[c] = t;
-      if (ts && c > jj) {  // H_j keeps ||[R(j, c); B(:, c)]||: ||B'(:, c)||^2 = ||B(:, c)||^2 + R(j, c)^2 - R'(j, c)^2
-        const double r0 = rrow[par * kQrMaxSb + c], r1 = r0 - tau * t;
-        const double tot = xn2all[c] + r0 * r0;
-        const double nw = tot - r1 * r1;
-        xn2all[c] = nw;
-        if (!(nw > kQrDowndateTol * tot)) stale[c] = 1;
-      }
     }
     __syncthreads();
     if (jj < 16) HG_STAMP(305 + 8 * jj);
@@ -373,10 +320,7 @@ __global__ void __cluster_dims__(kQrCl, 1, 1) __launch_bounds__(kQrThreads) k_qr
     }
     __syncthreads();
     if (jj < 16) HG_STAMP(306 + 8 * jj);
-    if (jj + 1 < sb) {
-      if (!ts || stale[jj + 1]) publish_norm(jj + 1, par ^ 1, rnext);
-      else stage_rrow(par ^ 1, rnext);
-    }
+    if (jj + 1 < sb) publish_norm(jj + 1, par ^ 1, rnext);
   }
   __syncthreads();
   for (int e = tid; e < sb * R; e += kQrThreads) {
@@ -553,8 +497,7 @@ static unsigned qr_panel_smem(int nb, int sb) {
   // the column loop's buffers follow the panel s[sb][R+1]; the end-of-panel T scratch
   // (qr_t_from_y, CTA 0) reuses the same region once they are dead
   const int R = nb / kQrCl;
-  const size_t loop = size_t(sb) * (R + 1) + 6 * kQrMaxSb + 2 * kQrCl * 2 + 2 * kQrCl * kQrMaxSb + 2 * kQrMaxSb +
-                      kQrMaxSb / 2;
+  const size_t loop = size_t(sb) * (R + 1) + 6 * kQrMaxSb + 2 * kQrCl * 2 + 2 * kQrCl * kQrMaxSb;
   const size_t t = size_t(sb) * (sb + 1) + sb + 7 * 256;
   return unsigned((loop > t ? loop : t) * sizeof(double));
 }
