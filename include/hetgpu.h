@@ -167,10 +167,12 @@ typedef struct hg_exec_plan {
   const int8_t* acc_mode;     /* HG_ACCESS_* per access (CSR like acc_block) */
   const int32_t* job_stage_job; /* host-staged route: the job whose first leg stages the block, or -1 */
   int32_t p2p;                /* 0: every GPU->GPU job is host-staged (GPU->host->GPU, platform.py:117) */
-  int32_t push;               /* 1: producer-push fusion -- a peer job moving a version written by a
-                                 POTRF / TRSM / SYRK / GEMM task is done by that task's own kernels
-                                 (epilogue stores into the consumer GPU's slot), not a copy node;
-                                 bytes per (version, destination) stay the plan's */
+  int32_t push;               /* 1: producer-push fusion -- a peer job moving a tile version is done by
+                                 the producing task's own kernels (stores into the consumer GPU's slot:
+                                 store epilogues of POTRF / TRSM / SYRK / GEMM, each column strip of the
+                                 LU / QR trailing updates, the last panel kernel of the LU / QR panels
+                                 with the side area), not a copy node; at most 8 (GPU, block) pairs per
+                                 task; bytes per (version, destination) stay the plan's */
 } hg_exec_plan;
 
 typedef struct hg_exec_opts {

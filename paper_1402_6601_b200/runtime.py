@@ -168,9 +168,9 @@ class Executor:
         self.graph = graph
         self.platform = platform
         self.trace = bool(trace)
-        # producer-push fusion: peer jobs of POTRF/TRSM/SYRK/GEMM outputs are
-        # stored into the consumer GPU's slot by the producing kernel instead of a copy node
-        self.push = bool(push) and os.environ.get("HG_PUSH", "1") != "0"
+        # producer-push fusion: peer jobs of tile versions are stored into the
+        # consumer GPU's slot by the producing task's kernels instead of a copy node (every kind)
+        self.push = bool(push)
         self.devices = devices
         # node priorities from the plan's own predicted durations (end - start):
         # changes only which ready kernel gets SMs first, never the plan
