@@ -174,7 +174,6 @@ class Executor:
         self.devices = devices
         # node priorities from the plan's own predicted durations (end - start):
         # changes only which ready kernel gets SMs first, never the plan
-        priority_levels = int(os.environ.get("HG_PRIORITY_LEVELS", priority_levels))
         self.task_weight = np.ascontiguousarray(np.asarray(plan.end, np.float64) - np.asarray(plan.start, np.float64))
         # host-staged routes (p2p=False, platform.py:117): GPU->host->GPU moves stage through
         # a page-locked image with the host image's layout (hg_matrix_register, released by close)
